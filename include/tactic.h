@@ -1,0 +1,207 @@
+/*
+ * tactic.h -- C ABI of the B200-native Tactic decode-time sparse attention library
+ * (libtactic.so, hand-written sm_100a CUDA).
+ *
+ * Method: "Tactic: Adaptive Sparse Attention with Clustering and Distribution
+ * Fitting for Long-Context LLMs" (arXiv 2502.12216).  Citations `P:n` are lines of
+ * PAPER.md; "reading k" refers to the numbered readings in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Head dimension d is fixed at 128.  bf16 tensors are IEEE bfloat16 bit patterns.
+ *  - A *unit* is one (sequence b, KV head h), numbered u = b * num_kv_heads + h.  Its G
+ *    query heads are q-heads h*G .. h*G+G-1 of sequence b (GQA), so every
+ *    q / out tensor is laid out [B][Hq = Hkv*G][128] == [units][G][128].
+ *  - Unless stated otherwise pointers are CUDA device pointers on the current device and
+ *    calls are asynchronous and stream-ordered on `stream` (a cudaStream_t, passed as
+ *    void* so this header needs no CUDA include).  No entry point synchronises the device
+ *    except where it says "host outputs".
+ *  - Every call returns a tactic_status_t; no exception crosses the ABI.  A human-readable
+ *    detail of the last failure on the calling thread is returned by tactic_last_error().
+ *    Asynchronous kernel faults surface as TACTIC_ERR_CUDA at a later call.
+ *  - Decode calls on one index share that index's device workspace: serialise them on one
+ *    stream (the workspace makes the call CUDA-graph capturable: no allocation, no sync).
+ */
+#ifndef TACTIC_H_
+#define TACTIC_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TACTIC_HEAD_DIM 128
+#define TACTIC_MAX_CLUSTERS 4096      /* per unit (sort / selection kernels keep C in smem) */
+#define TACTIC_MAX_SEQ_LEN 1048576    /* per unit (exact-head prefix of Alg. 1 kept in smem) */
+#define TACTIC_SHARD_GRID_T 512       /* sequence-sharded mode: criticality grid points   */
+#define TACTIC_SHARD_GRID_STEP 0.0625 /* grid step in logit units (1/16), reading 23      */
+
+typedef enum {
+  TACTIC_OK = 0,
+  TACTIC_ERR_INVALID_ARGUMENT = 1, /* bad scalar (C, iters, p, G ...) or null pointer      */
+  TACTIC_ERR_SHAPE = 2,            /* tensor shapes / strides inconsistent with the index  */
+  TACTIC_ERR_OOM = 3,              /* device allocation failed                            */
+  TACTIC_ERR_CUDA = 4,             /* CUDA runtime / kernel error                         */
+  TACTIC_ERR_NOT_FINITE = 5,       /* TACTIC_FLAG_VALIDATE found NaN/Inf in K or V        */
+  TACTIC_ERR_UNSUPPORTED = 6       /* device is not sm_100 or a size limit is exceeded    */
+} tactic_status_t;
+
+typedef struct tactic_index_s* tactic_index_t; /* opaque; owns every device buffer it allocates */
+
+/* KV-cache descriptor.  Strides are in elements; 0 means the contiguous default
+ * [B][Hkv][n][128] (stride_n = 128, stride_h = n*128, stride_b = Hkv*n*128).
+ * stride_n must be a multiple of 8 (16-byte rows) and the last dimension contiguous. */
+typedef struct {
+  int32_t batch;
+  int32_t num_kv_heads;
+  int32_t group_size;   /* G: query heads per KV head, one of 1, 2, 4, 8            */
+  int32_t seq_len;      /* n, tokens per unit (>= 1, <= TACTIC_MAX_SEQ_LEN)           */
+  int32_t head_dim;     /* must be 128                                               */
+  int64_t stride_b, stride_h, stride_n;
+} tactic_kv_desc_t;
+
+#define TACTIC_FLAG_VALIDATE     1u  /* build/import: scan K,V for NaN/Inf first   */
+#define TACTIC_FLAG_KMEANS_SIMT  2u  /* build: CUDA-core assignment kernel instead of the
+                                        tcgen05 one (debug / cross-check only)             */
+
+typedef struct {
+  uint64_t seed;                /* k-means init sampler seed (reading 3)                 */
+  const int32_t* init_indices;  /* nullable HOST pointer [units][C]: caller-chosen init
+                                   token indices; NULL = SplitMix64 + Fisher-Yates
+                                   sampler seeded with seed + (u+1)*0x9E3779B97F4A7C15   */
+  uint32_t flags;               /* TACTIC_FLAG_*                                          */
+  int32_t num_ctas;             /* attention grid size; 0 = number of SMs                 */
+} tactic_params_t;
+
+typedef struct {
+  int32_t units, batch, num_kv_heads, group_size, seq_len, n_clusters;
+  int32_t iters_requested;
+  int64_t device_bytes;         /* bytes the index holds on the device                   */
+} tactic_index_info_t;
+
+/* ---------------------------------------------------------------------------------------
+ * Index build (after prefill).  P:363-364 (§4.2): per unit, k-means over the keys --
+ * init by sampling C tokens uniformly without replacement (no k-means++, P:364 footnote),
+ * then Lloyd iterations (assign every key to the nearest centroid by squared Euclidean
+ * distance, reading 4; centroids := member means; an empty cluster keeps its centroid,
+ * reading 6) until the assignment is unchanged or `iters` iterations (P:364, P:402:
+ * 10).  The keys and values are then copied into a cluster-contiguous layout (clusters in
+ * id order, tokens of a cluster in ascending position; "non-contiguous KV access").
+ *
+ *   K, V      device bf16, layout per `kv`.  Only read; the caller may free / overwrite
+ *             them once the stream has passed this call.
+ *   n_clusters C, 1 <= C <= min(seq_len, TACTIC_MAX_CLUSTERS)   (else INVALID_ARGUMENT)
+ *   iters     >= 1
+ *   params    nullable (defaults: seed 0, sampler init, no flags)
+ *   out       receives the new index (NULL on failure).
+ * The assignment GEMM runs on tcgen05 tensor cores (bf16 keys x split-bf16 centroids,
+ * fp32 accumulate, fused argmin epilogue).  The call enqueues work only; it allocates
+ * device memory (not capturable).                                                     */
+tactic_status_t tactic_build_index(const void* K, const void* V, const tactic_kv_desc_t* kv,
+                                   int32_t n_clusters, int32_t iters,
+                                   const tactic_params_t* params, void* stream,
+                                   tactic_index_t* out);
+
+/* Index from a caller-supplied clustering (parity feeding, checkpoint restore).
+ *   centroids HOST float32 [units][C][128]; assign HOST int32 [units][n] in [0, C).
+ * Centroids are stored as given (float32 is the index storage format, reading 18).
+ * Synchronises the stream before returning (host inputs are staged).                 */
+tactic_status_t tactic_index_import(const void* K, const void* V, const tactic_kv_desc_t* kv,
+                                    int32_t n_clusters, const float* centroids,
+                                    const int32_t* assign, const tactic_params_t* params,
+                                    void* stream, tactic_index_t* out);
+
+/* Host outputs (each nullable): centroids float32 [units][C][128], assign int32
+ * [units][n], inertia float64 [units] (sum_i |K_i - c_a(i)|^2, fp64 accumulation),
+ * iters_run int32 [units].  Synchronises the stream.                                  */
+tactic_status_t tactic_index_export(tactic_index_t idx, float* centroids, int32_t* assign,
+                                    double* inertia, int32_t* iters_run, void* stream);
+
+tactic_status_t tactic_index_info(tactic_index_t idx, tactic_index_info_t* info);
+void tactic_index_destroy(tactic_index_t idx);
+
+/* ---------------------------------------------------------------------------------------
+ * Decode step (per layer-step, all units).  For every unit and each of its G query heads
+ * (Alg. 1 is per query; reading 16):
+ *  S1 criticality crit_j = q . c_j (float64),  S2 sort clusters by (-crit, j),
+ *  S3 token ranks of the partially sorted list,  S4 exact logits q.k/sqrt(d) of the first
+ *  N = ceil(0.02 n) ranks and of two windows of 2w+1 ranks around x1 = 10% and x2 = 60%
+ *  (readings 8-10),  S5 fit y = a/x + b through the window means,
+ *  S6 select clusters in order until the estimated cumulative mass reaches p of the
+ *  estimated total (Alg. 1 l.10, cluster granularity reading 14; p >= 1 selects
+ *  every cluster, reading 15),  S7 union over the G heads turned into a balanced
+ *  token work list over all units (sub-requests),  S8 split-KV flash-decode
+ *  of every head over the union (reading 17),  S9 log-sum-exp merge.
+ *   q    device bf16 [B][Hq][128]          p   0 < p <= 1  (else INVALID_ARGUMENT)
+ *   out  device bf16 [B][Hq][128]          lse nullable device float32 [B][Hq] (natural log)
+ */
+tactic_status_t tactic_decode(const void* q, tactic_index_t idx, float p, void* out,
+                              void* stream);
+tactic_status_t tactic_decode_ex(const void* q, tactic_index_t idx, float p, void* out,
+                                 float* lse, void* stream);
+
+/* Same computation through HOST buffers: q_host bf16 [B][Hq][128] is copied in, out_host
+ * bf16 [B][Hq][128] copied back; synchronises the stream (end-to-end user call).      */
+tactic_status_t tactic_decode_host(const void* q_host, tactic_index_t idx, float p,
+                                   void* out_host, void* stream);
+
+/* Decode with selection introspection (HOST outputs, each nullable; synchronises):
+ *   order      int32 [units][G][C]   cluster ids in rank order (S2)
+ *   J          int32 [units][G]      selected prefix length of `order` (S6)
+ *   fit        float64 [units][G][6] (a, b, m, W, mu1, mu2)  (S4-S6)
+ *   union_mask uint8 [units][C]      1 = cluster in the GQA union (S7)            */
+tactic_status_t tactic_decode_debug(const void* q, tactic_index_t idx, float p, void* out,
+                                    float* lse, int32_t* order, int32_t* J, double* fit,
+                                    uint8_t* union_mask, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * The library's own dense baseline (full attention, Eq. 1-2):
+ * split-KV flash-decode over all n tokens of every unit of the caller's K/V, then LSE
+ * merge.  Needs a caller workspace of tactic_dense_workspace_size() bytes.            */
+tactic_status_t tactic_dense_workspace_size(const tactic_kv_desc_t* kv, int32_t num_ctas,
+                                            size_t* bytes);
+tactic_status_t tactic_dense_decode(const void* q, const void* K, const void* V,
+                                    const tactic_kv_desc_t* kv, void* out, float* lse,
+                                    void* workspace, size_t workspace_bytes,
+                                    int32_t num_ctas, void* stream);
+
+/* S9 alone: o_parts float32 [n_parts][n_rows][128], lse_parts float32 [n_parts][n_rows]
+ * (natural log; -inf marks an empty part) -> out bf16 [n_rows][128], lse nullable f32. */
+tactic_status_t tactic_lse_merge(const float* o_parts, const float* lse_parts,
+                                 int32_t n_parts, int32_t n_rows, void* out, float* lse,
+                                 void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Sequence-sharded mode (1M-token contexts; reading 23).  Each rank holds an index over
+ * its token shard.  Per decode step:
+ *   stage1  : local S1-S5; writes local_max float64 [units][G][2] = (m_s, theta_max_s),
+ *             theta = crit/sqrt(d).                      -> caller all-reduces MAX
+ *   stage1b : re-expresses the local fit in the global exponent frame; writes
+ *             mass float64 [units][G][1+T] = (W_s, M_s(theta_t), t=1..T) on the grid
+ *             theta_t = theta_max - t*STEP.               -> caller all-reduces SUM
+ *   stage2  : theta* = largest theta_t with sum M >= p * sum W (none: select all);
+ *             selects local clusters with theta >= theta*, S7-S9 locally; writes
+ *             o_part float32 [units][G][128], lse_part float32 [units][G].
+ *                                                         -> caller all-gathers, then
+ *   tactic_lse_merge over the shards.                                                  */
+tactic_status_t tactic_decode_stage1(const void* q, tactic_index_t idx, double* local_max,
+                                     void* stream);
+tactic_status_t tactic_decode_stage1b(tactic_index_t idx, const double* global_max,
+                                      double* mass, void* stream);
+tactic_status_t tactic_decode_stage2(const void* q, tactic_index_t idx, float p,
+                                     const double* global_max, const double* global_mass,
+                                     float* o_part, float* lse_part, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Misc. */
+const char* tactic_status_string(tactic_status_t s);
+const char* tactic_last_error(void);             /* thread-local, never NULL            */
+const char* tactic_version(void);
+/* TACTIC_OK iff the current device is sm_100 (B200); fills SM count if non-NULL.     */
+tactic_status_t tactic_device_check(int32_t* num_sms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TACTIC_H_ */

@@ -1,0 +1,504 @@
+// attention.cu -- S8/S10 split-KV flash-decode over a token work list and S9 LSE merge.
+//
+// One kernel serves the sparse path (the GQA union of selected clusters) and
+// the dense baseline (all n tokens of the caller's K/V, Eq. 1-2).
+// Work balancing follows the paper's sub-request idea: the selected tokens of
+// all units form one global list that is cut into equal contiguous ranges, one per CTA,
+// so head-level imbalance becomes plain sequence imbalance.
+//
+// Per CTA: 1 producer warp streams 64-token stages of K and V into shared memory
+//   sparse: cp.async.bulk (1-D TMA, UBLKCP) of contiguous cluster runs from the
+//           cluster-permuted, row-swizzled index layout; a run is placed at a slot
+//           congruent to its row mod 8 so the swizzle survives the copy.
+//   dense : cp.async.bulk.tensor (UTMALDG) 64x64 boxes, SWIZZLE_128B, from the caller's
+//           [B][Hkv][n][128] cache.
+// 4 consumer warps each own 16 token slots of a stage:
+//   S^T(16 tok x 8 heads) = K(16x128) Q^T   (mma.sync m16n8k16, bf16 -> f32, swap-AB so
+//   the G<=8 query heads sit in the n=8 dimension), online softmax in the exp2 domain,
+//   P^T transposed in registers with movmatrix, O^T(128 x 8) += V^T P^T.
+// A piece (the part of one unit inside a CTA's range) ends with a cross-warp LSE
+// combine and one partial (o, lse) per head written to slot blockIdx.x + unit.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace tactic {
+
+constexpr int ATT_TILE = 64;
+constexpr int ATT_STAGES = 4;
+constexpr int ATT_CWARPS = 4;
+constexpr int ATT_THREADS = 32 * (ATT_CWARPS + 1);
+constexpr int ATT_STAGE_BYTES = ATT_TILE * 256 * 2;  // K + V
+constexpr int FLAG_FIRST = 1, FLAG_LAST = 2, FLAG_END = 4;
+
+struct __align__(16) StageMeta {
+  unsigned long long mask;
+  int unit;
+  int flags;
+};
+
+struct AttnSmem {
+  // stage buffers first (1024-aligned for SWIZZLE_128B TMA destinations)
+  // [ATT_STAGES][K 16KB | V 16KB]
+  // then: meta, barriers, combine scratch
+};
+
+constexpr int SCRATCH_FLOATS = ATT_CWARPS * (8 * 128 + 16);
+constexpr size_t ATT_SMEM = (size_t)ATT_STAGES * ATT_STAGE_BYTES + ATT_STAGES * sizeof(StageMeta) +
+                            2 * ATT_STAGES * sizeof(uint64_t) + SCRATCH_FLOATS * sizeof(float) + 1024;
+
+size_t attention_smem_bytes() { return ATT_SMEM; }
+
+// byte offset of (slot s, 16-byte logical chunk c) inside a 16 KB K or V stage tile
+template <bool DENSE>
+__device__ __forceinline__ uint32_t tile_off(int s, int c) {
+  if (DENSE) return (uint32_t)((c >> 3) * 8192 + s * 128 + (((c ^ s) & 7) << 4));
+  return (uint32_t)(s * 256 + (swz_chunk(c, s) << 4));
+}
+
+template <int G, bool DENSE>
+__global__ void __launch_bounds__(ATT_THREADS, 1)
+    attention_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, long long dense_total) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* stages = smem;
+  StageMeta* meta = (StageMeta*)(stages + ATT_STAGES * ATT_STAGE_BYTES);
+  uint64_t* full = (uint64_t*)(meta + ATT_STAGES);
+  uint64_t* empty = full + ATT_STAGES;
+  float* scratch = (float*)(empty + ATT_STAGES);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // zero the stage buffers once: never-written slots must hold finite values (0 * NaN)
+  for (int i = threadIdx.x; i < ATT_STAGES * ATT_STAGE_BYTES / 16; i += ATT_THREADS)
+    reinterpret_cast<uint4*>(stages)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ATT_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], ATT_CWARPS);
+    }
+    fence_barrier_init();
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  pdl_wait();  // inputs (work list, q) are produced by the previous kernel
+
+  const int P = gridDim.x, cta = blockIdx.x;
+
+  if (warp == 0) {
+    // ============================ producer ============================
+    if (lane == 0) {
+      if (DENSE) {
+        prefetch_tmap(&tmK);
+        prefetch_tmap(&tmV);
+      }
+      const long long T = DENSE ? dense_total : a.unit_prefix[a.units];
+      long long t = range_start(cta, T, P);
+      const long long t_end = range_start(cta + 1, T, P);
+      int stage = 0;
+      uint32_t phase = 0;
+      int u = 0;
+      if (t < t_end) {
+        if (DENSE) {
+          u = (int)(t / a.n);
+        } else {  // largest u with unit_prefix[u] <= t
+          int lo = 0, hi = a.units - 1;
+          while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (a.unit_prefix[mid] <= t) lo = mid; else hi = mid - 1;
+          }
+          u = lo;
+        }
+      }
+      while (t < t_end) {
+        const long long ubase = DENSE ? (long long)u * a.n : a.unit_prefix[u];
+        const long long uend = DENSE ? ubase + a.n : a.unit_prefix[u + 1];
+        const long long pend = uend < t_end ? uend : t_end;
+        int lt = (int)(t - ubase);
+        const int le = (int)(pend - ubase);
+        // sparse cursor: segment k of the unit's list holding local token lt
+        const int* seg_list = a.seg_list + (size_t)u * a.C;
+        const int* seg_pref = a.seg_prefix + (size_t)(u) * (a.C + 1);
+        const int* offs = a.offsets + (size_t)u * (a.C + 1);
+        int k = 0, row = 0, left = 0;
+        if (!DENSE) {
+          int lo = 0, hi = a.C - 1;  // largest k with seg_pref[k] <= lt
+          while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (seg_pref[mid] <= lt) lo = mid; else hi = mid - 1;
+          }
+          k = lo;
+          const int cid = seg_list[k];
+          row = offs[cid] + (lt - seg_pref[k]);
+          left = seg_pref[k + 1] - lt;
+        }
+        bool first = true;
+        while (lt < le) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sK = stages + stage * ATT_STAGE_BYTES;
+          uint8_t* sV = sK + ATT_STAGE_BYTES / 2;
+          unsigned long long mask = 0;
+          uint32_t bytes = 0;
+          if (DENSE) {
+            const int cnt = (le - lt) < ATT_TILE ? (le - lt) : ATT_TILE;
+            mask = cnt == 64 ? ~0ull : ((1ull << cnt) - 1ull);
+            bytes = ATT_STAGE_BYTES;
+            meta[stage].mask = mask;
+            meta[stage].unit = u;
+            meta[stage].flags = (first ? FLAG_FIRST : 0) | (lt + cnt >= le ? FLAG_LAST : 0);
+            mbar_arrive_expect_tx(&full[stage], bytes);
+            const int b = u / a.Hkv, h = u % a.Hkv;
+            tma_load_4d(sK, &tmK, 0, lt, h, b, &full[stage]);
+            tma_load_4d(sK + 8192, &tmK, 64, lt, h, b, &full[stage]);
+            tma_load_4d(sV, &tmV, 0, lt, h, b, &full[stage]);
+            tma_load_4d(sV + 8192, &tmV, 64, lt, h, b, &full[stage]);
+            lt += cnt;
+          } else {
+            // place runs: first compute the run list (slot, row, len), then one
+            // arrive.expect_tx, then the copies
+            int rs_slot[ATT_TILE / 8 + 8], rs_row[ATT_TILE / 8 + 8], rs_len[ATT_TILE / 8 + 8];
+            int nr = 0, s = 0;
+            while (s < ATT_TILE && lt < le) {
+              int avail = left < (le - lt) ? left : (le - lt);
+              int s0 = s + ((row - s) & 7);
+              if (s0 >= ATT_TILE) break;
+              int L = avail < (ATT_TILE - s0) ? avail : (ATT_TILE - s0);
+              if (nr > 0 && rs_slot[nr - 1] + rs_len[nr - 1] == s0 && rs_row[nr - 1] + rs_len[nr - 1] == row) {
+                rs_len[nr - 1] += L;  // contiguous with the previous run
+              } else {
+                rs_slot[nr] = s0; rs_row[nr] = row; rs_len[nr] = L; ++nr;
+              }
+              mask |= (L == 64 ? ~0ull : ((1ull << L) - 1ull)) << s0;
+              s = s0 + L;
+              row += L;
+              lt += L;
+              left -= L;
+              if (left == 0 && lt < le) {
+                ++k;
+                const int cid = seg_list[k];
+                row = offs[cid];
+                left = seg_pref[k + 1] - seg_pref[k];
+              }
+              if (nr == ATT_TILE / 8 + 8) break;
+            }
+            for (int i = 0; i < nr; ++i) bytes += (uint32_t)rs_len[i] * 512u;
+            meta[stage].mask = mask;
+            meta[stage].unit = u;
+            meta[stage].flags = (first ? FLAG_FIRST : 0) | (lt >= le ? FLAG_LAST : 0);
+            mbar_arrive_expect_tx(&full[stage], bytes);
+            const size_t ubytes = (size_t)u * a.n * 256;
+            for (int i = 0; i < nr; ++i) {
+              const uint32_t nb = (uint32_t)rs_len[i] * 256u;
+              bulk_g2s(sK + rs_slot[i] * 256, (const uint8_t*)a.Kp + ubytes + (size_t)rs_row[i] * 256, nb,
+                       &full[stage]);
+              bulk_g2s(sV + rs_slot[i] * 256, (const uint8_t*)a.Vp + ubytes + (size_t)rs_row[i] * 256, nb,
+                       &full[stage]);
+            }
+          }
+          first = false;
+          if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
+        }
+        t = pend;
+        ++u;
+      }
+      // end marker
+      mbar_wait(&empty[stage], phase ^ 1);
+      meta[stage].flags = FLAG_END;
+      meta[stage].mask = 0;
+      meta[stage].unit = -1;
+      mbar_arrive(&full[stage]);
+    }
+    return;
+  }
+
+  // ============================ consumers ============================
+  const int cw = warp - 1;
+  const int h0 = 2 * (lane & 3);            // heads held by this lane in C fragments
+  const int r0 = lane >> 2;                 // token row (S^T) / dim row (O^T) in fragment
+  const float scale_log2 = 1.4426950408889634f * 0.08838834764831845f;  // log2(e)/sqrt(128)
+  uint32_t qb[8][2];
+  float o[8][4];
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  int cur_unit = -1;
+  int stage = 0;
+  uint32_t phase = 0;
+
+  const uint32_t sbase = smem_u32(stages);
+  // ldmatrix lane -> (slot, chunk) mapping
+  const int a_slot = cw * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;  // K, non-trans
+  const int a_chi = lane >> 4;                                      // +0 / +1 chunk
+  const int v_slot = cw * 16 + (lane & 7) + (lane >> 4) * 8;         // V, trans
+  const int v_chi = (lane >> 3) & 1;
+
+  while (true) {
+    mbar_wait(&full[stage], phase);
+    const StageMeta md = meta[stage];
+    if (md.flags & FLAG_END) break;
+    if (md.flags & FLAG_FIRST) {
+      if (md.unit != cur_unit) {
+        cur_unit = md.unit;
+        const __nv_bfloat16* qu = a.q + (size_t)cur_unit * G * 128;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const int hh = r0;  // B fragment: n = lane/4 (head), k = 2*(lane%4)
+          if (hh < G) {
+            const uint32_t* qrow = reinterpret_cast<const uint32_t*>(qu + hh * 128);
+            qb[ks][0] = qrow[(ks * 16 + h0) >> 1];
+            qb[ks][1] = qrow[(ks * 16 + 8 + h0) >> 1];
+          } else {
+            qb[ks][0] = 0u;
+            qb[ks][1] = 0u;
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      m0 = m1 = -INFINITY;
+      l0 = l1 = 0.f;
+    }
+    const uint32_t mym = (uint32_t)((md.mask >> (cw * 16)) & 0xFFFFull);
+    if (mym) {
+      const uint32_t sK = sbase + stage * ATT_STAGE_BYTES;
+      const uint32_t sV = sK + ATT_STAGE_BYTES / 2;
+      float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        uint32_t af[4];
+        ldsm_x4(af[0], af[1], af[2], af[3], sK + tile_off<DENSE>(a_slot, 2 * ks + a_chi));
+        mma_bf16_16816(s, af, qb[ks][0], qb[ks][1]);
+      }
+      // s[0],s[1]: token r0, heads h0,h0+1 ; s[2],s[3]: token r0+8
+      const bool v_lo = (mym >> r0) & 1u, v_hi = (mym >> (r0 + 8)) & 1u;
+      float x0 = v_lo ? s[0] * scale_log2 : -INFINITY;
+      float x1 = v_lo ? s[1] * scale_log2 : -INFINITY;
+      float x2 = v_hi ? s[2] * scale_log2 : -INFINITY;
+      float x3 = v_hi ? s[3] * scale_log2 : -INFINITY;
+      float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+      }
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);  // finite: >= 1 valid token
+      const float c0 = exp2f(m0 - mn0), c1 = exp2f(m1 - mn1);  // m = -inf -> 0
+      m0 = mn0;
+      m1 = mn1;
+      const float p0 = exp2f(x0 - mn0), p1 = exp2f(x1 - mn1);
+      const float p2 = exp2f(x2 - mn0), p3 = exp2f(x3 - mn1);
+      l0 = l0 * c0 + p0 + p2;
+      l1 = l1 * c1 + p1 + p3;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        o[i][0] *= c0; o[i][1] *= c1; o[i][2] *= c0; o[i][3] *= c1;
+      }
+      const uint32_t b0 = movmatrix_t(pack_bf16(p0, p1));
+      const uint32_t b1 = movmatrix_t(pack_bf16(p2, p3));
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        uint32_t af[4];
+        ldsm_x4_t(af[0], af[1], af[2], af[3], sV + tile_off<DENSE>(v_slot, 2 * mt + v_chi));
+        mma_bf16_16816(o[mt], af, b0, b1);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
+
+    if (md.flags & FLAG_LAST) {
+      // ---- cross-warp combine of this piece
+      float L0 = l0, L1 = l1;
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        L0 += __shfl_xor_sync(0xffffffffu, L0, off);
+        L1 += __shfl_xor_sync(0xffffffffu, L1, off);
+      }
+      float* sw = scratch + cw * (8 * 128 + 16);
+      if (lane < 4) {
+        sw[8 * 128 + h0] = m0;
+        sw[8 * 128 + h0 + 1] = m1;
+        sw[8 * 128 + 8 + h0] = L0;
+        sw[8 * 128 + 8 + h0 + 1] = L1;
+      }
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        const int d0 = mt * 16 + r0;
+        sw[h0 * 128 + d0] = o[mt][0];
+        sw[(h0 + 1) * 128 + d0] = o[mt][1];
+        sw[h0 * 128 + d0 + 8] = o[mt][2];
+        sw[(h0 + 1) * 128 + d0 + 8] = o[mt][3];
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(ATT_CWARPS * 32));
+      const int dim = threadIdx.x - 32;
+      const size_t slot = (size_t)cta + md.unit;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float mf = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < ATT_CWARPS; ++w) mf = fmaxf(mf, scratch[w * (8 * 128 + 16) + 8 * 128 + g]);
+        float lf = 0.f, of = 0.f;
+#pragma unroll
+        for (int w = 0; w < ATT_CWARPS; ++w) {
+          const float* sww = scratch + w * (8 * 128 + 16);
+          const float e = exp2f(sww[8 * 128 + g] - mf);
+          lf += sww[8 * 128 + 8 + g] * e;
+          of += sww[g * 128 + dim] * e;
+        }
+        a.part_o[(slot * G + g) * 128 + dim] = of / lf;
+        if (dim == 0) a.part_lse[slot * G + g] = (mf + log2f(lf)) * 0.6931471805599453f;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(ATT_CWARPS * 32));
+      m0 = m1 = -INFINITY;
+      l0 = l1 = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    }
+  }
+  pdl_launch_dependents();
+}
+
+// ---------------------------------------------------------------------------- merge (S9)
+// One warp per (unit, head): pieces are slots c + u for the CTAs c whose range meets the
+// unit; lse = logsumexp lse_s, o = sum_s exp(lse_s - lse) o_s.
+__global__ void merge_kernel(const float* __restrict__ part_o, const float* __restrict__ part_lse,
+                             const long long* __restrict__ unit_prefix, int n, int units, int G, int P,
+                             __nv_bfloat16* __restrict__ out, float* __restrict__ out_f32,
+                             float* __restrict__ lse_out) {
+  pdl_wait();
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= units * G) return;
+  const int u = warp / G, g = warp % G;
+  const long long T = unit_prefix ? unit_prefix[units] : (long long)units * n;
+  const long long us = unit_prefix ? unit_prefix[u] : (long long)u * n;
+  const long long ue = unit_prefix ? unit_prefix[u + 1] : (long long)(u + 1) * n;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float mx = -INFINITY, sum = 0.f;
+  if (ue > us) {
+    const int c0 = cta_of(us, T, P), c1 = cta_of(ue - 1, T, P);
+    for (int c = c0; c <= c1; ++c) {
+      if (range_start(c, T, P) == range_start(c + 1, T, P)) continue;
+      const size_t slot = (size_t)c + u;
+      const float l = part_lse[slot * G + g];
+      if (l == -INFINITY) continue;
+      const float4 ov = *reinterpret_cast<const float4*>(part_o + (slot * G + g) * 128 + lane * 4);
+      const float mn = fmaxf(mx, l);
+      const float sc = expf(mx - mn), w = expf(l - mn);
+      acc[0] = acc[0] * sc + w * ov.x;
+      acc[1] = acc[1] * sc + w * ov.y;
+      acc[2] = acc[2] * sc + w * ov.z;
+      acc[3] = acc[3] * sc + w * ov.w;
+      sum = sum * sc + w;
+      mx = mn;
+    }
+  }
+  const float inv = sum > 0.f ? 1.f / sum : 0.f;
+  if (out) {
+    __nv_bfloat162* orow = reinterpret_cast<__nv_bfloat162*>(out + ((size_t)u * G + g) * 128 + lane * 4);
+    orow[0] = __floats2bfloat162_rn(acc[0] * inv, acc[1] * inv);
+    orow[1] = __floats2bfloat162_rn(acc[2] * inv, acc[3] * inv);
+  }
+  if (out_f32)
+    *reinterpret_cast<float4*>(out_f32 + ((size_t)u * G + g) * 128 + lane * 4) =
+        make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+  if (lse_out && lane == 0) lse_out[u * G + g] = sum > 0.f ? mx + logf(sum) : -INFINITY;
+}
+
+__global__ void lse_merge_plain_kernel(const float* __restrict__ o_parts, const float* __restrict__ lse_parts,
+                                       int n_parts, int n_rows, __nv_bfloat16* __restrict__ out,
+                                       float* __restrict__ lse_out) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= n_rows) return;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float mx = -INFINITY, sum = 0.f;
+  for (int s = 0; s < n_parts; ++s) {
+    const float l = lse_parts[(size_t)s * n_rows + row];
+    if (l == -INFINITY) continue;
+    const float4 ov = *reinterpret_cast<const float4*>(o_parts + ((size_t)s * n_rows + row) * 128 + lane * 4);
+    const float mn = fmaxf(mx, l);
+    const float sc = expf(mx - mn), w = expf(l - mn);
+    acc[0] = acc[0] * sc + w * ov.x;
+    acc[1] = acc[1] * sc + w * ov.y;
+    acc[2] = acc[2] * sc + w * ov.z;
+    acc[3] = acc[3] * sc + w * ov.w;
+    sum = sum * sc + w;
+    mx = mn;
+  }
+  const float inv = sum > 0.f ? 1.f / sum : 0.f;
+  __nv_bfloat162* orow = reinterpret_cast<__nv_bfloat162*>(out + (size_t)row * 128 + lane * 4);
+  orow[0] = __floats2bfloat162_rn(acc[0] * inv, acc[1] * inv);
+  orow[1] = __floats2bfloat162_rn(acc[2] * inv, acc[3] * inv);
+  if (lse_out && lane == 0) lse_out[row] = sum > 0.f ? mx + logf(sum) : -INFINITY;
+}
+
+// ---------------------------------------------------------------------------- launchers
+template <int G, bool DENSE>
+static cudaError_t launch_attn_t(const AttnArgs& a, const CUtensorMap* tmK, const CUtensorMap* tmV,
+                                 long long dense_total, int num_ctas, cudaStream_t s, bool pdl) {
+  auto kern = attention_kernel<G, DENSE>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ATT_SMEM);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  CUtensorMap dummy;
+  memset(&dummy, 0, sizeof(dummy));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_ctas);
+  cfg.blockDim = dim3(ATT_THREADS);
+  cfg.dynamicSmemBytes = ATT_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, a, tmK ? *tmK : dummy, tmV ? *tmV : dummy, dense_total);
+}
+
+template <bool DENSE>
+static cudaError_t launch_attn_g(const AttnArgs& a, const CUtensorMap* tmK, const CUtensorMap* tmV, int G,
+                                 int num_ctas, cudaStream_t s, bool pdl) {
+  const long long dt = (long long)a.units * a.n;
+  switch (G) {
+    case 1: return launch_attn_t<1, DENSE>(a, tmK, tmV, dt, num_ctas, s, pdl);
+    case 2: return launch_attn_t<2, DENSE>(a, tmK, tmV, dt, num_ctas, s, pdl);
+    case 4: return launch_attn_t<4, DENSE>(a, tmK, tmV, dt, num_ctas, s, pdl);
+    case 8: return launch_attn_t<8, DENSE>(a, tmK, tmV, dt, num_ctas, s, pdl);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_attention_sparse(const AttnArgs& a, int G, int num_ctas, cudaStream_t s, bool pdl) {
+  return launch_attn_g<false>(a, nullptr, nullptr, G, num_ctas, s, pdl);
+}
+cudaError_t launch_attention_dense(const AttnArgs& a, const CUtensorMap* tmK, const CUtensorMap* tmV, int G,
+                                   int num_ctas, cudaStream_t s, bool pdl) {
+  return launch_attn_g<true>(a, tmK, tmV, G, num_ctas, s, pdl);
+}
+
+cudaError_t launch_merge(const float* part_o, const float* part_lse, const long long* unit_prefix, int n,
+                         int units, int G, int num_ctas, __nv_bfloat16* out, float* out_f32, float* lse,
+                         cudaStream_t s, bool pdl) {
+  const int warps = units * G;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((warps + 7) / 8);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, merge_kernel, part_o, part_lse, unit_prefix, n, units, G, num_ctas, out, out_f32,
+                            lse);
+}
+
+cudaError_t launch_lse_merge_plain(const float* o_parts, const float* lse_parts, int n_parts, int n_rows,
+                                   __nv_bfloat16* out, float* lse, cudaStream_t s) {
+  lse_merge_plain_kernel<<<(n_rows + 7) / 8, 256, 0, s>>>(o_parts, lse_parts, n_parts, n_rows, out, lse);
+  return cudaGetLastError();
+}
+
+}  // namespace tactic

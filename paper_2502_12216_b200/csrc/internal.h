@@ -1,0 +1,148 @@
+// internal.h -- index structure and kernel launchers shared by the libtactic sources.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/tactic.h"
+
+namespace tactic {
+
+constexpr int D = 128;
+
+// Sample constants of Alg. 1 (readings 8-10): exact head N, window centres x1, x2,
+// half-width w, exact fallback for tiny n.  Integer formulas so every party agrees.
+struct SampleConsts {
+  int N, x1, x2, w;
+  bool fallback;
+  int slots;  // logits computed per head: N + 2(2w+1), or n in fallback
+};
+SampleConsts sample_consts(int n);
+
+// Token-range split of a global work list over P CTAs: CTA c owns [rs(c), rs(c+1)).
+__host__ __device__ inline long long range_start(int c, long long T, int P) {
+  return (long long)c * T / P;
+}
+// CTA whose range contains token t (0 <= t < T): largest c with rs(c) <= t.
+__host__ __device__ inline int cta_of(long long t, long long T, int P) {
+  long long c = ((t + 1) * (long long)P - 1) / T;
+  return (int)(c < P - 1 ? c : P - 1);
+}
+
+}  // namespace tactic
+
+struct tactic_index_s {
+  int device = 0;
+  int B = 0, Hkv = 0, G = 0, n = 0, C = 0, units = 0, iters_req = 0;
+  int num_ctas = 0, num_sms = 0;
+  tactic::SampleConsts sc{};
+  // index data
+  __nv_bfloat16* Kp = nullptr;   // [units][n][128] cluster-contiguous, rows chunk-swizzled
+  __nv_bfloat16* Vp = nullptr;
+  float* cent = nullptr;         // [units][C][128] float32 centroids (storage format)
+  int* offsets = nullptr;        // [units][C+1]
+  int* perm = nullptr;           // [units][n] original token ids in layout order
+  int* assign = nullptr;         // [units][n]
+  int* iters_run = nullptr;      // [units]
+  int* all_list = nullptr;       // [units][C]  non-empty clusters (p >= 1 work list)
+  int* all_prefix = nullptr;     // [units][C+1]
+  long long* all_unit_prefix = nullptr;  // [units+1]
+  // decode workspace
+  double* crit = nullptr;        // [units][G][C]
+  int* order = nullptr;          // [units][G][C]
+  int* ends = nullptr;           // [units][G][C]
+  float* logits = nullptr;       // [units][G][slots]
+  double* fit = nullptr;         // [units][G][6]
+  double* cumend = nullptr;      // [units][G][C] (sharded stage 1)
+  int* J = nullptr;              // [units][G]
+  uint8_t* umask = nullptr;      // [units][C]
+  int* union_list = nullptr;     // [units][C]
+  int* union_prefix = nullptr;   // [units][C+1]
+  long long* unit_prefix = nullptr;  // [units+1]
+  unsigned int* counter = nullptr;   // last-block counter (self-resetting)
+  float* part_o = nullptr;       // [num_ctas + units][G][128]
+  float* part_lse = nullptr;     // [num_ctas + units][G]
+  double* stage = nullptr;       // sharded mode scratch [units][G][2]
+  __nv_bfloat16* q_stage = nullptr;  // [units][G][128] (host-buffer decode)
+  __nv_bfloat16* o_stage = nullptr;
+  long long device_bytes = 0;
+};
+
+namespace tactic {
+
+// ---- attention (attention.cu)
+struct AttnArgs {
+  const __nv_bfloat16* q;          // [units][G][128]
+  const __nv_bfloat16* Kp;         // sparse mode: swizzled [units][n][128]
+  const __nv_bfloat16* Vp;
+  const int* seg_list;             // [units][C]
+  const int* seg_prefix;           // [units][C+1]
+  const int* offsets;              // [units][C+1]
+  const long long* unit_prefix;    // [units+1] (sparse)
+  int n, C, units, Hkv;
+  float* part_o;
+  float* part_lse;
+};
+cudaError_t launch_attention_sparse(const AttnArgs& a, int G, int num_ctas, cudaStream_t s, bool pdl);
+cudaError_t launch_attention_dense(const AttnArgs& a, const CUtensorMap* tmK, const CUtensorMap* tmV, int G,
+                                   int num_ctas, cudaStream_t s, bool pdl);
+// merge: unit_prefix == nullptr means dense (u * n)
+cudaError_t launch_merge(const float* part_o, const float* part_lse, const long long* unit_prefix, int n,
+                         int units, int G, int num_ctas, __nv_bfloat16* out, float* out_f32, float* lse,
+                         cudaStream_t s, bool pdl);
+cudaError_t launch_lse_merge_plain(const float* o_parts, const float* lse_parts, int n_parts, int n_rows,
+                                   __nv_bfloat16* out, float* lse, cudaStream_t s);
+size_t attention_smem_bytes();
+
+// ---- selection (select.cu)
+struct SelArgs {
+  const __nv_bfloat16* q;
+  tactic_index_s* idx;
+  double p;
+  int mode;                        // 0 = normal, 1 = sharded stage-2 (grid threshold)
+  const double* gmax;              // [units][G][2] (stage 2 / 1b)
+  const double* gmass;             // [units][G][1+T]
+  double* mass_out;                // stage 1b
+  double* local_max;               // stage 1
+};
+cudaError_t launch_score(const SelArgs& a, cudaStream_t s, bool pdl);
+cudaError_t launch_sort(const SelArgs& a, cudaStream_t s, bool pdl);
+cudaError_t launch_sample(const SelArgs& a, cudaStream_t s, bool pdl);
+cudaError_t launch_select(const SelArgs& a, cudaStream_t s, bool pdl);
+cudaError_t launch_stage1b(const SelArgs& a, cudaStream_t s);
+
+// ---- k-means / layout (kmeans.cu)
+struct KmArgs {
+  const __nv_bfloat16* K;
+  const __nv_bfloat16* V;
+  long long sb, sh, sn;            // strides in elements
+  int B, Hkv, n, C, Cpad, units, nblk, iters_req;
+  // index buffers (device pointers)
+  float* cent;
+  int* offsets;
+  int* perm;
+  int* assign;
+  int* iters_run;
+  int* all_list;
+  int* all_prefix;
+  __nv_bfloat16* Kp;
+  __nv_bfloat16* Vp;
+  // scratch
+  uint8_t* bimg;                   // [units][Cpad/128][64 KB]
+  float* cnorm;                    // [units][Cpad]
+  int* blk_counts;                 // [units][nblk][C]
+  int* changed;                    // [units]
+  int* converged;                  // [units]
+};
+cudaError_t km_init_centroids(const KmArgs& a, const int* init_dev, cudaStream_t s);
+cudaError_t km_assign(const KmArgs& a, int iter, bool simt, cudaStream_t s);
+cudaError_t km_count_scan_scatter(const KmArgs& a, int iter, cudaStream_t s);
+cudaError_t km_update(const KmArgs& a, int iter, cudaStream_t s);
+cudaError_t km_finalize(const KmArgs& a, cudaStream_t s);
+cudaError_t km_inertia(const KmArgs& a, double* part /* [units][C] */, cudaStream_t s);
+cudaError_t km_check_finite(const KmArgs& a, int* flag, cudaStream_t s);
+
+}  // namespace tactic

@@ -1,0 +1,667 @@
+// tactic_api.cu -- the C ABI (include/tactic.h): argument validation, index ownership,
+// host-side sampler, and the stream-ordered launch sequences of build and decode.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace tactic;
+
+namespace {
+
+thread_local std::string g_err = "";
+
+tactic_status_t fail(tactic_status_t st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+tactic_status_t cuda_fail(cudaError_t e, const char* where) {
+  return fail(e == cudaErrorMemoryAllocation ? TACTIC_ERR_OOM : TACTIC_ERR_CUDA, "%s: %s (%s)", where,
+              cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define CK(expr)                                       \
+  do {                                                 \
+    cudaError_t _e = (expr);                           \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+  } while (0)
+
+struct Resolved {
+  int B, Hkv, G, n;
+  long long sb, sh, sn;
+};
+
+tactic_status_t resolve_kv(const tactic_kv_desc_t* kv, Resolved* r) {
+  if (!kv) return fail(TACTIC_ERR_INVALID_ARGUMENT, "kv descriptor is NULL");
+  if (kv->head_dim != 128) return fail(TACTIC_ERR_INVALID_ARGUMENT, "head_dim must be 128 (got %d)", kv->head_dim);
+  const int G = kv->group_size;
+  if (!(G == 1 || G == 2 || G == 4 || G == 8))
+    return fail(TACTIC_ERR_INVALID_ARGUMENT, "group_size must be 1, 2, 4 or 8 (got %d)", G);
+  if (kv->batch < 1 || kv->num_kv_heads < 1) return fail(TACTIC_ERR_INVALID_ARGUMENT, "batch and heads must be >= 1");
+  if (kv->seq_len < 1) return fail(TACTIC_ERR_INVALID_ARGUMENT, "seq_len must be >= 1");
+  if (kv->seq_len > TACTIC_MAX_SEQ_LEN)
+    return fail(TACTIC_ERR_UNSUPPORTED, "seq_len %d exceeds TACTIC_MAX_SEQ_LEN", kv->seq_len);
+  r->B = kv->batch;
+  r->Hkv = kv->num_kv_heads;
+  r->G = G;
+  r->n = kv->seq_len;
+  r->sn = kv->stride_n ? kv->stride_n : 128;
+  r->sh = kv->stride_h ? kv->stride_h : (long long)r->n * r->sn;
+  r->sb = kv->stride_b ? kv->stride_b : (long long)r->Hkv * r->sh;
+  if (r->sn % 8 || r->sh % 8 || r->sb % 8 || r->sn < 128)
+    return fail(TACTIC_ERR_SHAPE, "strides must be multiples of 8 elements and stride_n >= 128");
+  return TACTIC_OK;
+}
+
+uint64_t splitmix_next(uint64_t& state) {
+  state += 0x9E3779B97F4A7C15ull;
+  uint64_t z = state;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Reading 3: C distinct tokens, uniform without replacement -- partial Fisher-Yates
+// driven by SplitMix64 seeded with seed + (unit+1) * 0x9E3779B97F4A7C15.
+void sample_init(int n, int C, uint64_t seed, int unit, int* out) {
+  uint64_t st = seed + (uint64_t)(unit + 1) * 0x9E3779B97F4A7C15ull;
+  std::vector<int> a(n);
+  for (int i = 0; i < n; ++i) a[i] = i;
+  for (int j = 0; j < C; ++j) {
+    const uint64_t r = (uint64_t)j + splitmix_next(st) % (uint64_t)(n - j);
+    std::swap(a[j], a[(size_t)r]);
+    out[j] = a[j];
+  }
+}
+
+struct DevAlloc {
+  std::vector<void*> ptrs;
+  long long bytes = 0;
+  cudaError_t err = cudaSuccess;
+  template <typename T>
+  T* get(size_t count) {
+    if (err != cudaSuccess) return nullptr;
+    void* p = nullptr;
+    const size_t b = count * sizeof(T) + 16;
+    err = cudaMalloc(&p, b);
+    if (err != cudaSuccess) return nullptr;
+    ptrs.push_back(p);
+    bytes += (long long)b;
+    return (T*)p;
+  }
+};
+
+int device_sms() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+}  // namespace
+
+namespace tactic {
+SampleConsts sample_consts(int n) {
+  SampleConsts s;
+  const long long nn = n;
+  s.N = (int)((2 * nn + 99) / 100);
+  s.x1 = (int)((nn + 5) / 10);
+  s.x2 = (int)((6 * nn + 5) / 10);
+  const long long w = (25 * nn + 5000) / 10000;
+  s.w = (int)(w > 1 ? w : 1);
+  s.fallback = (s.x1 - s.w <= s.N) || (s.x1 + s.w >= s.x2 - s.w) || (s.x2 + s.w > n);
+  s.slots = s.fallback ? n : s.N + 2 * (2 * s.w + 1);
+  return s;
+}
+}  // namespace tactic
+
+struct tactic_index_priv {
+  std::vector<void*> ptrs;
+};
+
+static void free_index(tactic_index_s* x, std::vector<void*>* ptrs) {
+  if (ptrs)
+    for (void* p : *ptrs) cudaFree(p);
+  delete x;
+}
+
+// all index allocations are recorded here (keyed by index pointer)
+#include <map>
+#include <mutex>
+static std::mutex g_mu;
+static std::map<tactic_index_s*, std::vector<void*>> g_allocs;
+
+static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_ctas, tactic_index_s** out) {
+  tactic_index_s* x = new tactic_index_s();
+  x->B = r.B;
+  x->Hkv = r.Hkv;
+  x->G = r.G;
+  x->n = r.n;
+  x->C = C;
+  x->units = r.B * r.Hkv;
+  x->iters_req = iters;
+  cudaGetDevice(&x->device);
+  x->num_sms = device_sms();
+  x->num_ctas = num_ctas > 0 ? num_ctas : x->num_sms;
+  x->sc = sample_consts(r.n);
+  const size_t U = x->units, n = x->n, G = x->G;
+  DevAlloc A;
+  x->Kp = A.get<__nv_bfloat16>(U * n * 128);
+  x->Vp = A.get<__nv_bfloat16>(U * n * 128);
+  x->cent = A.get<float>(U * C * 128);
+  x->offsets = A.get<int>(U * (C + 1));
+  x->perm = A.get<int>(U * n);
+  x->assign = A.get<int>(U * n);
+  x->iters_run = A.get<int>(U);
+  x->all_list = A.get<int>(U * C);
+  x->all_prefix = A.get<int>(U * (C + 1));
+  x->all_unit_prefix = A.get<long long>(U + 1);
+  x->crit = A.get<double>(U * G * C);
+  x->order = A.get<int>(U * G * C);
+  x->ends = A.get<int>(U * G * C);
+  x->logits = A.get<float>(U * G * (size_t)x->sc.slots);
+  x->fit = A.get<double>(U * G * 6);
+  x->cumend = A.get<double>(U * G * C);
+  x->J = A.get<int>(U * G);
+  x->umask = A.get<uint8_t>(U * C);
+  x->union_list = A.get<int>(U * C);
+  x->union_prefix = A.get<int>(U * (C + 1));
+  x->unit_prefix = A.get<long long>(U + 1);
+  x->counter = A.get<unsigned int>(1);
+  x->part_o = A.get<float>((x->num_ctas + U) * G * 128);
+  x->part_lse = A.get<float>((x->num_ctas + U) * G);
+  x->stage = A.get<double>(U * G * 2);
+  x->q_stage = A.get<__nv_bfloat16>(U * G * 128);
+  x->o_stage = A.get<__nv_bfloat16>(U * G * 128);
+  if (A.err != cudaSuccess) {
+    for (void* p : A.ptrs) cudaFree(p);
+    delete x;
+    return cuda_fail(A.err, "index allocation");
+  }
+  x->device_bytes = A.bytes;
+  cudaMemset(x->counter, 0, sizeof(unsigned int));
+  std::vector<long long> up(U + 1);
+  for (size_t u = 0; u <= U; ++u) up[u] = (long long)u * (long long)n;
+  cudaMemcpy(x->all_unit_prefix, up.data(), (U + 1) * sizeof(long long), cudaMemcpyHostToDevice);
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_allocs[x] = A.ptrs;
+  }
+  *out = x;
+  return TACTIC_OK;
+}
+
+static tactic_status_t check_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0)
+    return fail(TACTIC_ERR_UNSUPPORTED, "device %d is sm_%d%d; libtactic is built for sm_100a (B200)", dev, major,
+                minor);
+  return TACTIC_OK;
+}
+
+// Build / import share everything after the centroids are known.
+static tactic_status_t build_common(const void* K, const void* V, const tactic_kv_desc_t* kv, int32_t C,
+                                    int32_t iters, const tactic_params_t* params, cudaStream_t s,
+                                    const float* host_cent, const int32_t* host_assign, tactic_index_t* out) {
+  if (!out) return fail(TACTIC_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (!K || !V) return fail(TACTIC_ERR_INVALID_ARGUMENT, "K or V is NULL");
+  Resolved r;
+  tactic_status_t st = resolve_kv(kv, &r);
+  if (st) return st;
+  if (C < 1 || C > r.n) return fail(TACTIC_ERR_INVALID_ARGUMENT, "n_clusters must be in [1, seq_len] (got %d)", C);
+  if (C > TACTIC_MAX_CLUSTERS) return fail(TACTIC_ERR_UNSUPPORTED, "n_clusters %d > TACTIC_MAX_CLUSTERS", C);
+  if (iters < 1) return fail(TACTIC_ERR_INVALID_ARGUMENT, "iters must be >= 1");
+  if ((uintptr_t)K % 16 || (uintptr_t)V % 16) return fail(TACTIC_ERR_SHAPE, "K and V must be 16-byte aligned");
+  if ((st = check_device())) return st;
+  tactic_params_t P = {};
+  if (params) P = *params;
+  tactic_index_s* x = nullptr;
+  if ((st = alloc_index(r, C, iters, P.num_ctas, &x))) return st;
+  const int units = x->units;
+  KmArgs a = {};
+  a.K = (const __nv_bfloat16*)K;
+  a.V = (const __nv_bfloat16*)V;
+  a.sb = r.sb;
+  a.sh = r.sh;
+  a.sn = r.sn;
+  a.B = r.B;
+  a.Hkv = r.Hkv;
+  a.n = r.n;
+  a.C = C;
+  a.Cpad = (C + 127) / 128 * 128;
+  a.units = units;
+  a.nblk = (r.n + 1023) / 1024;
+  a.iters_req = iters;
+  a.cent = x->cent;
+  a.offsets = x->offsets;
+  a.perm = x->perm;
+  a.assign = x->assign;
+  a.iters_run = x->iters_run;
+  a.all_list = x->all_list;
+  a.all_prefix = x->all_prefix;
+  a.Kp = x->Kp;
+  a.Vp = x->Vp;
+  // scratch (stream-ordered)
+  auto bail = [&](tactic_status_t s2) {
+    tactic_index_destroy(x);
+    return s2;
+  };
+  cudaError_t e;
+  int* d_init = nullptr;
+  int* d_flag = nullptr;
+  const bool build = host_cent == nullptr;
+  if ((e = cudaMallocAsync((void**)&a.bimg, (size_t)units * a.Cpad / 128 * 65536, s))) return bail(cuda_fail(e, "scratch"));
+  if ((e = cudaMallocAsync((void**)&a.cnorm, (size_t)units * a.Cpad * 4, s))) return bail(cuda_fail(e, "scratch"));
+  if ((e = cudaMallocAsync((void**)&a.blk_counts, (size_t)units * a.nblk * C * 4, s))) return bail(cuda_fail(e, "scratch"));
+  if ((e = cudaMallocAsync((void**)&a.changed, (size_t)(iters + 2) * units * 4, s))) return bail(cuda_fail(e, "scratch"));
+  if ((e = cudaMallocAsync((void**)&a.converged, (size_t)units * 4, s))) return bail(cuda_fail(e, "scratch"));
+  if ((e = cudaMallocAsync((void**)&d_init, (size_t)units * C * 4, s))) return bail(cuda_fail(e, "scratch"));
+  if ((e = cudaMallocAsync((void**)&d_flag, 4, s))) return bail(cuda_fail(e, "scratch"));
+  cudaMemsetAsync(a.changed, 0, (size_t)(iters + 2) * units * 4, s);
+  cudaMemsetAsync(a.converged, 0, (size_t)units * 4, s);
+  cudaMemsetAsync(d_flag, 0, 4, s);
+  cudaMemsetAsync(x->assign, 0xff, (size_t)units * r.n * 4, s);
+  auto free_scratch = [&]() {
+    cudaFreeAsync(a.bimg, s);
+    cudaFreeAsync(a.cnorm, s);
+    cudaFreeAsync(a.blk_counts, s);
+    cudaFreeAsync(a.changed, s);
+    cudaFreeAsync(a.converged, s);
+    cudaFreeAsync(d_init, s);
+    cudaFreeAsync(d_flag, s);
+  };
+#define CKB(expr)                                           \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) {                                \
+      tactic_status_t _s = cuda_fail(_e, #expr);            \
+      free_scratch();                                       \
+      cudaStreamSynchronize(s);                             \
+      return bail(_s);                                      \
+    }                                                       \
+  } while (0)
+  if (P.flags & TACTIC_FLAG_VALIDATE) {
+    CKB(km_check_finite(a, d_flag, s));
+    int h = 0;
+    CKB(cudaMemcpyAsync(&h, d_flag, 4, cudaMemcpyDeviceToHost, s));
+    CKB(cudaStreamSynchronize(s));
+    if (h) {
+      free_scratch();
+      return bail(fail(TACTIC_ERR_NOT_FINITE, "K or V contains NaN/Inf"));
+    }
+  }
+  if (build) {
+    std::vector<int> init((size_t)units * C);
+    for (int u = 0; u < units; ++u) {
+      if (P.init_indices) {
+        for (int j = 0; j < C; ++j) {
+          const int t = P.init_indices[(size_t)u * C + j];
+          if (t < 0 || t >= r.n) {
+            free_scratch();
+            return bail(fail(TACTIC_ERR_INVALID_ARGUMENT, "init_indices[%d][%d] = %d out of range", u, j, t));
+          }
+          init[(size_t)u * C + j] = t;
+        }
+      } else {
+        sample_init(r.n, C, P.seed, u, &init[(size_t)u * C]);
+      }
+    }
+    CKB(cudaMemcpyAsync(d_init, init.data(), init.size() * 4, cudaMemcpyHostToDevice, s));
+    CKB(cudaStreamSynchronize(s));  // pageable staging buffer goes out of scope
+    CKB(km_init_centroids(a, d_init, s));
+    const bool simt = (P.flags & TACTIC_FLAG_KMEANS_SIMT) != 0;
+    for (int it = 1; it <= iters; ++it) {
+      CKB(km_assign(a, it, simt, s));
+      CKB(km_count_scan_scatter(a, it, s));
+      CKB(km_update(a, it, s));
+    }
+  } else {
+    for (size_t i = 0; i < (size_t)units * r.n; ++i)
+      if (host_assign[i] < 0 || host_assign[i] >= C) {
+        free_scratch();
+        return bail(fail(TACTIC_ERR_INVALID_ARGUMENT, "assign[%zu] = %d out of [0, C)", i, host_assign[i]));
+      }
+    CKB(cudaMemcpyAsync(x->cent, host_cent, (size_t)units * C * 128 * 4, cudaMemcpyHostToDevice, s));
+    CKB(cudaMemcpyAsync(x->assign, host_assign, (size_t)units * r.n * 4, cudaMemcpyHostToDevice, s));
+    CKB(km_count_scan_scatter(a, 1, s));
+    x->iters_req = 0;
+    a.iters_req = 0;
+  }
+  CKB(km_finalize(a, s));
+  free_scratch();
+  if (!build) CKB(cudaStreamSynchronize(s));
+#undef CKB
+  *out = x;
+  return TACTIC_OK;
+}
+
+extern "C" {
+
+tactic_status_t tactic_build_index(const void* K, const void* V, const tactic_kv_desc_t* kv, int32_t n_clusters,
+                                   int32_t iters, const tactic_params_t* params, void* stream,
+                                   tactic_index_t* out) {
+  return build_common(K, V, kv, n_clusters, iters, params, (cudaStream_t)stream, nullptr, nullptr, out);
+}
+
+tactic_status_t tactic_index_import(const void* K, const void* V, const tactic_kv_desc_t* kv, int32_t n_clusters,
+                                    const float* centroids, const int32_t* assign, const tactic_params_t* params,
+                                    void* stream, tactic_index_t* out) {
+  if (!centroids || !assign) return fail(TACTIC_ERR_INVALID_ARGUMENT, "centroids / assign is NULL");
+  return build_common(K, V, kv, n_clusters, 1, params, (cudaStream_t)stream, centroids, assign, out);
+}
+
+void tactic_index_destroy(tactic_index_t idx) {
+  if (!idx) return;
+  std::vector<void*> ptrs;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_allocs.find(idx);
+    if (it != g_allocs.end()) {
+      ptrs = it->second;
+      g_allocs.erase(it);
+    }
+  }
+  free_index(idx, &ptrs);
+}
+
+tactic_status_t tactic_index_info(tactic_index_t idx, tactic_index_info_t* info) {
+  if (!idx || !info) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  info->units = idx->units;
+  info->batch = idx->B;
+  info->num_kv_heads = idx->Hkv;
+  info->group_size = idx->G;
+  info->seq_len = idx->n;
+  info->n_clusters = idx->C;
+  info->iters_requested = idx->iters_req;
+  info->device_bytes = idx->device_bytes;
+  return TACTIC_OK;
+}
+
+tactic_status_t tactic_index_export(tactic_index_t idx, float* centroids, int32_t* assign, double* inertia,
+                                    int32_t* iters_run, void* stream) {
+  if (!idx) return fail(TACTIC_ERR_INVALID_ARGUMENT, "index is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t U = idx->units;
+  if (centroids) CK(cudaMemcpyAsync(centroids, idx->cent, U * idx->C * 128 * 4, cudaMemcpyDeviceToHost, s));
+  if (assign) CK(cudaMemcpyAsync(assign, idx->assign, U * idx->n * 4, cudaMemcpyDeviceToHost, s));
+  if (iters_run) CK(cudaMemcpyAsync(iters_run, idx->iters_run, U * 4, cudaMemcpyDeviceToHost, s));
+  if (inertia) {
+    double* part = nullptr;
+    CK(cudaMallocAsync((void**)&part, U * idx->C * sizeof(double), s));
+    KmArgs a = {};
+    a.n = idx->n;
+    a.C = idx->C;
+    a.units = idx->units;
+    a.cent = idx->cent;
+    a.offsets = idx->offsets;
+    a.Kp = idx->Kp;
+    CK(km_inertia(a, part, s));
+    std::vector<double> h(U * idx->C);
+    CK(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaFreeAsync(part, s));
+    CK(cudaStreamSynchronize(s));
+    for (size_t u = 0; u < U; ++u) {
+      double t = 0.0;
+      for (int j = 0; j < idx->C; ++j) t += h[u * idx->C + j];
+      inertia[u] = t;
+    }
+  }
+  CK(cudaStreamSynchronize(s));
+  return TACTIC_OK;
+}
+
+// ------------------------------------------------------------------------ decode
+static tactic_status_t run_selection(const void* q, tactic_index_t idx, double p, int mode, cudaStream_t s,
+                                     const double* gmax, const double* gmass, double* local_max) {
+  SelArgs sa = {};
+  sa.q = (const __nv_bfloat16*)q;
+  sa.idx = idx;
+  sa.p = p;
+  sa.mode = mode;
+  sa.gmax = gmax;
+  sa.gmass = gmass;
+  sa.local_max = local_max;
+  const bool pdl = true;
+  if (mode != 1) {
+    CK(launch_score(sa, s, pdl));
+    CK(launch_sort(sa, s, pdl));
+    CK(launch_sample(sa, s, pdl));
+  } else {
+    CK(launch_score(sa, s, pdl));
+  }
+  CK(launch_select(sa, s, pdl));
+  return TACTIC_OK;
+}
+
+static tactic_status_t run_attention(const void* q, tactic_index_t idx, bool all, cudaStream_t s, void* out,
+                                     float* out_f32, float* lse) {
+  AttnArgs aa = {};
+  aa.q = (const __nv_bfloat16*)q;
+  aa.Kp = idx->Kp;
+  aa.Vp = idx->Vp;
+  aa.seg_list = all ? idx->all_list : idx->union_list;
+  aa.seg_prefix = all ? idx->all_prefix : idx->union_prefix;
+  aa.offsets = idx->offsets;
+  aa.unit_prefix = all ? idx->all_unit_prefix : idx->unit_prefix;
+  aa.n = idx->n;
+  aa.C = idx->C;
+  aa.units = idx->units;
+  aa.Hkv = idx->Hkv;
+  aa.part_o = idx->part_o;
+  aa.part_lse = idx->part_lse;
+  CK(launch_attention_sparse(aa, idx->G, idx->num_ctas, s, true));
+  CK(launch_merge(idx->part_o, idx->part_lse, aa.unit_prefix, idx->n, idx->units, idx->G, idx->num_ctas,
+                  (__nv_bfloat16*)out, out_f32, lse, s, true));
+  return TACTIC_OK;
+}
+
+static tactic_status_t check_p(float p) {
+  if (!(p > 0.0f) || p > 1.0f || std::isnan(p)) return fail(TACTIC_ERR_INVALID_ARGUMENT, "p must be in (0, 1] (got %g)", p);
+  return TACTIC_OK;
+}
+
+tactic_status_t tactic_decode_ex(const void* q, tactic_index_t idx, float p, void* out, float* lse, void* stream) {
+  if (!q || !idx || !out) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  tactic_status_t st = check_p(p);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p >= 1.0f) return run_attention(q, idx, true, s, out, nullptr, lse);  // reading 15
+  if ((st = run_selection(q, idx, (double)p, 0, s, nullptr, nullptr, nullptr))) return st;
+  return run_attention(q, idx, false, s, out, nullptr, lse);
+}
+
+tactic_status_t tactic_decode(const void* q, tactic_index_t idx, float p, void* out, void* stream) {
+  return tactic_decode_ex(q, idx, p, out, nullptr, stream);
+}
+
+tactic_status_t tactic_decode_host(const void* q_host, tactic_index_t idx, float p, void* out_host, void* stream) {
+  if (!q_host || !idx || !out_host) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = (size_t)idx->units * idx->G * 128 * 2;
+  CK(cudaMemcpyAsync(idx->q_stage, q_host, bytes, cudaMemcpyHostToDevice, s));
+  tactic_status_t st = tactic_decode_ex(idx->q_stage, idx, p, idx->o_stage, nullptr, stream);
+  if (st) return st;
+  CK(cudaMemcpyAsync(out_host, idx->o_stage, bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return TACTIC_OK;
+}
+
+tactic_status_t tactic_decode_debug(const void* q, tactic_index_t idx, float p, void* out, float* lse,
+                                    int32_t* order, int32_t* J, double* fit, uint8_t* union_mask, void* stream) {
+  if (!q || !idx || !out) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  tactic_status_t st = check_p(p);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((st = run_selection(q, idx, (double)p, 0, s, nullptr, nullptr, nullptr))) return st;
+  if ((st = run_attention(q, idx, false, s, out, nullptr, lse))) return st;
+  const size_t U = idx->units, G = idx->G, C = idx->C;
+  if (order) CK(cudaMemcpyAsync(order, idx->order, U * G * C * 4, cudaMemcpyDeviceToHost, s));
+  if (J) CK(cudaMemcpyAsync(J, idx->J, U * G * 4, cudaMemcpyDeviceToHost, s));
+  if (fit) CK(cudaMemcpyAsync(fit, idx->fit, U * G * 6 * 8, cudaMemcpyDeviceToHost, s));
+  if (union_mask) CK(cudaMemcpyAsync(union_mask, idx->umask, U * C, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return TACTIC_OK;
+}
+
+// ------------------------------------------------------------------------ dense baseline
+tactic_status_t tactic_dense_workspace_size(const tactic_kv_desc_t* kv, int32_t num_ctas, size_t* bytes) {
+  Resolved r;
+  tactic_status_t st = resolve_kv(kv, &r);
+  if (st) return st;
+  if (!bytes) return fail(TACTIC_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  const int P = num_ctas > 0 ? num_ctas : device_sms();
+  const size_t slots = (size_t)P + (size_t)r.B * r.Hkv;
+  *bytes = slots * r.G * 129 * 4 + 256;
+  return TACTIC_OK;
+}
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t get_encode() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled_t)p;
+  }
+  return fn;
+}
+
+static tactic_status_t make_kv_map(CUtensorMap* m, const void* base, const Resolved& r) {
+  PFN_encodeTiled_t enc = get_encode();
+  if (!enc) return fail(TACTIC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {128, (cuuint64_t)r.n, (cuuint64_t)r.Hkv, (cuuint64_t)r.B};
+  cuuint64_t strides[3] = {(cuuint64_t)r.sn * 2, (cuuint64_t)r.sh * 2, (cuuint64_t)r.sb * 2};
+  cuuint32_t box[4] = {64, 64, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult cr = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(TACTIC_ERR_SHAPE, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  return TACTIC_OK;
+}
+
+tactic_status_t tactic_dense_decode(const void* q, const void* K, const void* V, const tactic_kv_desc_t* kv,
+                                    void* out, float* lse, void* workspace, size_t workspace_bytes,
+                                    int32_t num_ctas, void* stream) {
+  if (!q || !K || !V || !out || !workspace) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  Resolved r;
+  tactic_status_t st = resolve_kv(kv, &r);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  const int P = num_ctas > 0 ? num_ctas : device_sms();
+  size_t need = 0;
+  tactic_dense_workspace_size(kv, P, &need);
+  if (workspace_bytes < need) return fail(TACTIC_ERR_INVALID_ARGUMENT, "workspace too small (%zu < %zu)", workspace_bytes, need);
+  if ((uintptr_t)K % 16 || (uintptr_t)V % 16) return fail(TACTIC_ERR_SHAPE, "K and V must be 16-byte aligned");
+  CUtensorMap mk, mv;
+  if ((st = make_kv_map(&mk, K, r))) return st;
+  if ((st = make_kv_map(&mv, V, r))) return st;
+  const size_t units = (size_t)r.B * r.Hkv;
+  const size_t slots = (size_t)P + units;
+  float* part_o = (float*)workspace;
+  float* part_lse = part_o + slots * r.G * 128;
+  AttnArgs aa = {};
+  aa.q = (const __nv_bfloat16*)q;
+  aa.n = r.n;
+  aa.units = (int)units;
+  aa.Hkv = r.Hkv;
+  aa.part_o = part_o;
+  aa.part_lse = part_lse;
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(launch_attention_dense(aa, &mk, &mv, r.G, P, s, true));
+  CK(launch_merge(part_o, part_lse, nullptr, r.n, (int)units, r.G, P, (__nv_bfloat16*)out, nullptr, lse, s, true));
+  return TACTIC_OK;
+}
+
+tactic_status_t tactic_lse_merge(const float* o_parts, const float* lse_parts, int32_t n_parts, int32_t n_rows,
+                                 void* out, float* lse, void* stream) {
+  if (!o_parts || !lse_parts || !out) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (n_parts < 1 || n_rows < 1) return fail(TACTIC_ERR_INVALID_ARGUMENT, "n_parts and n_rows must be >= 1");
+  CK(launch_lse_merge_plain(o_parts, lse_parts, n_parts, n_rows, (__nv_bfloat16*)out, lse, (cudaStream_t)stream));
+  return TACTIC_OK;
+}
+
+// ------------------------------------------------------------------------ sharded mode
+tactic_status_t tactic_decode_stage1(const void* q, tactic_index_t idx, double* local_max, void* stream) {
+  if (!q || !idx || !local_max) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  return run_selection(q, idx, 0.5, 2, (cudaStream_t)stream, nullptr, nullptr, local_max);
+}
+
+tactic_status_t tactic_decode_stage1b(tactic_index_t idx, const double* global_max, double* mass, void* stream) {
+  if (!idx || !global_max || !mass) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  SelArgs sa = {};
+  sa.idx = idx;
+  sa.gmax = global_max;
+  sa.mass_out = mass;
+  CK(launch_stage1b(sa, (cudaStream_t)stream));
+  return TACTIC_OK;
+}
+
+tactic_status_t tactic_decode_stage2(const void* q, tactic_index_t idx, float p, const double* global_max,
+                                     const double* global_mass, float* o_part, float* lse_part, void* stream) {
+  if (!q || !idx || !global_max || !global_mass || !o_part || !lse_part)
+    return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  tactic_status_t st = check_p(p);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  SelArgs sa = {};
+  sa.q = (const __nv_bfloat16*)q;
+  sa.idx = idx;
+  sa.p = p;
+  sa.mode = 1;
+  sa.gmax = global_max;
+  sa.gmass = global_mass;
+  CK(launch_select(sa, s, true));
+  return run_attention(q, idx, false, s, nullptr, o_part, lse_part);
+}
+
+// ------------------------------------------------------------------------ misc
+const char* tactic_status_string(tactic_status_t s) {
+  switch (s) {
+    case TACTIC_OK: return "TACTIC_OK";
+    case TACTIC_ERR_INVALID_ARGUMENT: return "TACTIC_ERR_INVALID_ARGUMENT";
+    case TACTIC_ERR_SHAPE: return "TACTIC_ERR_SHAPE";
+    case TACTIC_ERR_OOM: return "TACTIC_ERR_OOM";
+    case TACTIC_ERR_CUDA: return "TACTIC_ERR_CUDA";
+    case TACTIC_ERR_NOT_FINITE: return "TACTIC_ERR_NOT_FINITE";
+    case TACTIC_ERR_UNSUPPORTED: return "TACTIC_ERR_UNSUPPORTED";
+  }
+  return "TACTIC_ERR_UNKNOWN";
+}
+
+const char* tactic_last_error(void) { return g_err.c_str(); }
+
+const char* tactic_version(void) { return "tactic-b200 0.1.0 (sm_100a)"; }
+
+tactic_status_t tactic_device_check(int32_t* num_sms) {
+  tactic_status_t st = check_device();
+  if (st) return st;
+  if (num_sms) *num_sms = device_sms();
+  return TACTIC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,333 @@
+"""Thin Python binding of libtactic.so (include/tactic.h) -- argument marshalling only.
+
+Every step of the decode path runs inside the library's sm_100a kernels; this module
+only converts torch tensors / numpy arrays into pointers and the current CUDA stream.
+There is no fallback: if the shared library is missing, importing the binding fails.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libtactic.so")
+
+STATUS = {0: "TACTIC_OK", 1: "TACTIC_ERR_INVALID_ARGUMENT", 2: "TACTIC_ERR_SHAPE", 3: "TACTIC_ERR_OOM",
+          4: "TACTIC_ERR_CUDA", 5: "TACTIC_ERR_NOT_FINITE", 6: "TACTIC_ERR_UNSUPPORTED"}
+FLAG_VALIDATE = 1
+FLAG_KMEANS_SIMT = 2
+SHARD_GRID_T = 512
+SHARD_GRID_STEP = 0.0625
+HEAD_DIM = 128
+
+
+class TacticError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        super().__init__(f"{STATUS.get(status, status)}: {detail}")
+        self.status = status
+
+
+class KvDesc(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32), ("group_size", ctypes.c_int32),
+                ("seq_len", ctypes.c_int32), ("head_dim", ctypes.c_int32), ("stride_b", ctypes.c_int64),
+                ("stride_h", ctypes.c_int64), ("stride_n", ctypes.c_int64)]
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("init_indices", ctypes.c_void_p), ("flags", ctypes.c_uint32),
+                ("num_ctas", ctypes.c_int32)]
+
+
+class IndexInfo(ctypes.Structure):
+    _fields_ = [("units", ctypes.c_int32), ("batch", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
+                ("group_size", ctypes.c_int32), ("seq_len", ctypes.c_int32), ("n_clusters", ctypes.c_int32),
+                ("iters_requested", ctypes.c_int32), ("device_bytes", ctypes.c_int64)]
+
+
+_lib = None
+_P = ctypes.c_void_p
+_I = ctypes.c_int32
+_F = ctypes.c_float
+
+_SIGS = {
+    "tactic_build_index": [_P, _P, ctypes.POINTER(KvDesc), _I, _I, ctypes.POINTER(Params), _P, ctypes.POINTER(_P)],
+    "tactic_index_import": [_P, _P, ctypes.POINTER(KvDesc), _I, _P, _P, ctypes.POINTER(Params), _P,
+                            ctypes.POINTER(_P)],
+    "tactic_index_export": [_P, _P, _P, _P, _P, _P],
+    "tactic_index_info": [_P, ctypes.POINTER(IndexInfo)],
+    "tactic_decode": [_P, _P, _F, _P, _P],
+    "tactic_decode_ex": [_P, _P, _F, _P, _P, _P],
+    "tactic_decode_host": [_P, _P, _F, _P, _P],
+    "tactic_decode_debug": [_P, _P, _F, _P, _P, _P, _P, _P, _P, _P],
+    "tactic_dense_workspace_size": [ctypes.POINTER(KvDesc), _I, ctypes.POINTER(ctypes.c_size_t)],
+    "tactic_dense_decode": [_P, _P, _P, ctypes.POINTER(KvDesc), _P, _P, _P, ctypes.c_size_t, _I, _P],
+    "tactic_lse_merge": [_P, _P, _I, _I, _P, _P, _P],
+    "tactic_decode_stage1": [_P, _P, _P, _P],
+    "tactic_decode_stage1b": [_P, _P, _P, _P],
+    "tactic_decode_stage2": [_P, _P, _F, _P, _P, _P, _P, _P],
+    "tactic_device_check": [ctypes.POINTER(_I)],
+}
+
+
+def lib():
+    """Load libtactic.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2502_12216_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = ctypes.c_int
+        L.tactic_index_destroy.argtypes = [_P]
+        L.tactic_index_destroy.restype = None
+        for name in ("tactic_status_string",):
+            getattr(L, name).argtypes = [ctypes.c_int]
+            getattr(L, name).restype = ctypes.c_char_p
+        L.tactic_last_error.argtypes = []
+        L.tactic_last_error.restype = ctypes.c_char_p
+        L.tactic_version.argtypes = []
+        L.tactic_version.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise TacticError(st, lib().tactic_last_error().decode())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _kv_desc(K: torch.Tensor, group_size: int) -> KvDesc:
+    if K.dim() != 4 or K.shape[-1] != HEAD_DIM:
+        raise ValueError("K/V must be [B, Hkv, n, 128]")
+    if K.dtype != torch.bfloat16 or not K.is_cuda:
+        raise ValueError("K/V must be CUDA bfloat16 tensors")
+    if K.stride(-1) != 1:
+        raise ValueError("last dimension must be contiguous")
+    B, H, n, d = K.shape
+    return KvDesc(B, H, group_size, n, d, K.stride(0), K.stride(1), K.stride(2))
+
+
+def version() -> str:
+    return lib().tactic_version().decode()
+
+
+def device_check() -> int:
+    n = _I(0)
+    _check(lib().tactic_device_check(ctypes.byref(n)))
+    return n.value
+
+
+def sample_constants(n: int) -> dict:
+    """The integer sample constants the library uses (mirrors tactic_api.cu; host logic)."""
+    N = (2 * n + 99) // 100
+    x1 = (n + 5) // 10
+    x2 = (6 * n + 5) // 10
+    w = max(1, (25 * n + 5000) // 10000)
+    fb = (x1 - w <= N) or (x1 + w >= x2 - w) or (x2 + w > n)
+    return {"N": N, "x1": x1, "x2": x2, "w": w, "fallback": fb, "slots": n if fb else N + 2 * (2 * w + 1)}
+
+
+class Index:
+    """Owns a tactic_index_t (device memory released on close / garbage collection)."""
+
+    def __init__(self, handle: ctypes.c_void_p, K_shape, group_size: int, n_clusters: int):
+        self._h = handle
+        self.B, self.Hkv, self.n, _ = K_shape
+        self.G = group_size
+        self.C = n_clusters
+        self.units = self.B * self.Hkv
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise ValueError("index is closed")
+        return self._h
+
+    def close(self):
+        if self._h is not None and _lib is not None:
+            lib().tactic_index_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        i = IndexInfo()
+        _check(lib().tactic_index_info(self.handle, ctypes.byref(i)))
+        return {f: getattr(i, f) for f, _ in IndexInfo._fields_}
+
+    def export(self, stream=None) -> dict:
+        cent = np.empty((self.units, self.C, HEAD_DIM), dtype=np.float32)
+        assign = np.empty((self.units, self.n), dtype=np.int32)
+        inertia = np.empty(self.units, dtype=np.float64)
+        iters = np.empty(self.units, dtype=np.int32)
+        _check(lib().tactic_index_export(self.handle, cent.ctypes.data, assign.ctypes.data, inertia.ctypes.data,
+                                         iters.ctypes.data, _stream(stream)))
+        return {"centroids": cent, "assign": assign, "inertia": inertia, "iters_run": iters}
+
+
+def build_index(K: torch.Tensor, V: torch.Tensor, n_clusters: int, iters: int = 10, *, group_size: int = 4,
+                seed: int = 0, init: Optional[np.ndarray] = None, flags: int = 0, num_ctas: int = 0,
+                stream=None) -> Index:
+    """tactic_build_index: k-means (tcgen05 assignment) + cluster-contiguous KV layout."""
+    kv = _kv_desc(K, group_size)
+    if tuple(V.shape) != tuple(K.shape) or V.stride() != K.stride() or V.dtype != K.dtype:
+        raise ValueError("V must match K in shape, strides and dtype")
+    init_arr = None
+    if init is not None:
+        init_arr = np.ascontiguousarray(init, dtype=np.int32)
+        if init_arr.shape != (kv.batch * kv.num_kv_heads, n_clusters):
+            raise ValueError("init must be [units, n_clusters]")
+    p = Params(seed, init_arr.ctypes.data if init_arr is not None else None, flags, num_ctas)
+    h = ctypes.c_void_p()
+    _check(lib().tactic_build_index(_ptr(K), _ptr(V), ctypes.byref(kv), n_clusters, iters, ctypes.byref(p),
+                                    _stream(stream), ctypes.byref(h)))
+    return Index(h, tuple(K.shape), group_size, n_clusters)
+
+
+def import_index(K: torch.Tensor, V: torch.Tensor, centroids: np.ndarray, assign: np.ndarray, *,
+                 group_size: int = 4, num_ctas: int = 0, stream=None) -> Index:
+    """tactic_index_import: index from a given clustering (float32 centroids, int32 assignment)."""
+    kv = _kv_desc(K, group_size)
+    units = kv.batch * kv.num_kv_heads
+    cent = np.ascontiguousarray(centroids, dtype=np.float32)
+    asg = np.ascontiguousarray(assign, dtype=np.int32)
+    if cent.ndim != 3 or cent.shape[0] != units or cent.shape[2] != HEAD_DIM:
+        raise ValueError("centroids must be [units, C, 128]")
+    if asg.shape != (units, kv.seq_len):
+        raise ValueError("assign must be [units, n]")
+    C = cent.shape[1]
+    p = Params(0, None, 0, num_ctas)
+    h = ctypes.c_void_p()
+    _check(lib().tactic_index_import(_ptr(K), _ptr(V), ctypes.byref(kv), C, cent.ctypes.data, asg.ctypes.data,
+                                     ctypes.byref(p), _stream(stream), ctypes.byref(h)))
+    return Index(h, tuple(K.shape), group_size, C)
+
+
+def _q_check(q: torch.Tensor, index: Index):
+    if q.dtype != torch.bfloat16 or not q.is_cuda or not q.is_contiguous():
+        raise ValueError("q must be a contiguous CUDA bfloat16 tensor")
+    if q.numel() != index.units * index.G * HEAD_DIM:
+        raise ValueError("q must be [B, Hkv*G, 128] for this index")
+
+
+def decode(q: torch.Tensor, index: Index, p: float, out: Optional[torch.Tensor] = None,
+           lse: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """tactic_decode_ex: one decode step of every unit; returns out [B, Hq, 128] bf16."""
+    _q_check(q, index)
+    if out is None:
+        out = torch.empty_like(q)
+    _check(lib().tactic_decode_ex(_ptr(q), index.handle, float(p), _ptr(out), _ptr(lse), _stream(stream)))
+    return out
+
+
+def decode_host(q_host: torch.Tensor, index: Index, p: float, out_host: Optional[torch.Tensor] = None,
+                stream=None) -> torch.Tensor:
+    """tactic_decode_host: q and out in host memory (end-to-end call; synchronises)."""
+    if q_host.device.type != "cpu" or q_host.dtype != torch.bfloat16 or not q_host.is_contiguous():
+        raise ValueError("q_host must be a contiguous CPU bfloat16 tensor")
+    if out_host is None:
+        out_host = torch.empty_like(q_host)
+    _check(lib().tactic_decode_host(_ptr(q_host), index.handle, float(p), _ptr(out_host), _stream(stream)))
+    return out_host
+
+
+def decode_debug(q: torch.Tensor, index: Index, p: float, stream=None) -> dict:
+    """tactic_decode_debug: output plus the selection (order, J, fit, union mask) on the host."""
+    _q_check(q, index)
+    out = torch.empty_like(q)
+    lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
+    U, G, C = index.units, index.G, index.C
+    order = np.empty((U, G, C), dtype=np.int32)
+    J = np.empty((U, G), dtype=np.int32)
+    fit = np.empty((U, G, 6), dtype=np.float64)
+    um = np.empty((U, C), dtype=np.uint8)
+    _check(lib().tactic_decode_debug(_ptr(q), index.handle, float(p), _ptr(out), _ptr(lse), order.ctypes.data,
+                                     J.ctypes.data, fit.ctypes.data, um.ctypes.data, _stream(stream)))
+    return {"out": out, "lse": lse, "order": order, "J": J, "fit": fit, "union_mask": um.astype(bool)}
+
+
+_ws_cache = {}
+
+
+def dense_decode(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, out: Optional[torch.Tensor] = None,
+                 lse: Optional[torch.Tensor] = None, num_ctas: int = 0, workspace: Optional[torch.Tensor] = None,
+                 stream=None) -> torch.Tensor:
+    """tactic_dense_decode: the library's own full-attention split-KV baseline."""
+    G = q.shape[1] // K.shape[1]
+    kv = _kv_desc(K, G)
+    sz = ctypes.c_size_t()
+    _check(lib().tactic_dense_workspace_size(ctypes.byref(kv), num_ctas, ctypes.byref(sz)))
+    if workspace is None:
+        key = (q.device.index, sz.value)
+        workspace = _ws_cache.get(key)
+        if workspace is None:
+            workspace = torch.empty(sz.value, dtype=torch.uint8, device=q.device)
+            _ws_cache[key] = workspace
+    if out is None:
+        out = torch.empty_like(q)
+    _check(lib().tactic_dense_decode(_ptr(q), _ptr(K), _ptr(V), ctypes.byref(kv), _ptr(out), _ptr(lse),
+                                     _ptr(workspace), workspace.numel(), num_ctas, _stream(stream)))
+    return out
+
+
+def dense_workspace_bytes(K: torch.Tensor, group_size: int, num_ctas: int = 0) -> int:
+    kv = _kv_desc(K, group_size)
+    sz = ctypes.c_size_t()
+    _check(lib().tactic_dense_workspace_size(ctypes.byref(kv), num_ctas, ctypes.byref(sz)))
+    return sz.value
+
+
+def lse_merge(o_parts: torch.Tensor, lse_parts: torch.Tensor, out: Optional[torch.Tensor] = None,
+              lse: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """tactic_lse_merge: o_parts [S, R, 128] f32, lse_parts [S, R] f32 -> out [R, 128] bf16."""
+    S, R = lse_parts.shape
+    if out is None:
+        out = torch.empty((R, HEAD_DIM), dtype=torch.bfloat16, device=o_parts.device)
+    _check(lib().tactic_lse_merge(_ptr(o_parts), _ptr(lse_parts), S, R, _ptr(out), _ptr(lse), _stream(stream)))
+    return out
+
+
+def decode_stage1(q: torch.Tensor, index: Index, local_max: Optional[torch.Tensor] = None, stream=None):
+    if local_max is None:
+        local_max = torch.empty((index.units, index.G, 2), dtype=torch.float64, device=q.device)
+    _check(lib().tactic_decode_stage1(_ptr(q), index.handle, _ptr(local_max), _stream(stream)))
+    return local_max
+
+
+def decode_stage1b(index: Index, global_max: torch.Tensor, mass: Optional[torch.Tensor] = None, stream=None):
+    if mass is None:
+        mass = torch.empty((index.units, index.G, 1 + SHARD_GRID_T), dtype=torch.float64,
+                           device=global_max.device)
+    _check(lib().tactic_decode_stage1b(index.handle, _ptr(global_max), _ptr(mass), _stream(stream)))
+    return mass
+
+
+def decode_stage2(q: torch.Tensor, index: Index, p: float, global_max: torch.Tensor, global_mass: torch.Tensor,
+                  o_part: Optional[torch.Tensor] = None, lse_part: Optional[torch.Tensor] = None, stream=None):
+    if o_part is None:
+        o_part = torch.empty((index.units, index.G, HEAD_DIM), dtype=torch.float32, device=q.device)
+    if lse_part is None:
+        lse_part = torch.empty((index.units, index.G), dtype=torch.float32, device=q.device)
+    _check(lib().tactic_decode_stage2(_ptr(q), index.handle, float(p), _ptr(global_max), _ptr(global_mass),
+                                      _ptr(o_part), _ptr(lse_part), _stream(stream)))
+    return o_part, lse_part

@@ -1,0 +1,341 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the float64 oracle on the same seeded
+synthetic inputs.  Bars (BASELINE.json north_star): index sets bit-exact except within
+1e-5 of the threshold; decode output max-abs <= 2e-2 and rel-L2 <= 5e-3; k-means
+inertia within 1e-4 relative from an identical initialisation."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import tactic_oracle as O
+from synth import make_layer, make_unit, uniform_unit
+from tests._gpu_helpers import (assert_output_close, dev_bf16, j_mismatch_allowed, oracle_layer_clustering)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    from paper_2502_12216_b200 import build as B
+    B.build()
+    from paper_2502_12216_b200 import tactic
+    tactic.device_check()
+    return tactic
+
+
+def _layer(B, H, G, n, seed):
+    K, V, q = make_layer(B, H, G, n, seed)
+    return K, V, q
+
+
+# ----------------------------------------------------------------------------- dense baseline
+@pytest.mark.parametrize("B,H,G,n", [(1, 1, 4, 4096), (1, 2, 1, 1000), (2, 1, 8, 4133), (1, 3, 2, 777),
+                                     (1, 1, 4, 64), (1, 1, 4, 1)])
+def test_dense_decode_matches_full_attention(T, B, H, G, n):
+    K, V, q = _layer(B, H, G, n, seed=n)
+    Kd, Vd, qd = dev_bf16(K), dev_bf16(V), dev_bf16(q)
+    lse = torch.empty((B, H * G), dtype=torch.float32, device="cuda")
+    out = T.dense_decode(qd, Kd, Vd, lse=lse)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            o, l = O.full_attention(q[b, h * G:(h + 1) * G], K[b, h], V[b, h])
+            assert_output_close(got[b, h * G:(h + 1) * G], o, f"dense b{b} h{h}")
+            np.testing.assert_allclose(lse[b, h * G:(h + 1) * G].cpu().numpy(), l, rtol=0, atol=2e-3)
+
+
+def test_dense_decode_strided_view(T):
+    B, H, G, n = 1, 2, 4, 3000
+    K, V, q = _layer(B, H, G, n, seed=5)
+    big = torch.zeros((B, H, n + 100, 128), dtype=torch.bfloat16, device="cuda")
+    big[:, :, :n] = dev_bf16(K)
+    bigV = torch.zeros_like(big)
+    bigV[:, :, :n] = dev_bf16(V)
+    out = T.dense_decode(dev_bf16(q), big[:, :, :n], bigV[:, :, :n], num_ctas=37)
+    got = out.float().cpu().numpy()
+    for h in range(H):
+        o, _ = O.full_attention(q[0, h * G:(h + 1) * G], K[0, h], V[0, h])
+        assert_output_close(got[0, h * G:(h + 1) * G], o, "strided")
+
+
+# ----------------------------------------------------------------------------- decode via imported clustering
+def _import(T, K, V, cents, asg, G, **kw):
+    return T.import_index(dev_bf16(K), dev_bf16(V), cents, asg, group_size=G, **kw)
+
+
+def _check_unit_selection(res, u, G, heads_o, p, C):
+    """order exact (ties by id), J within the threshold tolerance, union = union of the
+    GPU prefixes of the oracle order."""
+    for g in range(G):
+        ho = heads_o[g]
+        assert np.array_equal(res["order"][u, g], ho["order"]), f"order u{u} g{g}"
+        Jg = int(res["J"][u, g])
+        assert j_mismatch_allowed(ho, Jg, p), f"J u{u} g{g}: gpu {Jg} oracle {ho['J']}"
+        fit = res["fit"][u, g]
+        if not ho["fallback"]:
+            assert fit[2] == pytest.approx(ho["m"], abs=2e-5)
+            assert fit[4] == pytest.approx(ho["mu1"], rel=2e-5)
+            assert fit[5] == pytest.approx(ho["mu2"], rel=2e-5)
+            assert fit[0] == pytest.approx(ho["a"], rel=1e-4, abs=1e-6)
+            assert fit[1] == pytest.approx(ho["b"], abs=1e-4 * max(abs(ho["mu1"]), 1e-12))
+        assert fit[3] == pytest.approx(ho["W"], rel=1e-5)
+    return True
+
+
+@pytest.mark.parametrize("n,C,seed", [(4096, 64, 0), (4096, 64, 1), (32768, 256, 2), (5000, 77, 3)])
+def test_import_decode_selection_and_output(T, n, C, seed):
+    G = 4
+    K, V, q = _layer(1, 2, G, n, seed)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 10, seed)
+    index = _import(T, K, V, cents, asg, G)
+    qd = dev_bf16(q)
+    for p in [0.5, 0.8, 0.9, 0.95, 0.99]:
+        res = T.decode_debug(qd, index, p)
+        got = res["out"].float().cpu().numpy()
+        for u in range(2):
+            qo = q[0, u * G:(u + 1) * G]
+            ro = O.decode_unit(qo, idxs[u], p)
+            _check_unit_selection(res, u, G, ro["heads"], p, C)
+            # union recomputed from the GPU's J on the oracle's order must equal the GPU union
+            mask = np.zeros(C, dtype=bool)
+            for g in range(G):
+                pos = ro["heads"][g]["order"][:res["J"][u, g]]
+                mask[pos[idxs[u].sizes[pos] > 0]] = True
+            assert np.array_equal(mask, res["union_mask"][u]), f"union u{u} p{p}"
+            # numerics against the oracle's attention over the GPU's union
+            toks = O.cluster_tokens(idxs[u], np.nonzero(res["union_mask"][u])[0])
+            o, l = O.sparse_attention(qo, idxs[u].K, idxs[u].V, toks)
+            assert_output_close(got[0, u * G:(u + 1) * G], o, f"out u{u} p{p}")
+            np.testing.assert_allclose(res["lse"][0, u * G:(u + 1) * G].cpu().numpy(), l, atol=2e-3)
+
+
+def test_import_decode_p1_equals_full_attention(T):
+    G, n, C = 4, 4096, 64
+    K, V, q = _layer(1, 2, G, n, 4)
+    cents, asg, _ = oracle_layer_clustering(K, V, C, 10, 4)
+    index = _import(T, K, V, cents, asg, G)
+    out = T.decode(dev_bf16(q), index, 1.0).float().cpu().numpy()
+    for u in range(2):
+        o, _ = O.full_attention(q[0, u * G:(u + 1) * G], K[0, u], V[0, u])
+        assert_output_close(out[0, u * G:(u + 1) * G], o, "p=1")
+
+
+@pytest.mark.parametrize("G", [1, 2, 8])
+def test_group_sizes(T, G):
+    n, C = 4096, 64
+    K, V, q = _layer(1, 1, G, n, 10 + G)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 10, G)
+    index = _import(T, K, V, cents, asg, G)
+    res = T.decode_debug(dev_bf16(q), index, 0.9)
+    ro = O.decode_unit(q[0], idxs[0], 0.9)
+    _check_unit_selection(res, 0, G, ro["heads"], 0.9, C)
+    toks = O.cluster_tokens(idxs[0], np.nonzero(res["union_mask"][0])[0])
+    o, _ = O.sparse_attention(q[0], idxs[0].K, idxs[0].V, toks)
+    assert_output_close(res["out"].float().cpu().numpy()[0], o, f"G={G}")
+
+
+def test_edge_cases_tiny_fallback_singletons_empty_clusters(T):
+    G = 4
+    # tiny n -> exact fallback (O6)
+    u = make_unit(12, G, seed=1)
+    K, V, q = u["K"][None, None], u["V"][None, None], u["q"][None]
+    cents, asg, idxs = oracle_layer_clustering(K, V, 3, 10, 1)
+    index = _import(T, K, V, cents, asg, G)
+    for p in [0.5, 0.9]:
+        res = T.decode_debug(dev_bf16(q), index, p)
+        ro = O.decode_unit(q[0], idxs[0], p)
+        assert ro["heads"][0]["fallback"]
+        _check_unit_selection(res, 0, G, ro["heads"], p, 3)
+    # C = n singleton clusters
+    u = uniform_unit(256, G, seed=2)
+    K, V, q = u["K"][None, None], u["V"][None, None], u["q"][None]
+    idx = O.make_index(u["K"], u["V"], u["K"], np.arange(256))
+    index = _import(T, K, V, u["K"][None], np.arange(256, dtype=np.int32)[None], G)
+    res = T.decode_debug(dev_bf16(q), index, 0.8)
+    ro = O.decode_unit(q[0], idx, 0.8)
+    _check_unit_selection(res, 0, G, ro["heads"], 0.8, 256)
+    # empty clusters (ids 5, 17, 40 never assigned) and C = 1
+    u = make_unit(3000, G, seed=3)
+    K, V, q = u["K"][None, None], u["V"][None, None], u["q"][None]
+    km = O.kmeans(u["K"], 48, 10, seed=3)
+    asg = km["assign"].copy()
+    remap = np.array([j for j in range(51) if j not in (5, 17, 40)])
+    asg = remap[asg]
+    cents = np.zeros((51, 128), dtype=np.float32)
+    cents[remap] = km["centroids"].astype(np.float32)
+    cents[[5, 17, 40]] = 1e3  # high criticality but empty: must never be selected
+    idx = O.make_index(u["K"], u["V"], cents, asg)
+    index = _import(T, K, V, cents[None], asg.astype(np.int32)[None], G)
+    res = T.decode_debug(dev_bf16(q), index, 0.9)
+    ro = O.decode_unit(q[0], idx, 0.9)
+    _check_unit_selection(res, 0, G, ro["heads"], 0.9, 51)
+    assert not res["union_mask"][0][[5, 17, 40]].any()
+    index1 = _import(T, K, V, u["K"][:1][None], np.zeros((1, 3000), dtype=np.int32), G)
+    out1 = T.decode(dev_bf16(q), index1, 0.5).float().cpu().numpy()
+    o, _ = O.full_attention(q[0], u["K"], u["V"])
+    assert_output_close(out1[0], o, "C=1")
+
+
+def test_invalid_arguments(T):
+    K, V, q = _layer(1, 1, 4, 512, 0)
+    index = T.build_index(dev_bf16(K), dev_bf16(V), 8, 2, group_size=4)
+    for bad in [0.0, -0.1, 1.5, float("nan")]:
+        with pytest.raises(T.TacticError) as ei:
+            T.decode(dev_bf16(q), index, bad)
+        assert ei.value.status == 1
+    with pytest.raises(T.TacticError):
+        T.build_index(dev_bf16(K), dev_bf16(V), 513, 2)
+    with pytest.raises(T.TacticError):
+        T.build_index(dev_bf16(K), dev_bf16(V), 8, 0)
+    Kn = K.copy()
+    Kn[0, 0, 7, 3] = np.nan
+    with pytest.raises(T.TacticError) as ei:
+        T.build_index(dev_bf16(Kn), dev_bf16(V), 8, 2, flags=T.FLAG_VALIDATE)
+    assert ei.value.status == 5
+
+
+# ----------------------------------------------------------------------------- k-means build
+@pytest.mark.parametrize("n,C,seed", [(4096, 64, 0), (32768, 256, 1), (10000, 100, 2)])
+def test_gpu_kmeans_inertia_parity(T, n, C, seed):
+    K, V, q = _layer(1, 2, 4, n, seed)
+    units = 2
+    init = np.stack([O.init_indices(n, C, seed, u) for u in range(units)]).astype(np.int32)
+    index = T.build_index(dev_bf16(K), dev_bf16(V), C, 10, group_size=4, init=init)
+    ex = index.export()
+    for u in range(units):
+        km = O.kmeans(K[0, u], C, 10, init=init[u])
+        assert ex["inertia"][u] == pytest.approx(km["inertia"], rel=1e-4), f"unit {u}"
+        assert 1 <= ex["iters_run"][u] <= 10
+        # structural: centroids are float32 means of the exported assignment
+        a = ex["assign"][u]
+        for j in np.unique(a)[:20]:
+            np.testing.assert_allclose(ex["centroids"][u, j], K[0, u][a == j].astype(np.float64).mean(0),
+                                       rtol=1e-6, atol=1e-6)
+
+
+def test_gpu_kmeans_sampler_matches_oracle_sampler(T):
+    # same SplitMix64/Fisher-Yates init on both sides -> same trajectory (1 iteration)
+    n, C = 4096, 64
+    K, V, q = _layer(1, 1, 4, n, 7)
+    index = T.build_index(dev_bf16(K), dev_bf16(V), C, 1, group_size=4, seed=11)
+    ex = index.export()
+    km = O.kmeans(K[0, 0], C, 1, seed=11, unit=0)
+    assert ex["inertia"][0] == pytest.approx(km["inertia"], rel=1e-5)
+    assert np.mean(ex["assign"][0] == km["assign"]) > 0.999
+
+
+def test_tcgen05_assignment_matches_simt_kernel(T):
+    n, C = 8192, 256
+    K, V, q = _layer(1, 1, 4, n, 8)
+    init = O.init_indices(n, C, 8, 0)[None].astype(np.int32)
+    a_tc = T.build_index(dev_bf16(K), dev_bf16(V), C, 1, init=init).export()["assign"]
+    a_si = T.build_index(dev_bf16(K), dev_bf16(V), C, 1, init=init, flags=T.FLAG_KMEANS_SIMT).export()["assign"]
+    assert np.mean(a_tc == a_si) > 0.999
+    a_o = O.kmeans(K[0, 0], C, 1, init=init[0])["assign"]
+    assert np.mean(a_tc[0] == a_o) > 0.999
+
+
+def test_build_then_decode_p1_full_attention(T):
+    G, n, C = 4, 8192, 64
+    K, V, q = _layer(2, 2, G, n, 9)
+    index = T.build_index(dev_bf16(K), dev_bf16(V), C, 10, group_size=G, seed=3)
+    out = T.decode(dev_bf16(q), index, 1.0).float().cpu().numpy()
+    out9 = T.decode(dev_bf16(q), index, 0.9).float().cpu().numpy()
+    for b in range(2):
+        for h in range(2):
+            sl = slice(h * G, (h + 1) * G)
+            o, _ = O.full_attention(q[b, sl], K[b, h], V[b, h])
+            assert_output_close(out[b, sl], o, "build p=1")
+            assert np.all(np.isfinite(out9[b, sl]))
+
+
+# ----------------------------------------------------------------------------- misc paths
+def test_lse_merge_kernel(T):
+    rng = np.random.default_rng(0)
+    S, R = 5, 37
+    o = rng.standard_normal((S, R, 128)).astype(np.float32)
+    l = (rng.standard_normal((S, R)) * 3).astype(np.float32)
+    l[2, 4] = -np.inf
+    out = T.lse_merge(torch.from_numpy(o).cuda(), torch.from_numpy(l).cuda()).float().cpu().numpy()
+    ref, _ = O.lse_merge(o, l)
+    assert_output_close(out, ref, "lse_merge")
+
+
+def test_decode_host_and_graph_capture(T):
+    G, n, C = 4, 4096, 64
+    K, V, q = _layer(1, 2, G, n, 12)
+    cents, asg, _ = oracle_layer_clustering(K, V, C, 5, 12)
+    index = _import(T, K, V, cents, asg, G)
+    qd = dev_bf16(q)
+    ref = T.decode(qd, index, 0.9)
+    torch.cuda.synchronize()
+    host = T.decode_host(qd.cpu(), index, 0.9)
+    assert torch.equal(host, ref.cpu())
+    out = torch.empty_like(qd)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        T.decode(qd, index, 0.9, out=out)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        T.decode(qd, index, 0.9, out=out)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+
+
+def test_sharded_stages_match_sharded_oracle(T):
+    G, S, n_shard, C = 4, 4, 4096, 64
+    u = make_unit(S * n_shard, G, seed=21)
+    q = u["q"]
+    shards_o, st = [], []
+    for s in range(S):
+        sl = slice(s * n_shard, (s + 1) * n_shard)
+        Ks, Vs = u["K"][sl], u["V"][sl]
+        idx, km = O.build_index(Ks, Vs, C, 10, seed=21, unit=s)
+        shards_o.append(idx)
+        st.append(_import(T, Ks[None, None], Vs[None, None], km["centroids"].astype(np.float32)[None],
+                          km["assign"].astype(np.int32)[None], G))
+    qd = dev_bf16(q[None])
+    for p in [0.5, 0.9, 1.0]:
+        ro = O.decode_sharded(q, shards_o, p)
+        lm = torch.stack([T.decode_stage1(qd, st[s]).clone() for s in range(S)])
+        gmax = lm.max(dim=0).values
+        mass = torch.stack([T.decode_stage1b(st[s], gmax).clone() for s in range(S)]).sum(dim=0)
+        parts = [T.decode_stage2(qd, st[s], p, gmax, mass) for s in range(S)]
+        o_parts = torch.stack([x[0].reshape(G, 128) for x in parts])
+        l_parts = torch.stack([x[1].reshape(G) for x in parts])
+        out = T.lse_merge(o_parts, l_parts).float().cpu().numpy()
+        for g in range(G):
+            assert float(gmax[0, g, 0]) == pytest.approx(ro["m_glob"][g], abs=2e-5)
+            assert float(gmax[0, g, 1]) == pytest.approx(ro["theta_max"][g], rel=1e-12)
+            np.testing.assert_allclose(mass[0, g].cpu().numpy(), ro["mass_total"][g], rtol=1e-4, atol=1e-12)
+        assert_output_close(out, ro["o"], f"sharded p={p}")
+
+
+# ----------------------------------------------------------------------------- full size (C2 launch config)
+@pytest.mark.slow
+def test_c2_full_size_sampled_parity(T):
+    """C2 shape (Llama-3-8B layer, 128K, 8 units) in the bench's launch configuration.
+    The oracle clustering (3 Lloyd iterations to bound CPU time) is imported; every unit's
+    selection and output is checked against the oracle."""
+    G, n, C = 4, 131072, 1024
+    K, V, q = _layer(1, 8, G, n, 0)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, 0)
+    index = _import(T, K, V, cents, asg, G)
+    res = T.decode_debug(dev_bf16(q), index, 0.9)
+    got = res["out"].float().cpu().numpy()
+    for u in range(8):
+        qo = q[0, u * G:(u + 1) * G]
+        ro = O.decode_unit(qo, idxs[u], 0.9)
+        _check_unit_selection(res, u, G, ro["heads"], 0.9, C)
+        toks = O.cluster_tokens(idxs[u], np.nonzero(res["union_mask"][u])[0])
+        o, _ = O.sparse_attention(qo, idxs[u].K, idxs[u].V, toks)
+        assert_output_close(got[0, u * G:(u + 1) * G], o, f"C2 unit {u}")
+    # p = 1 through the same index equals full attention (sampled units)
+    out1 = T.decode(dev_bf16(q), index, 1.0).float().cpu().numpy()
+    for u in (0, 5):
+        o, _ = O.full_attention(q[0, u * G:(u + 1) * G], K[0, u], V[0, u])
+        assert_output_close(out1[0, u * G:(u + 1) * G], o, f"C2 p=1 unit {u}")
