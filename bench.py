@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""bench.py -- Tactic decode-attention on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--p 0.9]
+
+A *step* is one decode layer-step of the whole hot path (S1-S9: centroid scoring, cluster
+sort, sampled exact scoring, a/x+b fit, estimated-mass selection, GQA union + work list,
+split-KV flash-decode, LSE merge) over one C2 layer: Llama-3-8B shape (32 Q / 8 KV
+heads, d=128), 128K context, batch 1, 1024 clusters per KV head, p=0.9, bf16 KV.
+The index (tcgen05 k-means + cluster-contiguous relayout) is built once per layer and
+timed separately ("build").  N>1 (torchrun): each rank runs its own batch-1 C2 layer
+(batch x KV-head sharding, no collective on the data path), scaling "weak"; the
+reported time is the max over ranks divided by N (job-level us per layer-step).
+
+L2: a 256 MiB buffer is written before every timed step (the 40 MB sparse working set
+would otherwise stay in the 126 MB L2); each step is bracketed by CUDA events on the
+launching stream.  --impl reference times the float64 CPU oracle (the reference arm of
+this tier) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode-attn µs/layer-step & HBM GB/s vs own dense decode @128K, p=0.9, 1/2/4/8 GPU"
+UNIT = "µs/layer-step"
+WORKLOAD = "C2"
+CFG = dict(B=1, Hkv=8, G=4, n=131072, C=1024, iters=10)
+PAPER_CONTEXT = ("paper (context, not target): up to 7.29x decode-attention and 1.58x end-to-end speedup vs "
+                 "FlashInfer full attention on Nvidia Ada 6000, CUDA 12.4 (P:47, P:404, P:691, P:701)")
+
+
+def _config(args, n_gpus):
+    return {"workload": f"{WORKLOAD}: Llama-3-8B layer (32 Q / 8 KV heads, d=128), 128K context, batch 1 per GPU, "
+                        f"1024 clusters/KV head, p={args.p}",
+            "global_batch": n_gpus, "seq_len": CFG["n"], "n_clusters": CFG["C"], "p": args.p,
+            "parallelism": f"batch x KV-head sharded over {n_gpus} GPU(s), no data-path collective",
+            "l2": "256 MiB buffer written before every timed step (cold L2)",
+            "inputs": "tactic-synth-v1 (synth/), seed = rank"}
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------ clocks (NVML sampling thread)
+class ClockSampler:
+    def __init__(self, dev_index: int, period_s: float = 0.002):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.period = period_s
+
+    def _run(self):
+        nv = self.nv
+        names = {}
+        for attr in ("nvmlClocksEventReasonHwSlowdown", "nvmlClocksEventReasonHwThermalSlowdown",
+                     "nvmlClocksEventReasonSwThermalSlowdown", "nvmlClocksEventReasonSwPowerCap",
+                     "nvmlClocksEventReasonHwPowerBrakeSlowdown"):
+            if hasattr(nv, attr):
+                names[getattr(nv, attr)] = attr.replace("nvmlClocksEventReason", "")
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, nm in names.items():
+                    if r & bit:
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ byte model
+def step_bytes(dbg, sizes, G, n, C):
+    """Algorithmic bytes of one layer-step: fp32 centroids, sampled K rows not re-read by the
+    attention, selected (union) K+V rows, q/out, from the selection the GPU actually made."""
+    from paper_2502_12216_b200.tactic import sample_constants
+    sc = sample_constants(n)
+    units = sizes.shape[0]
+    tot_union, tot_sampled_extra = 0, 0
+    for u in range(units):
+        off = np.concatenate([[0], np.cumsum(sizes[u])])
+        um = dbg["union_mask"][u]
+        tot_union += int(sizes[u][um].sum())
+        rows = set()
+        if sc["fallback"]:
+            continue
+        ranks = np.concatenate([np.arange(1, sc["N"] + 1), np.arange(sc["x1"] - sc["w"], sc["x1"] + sc["w"] + 1),
+                                np.arange(sc["x2"] - sc["w"], sc["x2"] + sc["w"] + 1)])
+        for g in range(G):
+            order = dbg["order"][u, g]
+            ends = np.cumsum(sizes[u][order])
+            r = np.searchsorted(ends, ranks, side="left")
+            cid = order[r]
+            start = ends[r] - sizes[u][cid]
+            row = off[cid] + (ranks - 1 - start)
+            sel = ~um[cid]
+            rows.update(row[sel].tolist())
+        tot_sampled_extra += len(rows)
+    cent = units * C * 128 * 4
+    qo = 2 * units * G * 128 * 2
+    attn = tot_union * 128 * 2 * 2
+    return {"centroids": cent, "sampled_k_extra": tot_sampled_extra * 256, "union_kv": attn, "q_out": qo,
+            "total": cent + tot_sampled_extra * 256 + attn + qo, "union_tokens": tot_union,
+            "union_frac": tot_union / (units * n)}
+
+
+# ------------------------------------------------------------------ reference arm (oracle on CPU)
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import tactic_oracle as O
+    from synth import make_unit
+    threads = _cpu_threads()
+    u = make_unit(CFG["n"], CFG["G"], seed=0, b=0, h=0)
+    idx, _ = O.build_index(u["K"], u["V"], CFG["C"], 1, seed=0, unit=0)   # setup, untimed
+    for _ in range(args.warmup):
+        O.decode_unit(u["q"], idx, args.p)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.decode_unit(u["q"], idx, args.p)
+        ts.append(time.perf_counter() - t0)
+    per_unit = float(np.mean(ts))
+    val = per_unit * CFG["B"] * CFG["Hkv"] * 1e6          # one layer-step = 8 units
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": val / 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": _config(args, world),
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"1 of 8 units per step (KV head 0, n=131072, C=1024; index from 1 oracle "
+                                       f"Lloyd iteration, untimed), scaled x8 to a layer-step"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        if info:
+            return int(max(i.get("num_threads", 1) for i in info))
+    except Exception:
+        pass
+    return len(os.sched_getaffinity(0))
+
+
+def cpu_baseline(args, budget_s=12.0):
+    """Time the oracle decode (as it stands) on a bounded sample of the C2 workload."""
+    from oracle import tactic_oracle as O
+    from synth import make_unit
+    u = make_unit(CFG["n"], CFG["G"], seed=0, b=0, h=0)
+    idx, _ = O.build_index(u["K"], u["V"], CFG["C"], 1, seed=0, unit=0)
+    O.decode_unit(u["q"], idx, args.p)
+    ts, t_start = [], time.perf_counter()
+    while time.perf_counter() - t_start < budget_s or len(ts) < 3:
+        t0 = time.perf_counter()
+        O.decode_unit(u["q"], idx, args.p)
+        ts.append(time.perf_counter() - t0)
+        if len(ts) >= 400:
+            break
+    val = float(np.mean(ts)) * CFG["B"] * CFG["Hkv"] * 1e6
+    return {"value": val, "unit": UNIT, "cores": _cpu_threads(), "kind": "oracle",
+            "sample": f"{len(ts)} oracle decode_unit calls on KV head 0 of C2 (n=131072, C=1024, G=4, p={args.p}; "
+                      f"index from 1 untimed oracle Lloyd iteration), mean x 8 units = one layer-step"}
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2502_12216_b200 import build as B
+    B.build()
+    from paper_2502_12216_b200 import tactic as T
+    from synth import make_layer
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    T.device_check()
+    G, n, C = CFG["G"], CFG["n"], CFG["C"]
+    K, V, q = make_layer(CFG["B"], CFG["Hkv"], G, n, seed=rank)
+    to = lambda a: torch.from_numpy(a).to(dev).to(torch.bfloat16)  # noqa: E731
+    Kd, Vd, qd = to(K), to(V), to(q)
+    del K, V
+    stream = torch.cuda.current_stream()
+
+    # ---- index build (tcgen05 k-means), timed separately
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    T.build_index(Kd[:, :1, :8192].contiguous(), Vd[:, :1, :8192].contiguous(), 64, 2, group_size=G)  # warm
+    torch.cuda.synchronize()
+    e0.record()
+    index = T.build_index(Kd, Vd, C, CFG["iters"], group_size=G, seed=rank)
+    e1.record()
+    torch.cuda.synchronize()
+    build_ms = e0.elapsed_time(e1)
+    ex = index.export()
+    iters_run = ex["iters_run"].tolist()
+    sizes = np.stack([np.bincount(ex["assign"][u], minlength=C) for u in range(index.units)])
+    alg_tflop = 2.0 * n * C * 128 * sum(iters_run) / 1e12
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    out = torch.empty_like(qd)
+
+    # ---- CUDA graph of one decode step
+    T.decode(qd, index, args.p, out=out)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        T.decode(qd, index, args.p, out=out)
+    torch.cuda.synchronize()
+
+    def timed_loop(fn, steps, flush_each=True):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for a, b in evs:
+            if flush_each:
+                flush.fill_(1)
+            a.record()
+            fn()
+            b.record()
+        return evs
+
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        g.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        evs = timed_loop(g.replay, args.steps)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        # keep the GPU busy a little longer for the clock sampler (not part of the number)
+        timed_loop(g.replay, min(args.steps, 200))
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- per-stage breakdown (selection / attention / merge), events between stages
+    st = []
+    for _ in range(max(20, min(args.steps, 200))):
+        flush.fill_(1)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        T.decode_profiled(qd, index, args.p, ev, out=out)
+        st.append(ev)
+    torch.cuda.synchronize()
+    sel_us = 1e3 * float(np.mean([e[0].elapsed_time(e[1]) for e in st]))
+    att_us = 1e3 * float(np.mean([e[1].elapsed_time(e[2]) for e in st]))
+    mrg_us = 1e3 * float(np.mean([e[2].elapsed_time(e[3]) for e in st]))
+
+    # ---- algorithmic bytes from the selection the GPU made
+    dbg = T.decode_debug(qd, index, args.p)
+    assert torch.equal(dbg["out"], out), "debug decode must reproduce the graph output"
+    bm = step_bytes(dbg, sizes, G, n, C)
+
+    # ---- dense baseline (own split-KV flash-decode over the caller's K/V)
+    dout = torch.empty_like(qd)
+    T.dense_decode(qd, Kd, Vd, out=dout)
+    gd = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gd):
+        T.dense_decode(qd, Kd, Vd, out=dout)
+    for _ in range(3):
+        gd.replay()
+    torch.cuda.synchronize()
+    devs = timed_loop(gd.replay, max(10, min(args.steps, 100)))
+    torch.cuda.synchronize()
+    dense_ms = float(np.mean([a.elapsed_time(b) for a, b in devs]))
+    dense_bytes = 2 * index.units * n * 128 * 2 + 2 * index.units * G * 128 * 2
+
+    # ---- e2e through the C ABI with host buffers (H2D q, D2H out inside the timed region)
+    q_host = qd.cpu().pin_memory()
+    o_host = torch.empty_like(q_host).pin_memory()
+    for _ in range(3):
+        T.decode_host(q_host, index, args.p, o_host)
+    e2e = []
+    for _ in range(max(10, min(args.steps, 200))):
+        flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        T.decode_host(q_host, index, args.p, o_host)
+        b.record()
+        torch.cuda.synchronize()
+        e2e.append(a.elapsed_time(b))
+    e2e_ms = float(np.mean(e2e))
+    if world > 1:
+        t = torch.tensor([e2e_ms, dense_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms, dense_ms = float(t[0]), float(t[1])
+
+    if rank != 0:
+        return
+    peaks = _peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING)"
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    attn_bytes = bm["union_kv"] + bm["q_out"] // 2 + (n_sm + index.units) * G * 129 * 4   # K/V, q, partials
+    att_gbs = attn_bytes / (att_us * 1e-6) / 1e9
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tr.get("attention_kernel_sparse_bytes_per_launch")
+    except Exception:
+        pass
+    value_us = ms * 1e3 / world
+    line = {
+        "metric": METRIC, "value": value_us, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": _config(args, world),
+        "gpu_launches": 6 * args.steps,
+        "roofline": {"bound": "hbm", "kernel": "attention_kernel<4,false> (S8 sparse split-KV)",
+                     "achieved": att_gbs, "peak": hbm, "unit": "GB/s", "frac": att_gbs / hbm,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "bytes_per_launch": attn_bytes, "us_per_launch": att_us},
+        "step_roofline": {"bytes_per_step": bm["total"], "achieved_gbs": bm["total"] / (ms * 1e-3) / 1e9,
+                          "frac": bm["total"] / (ms * 1e-3) / 1e9 / hbm, "bytes": bm},
+        "stages_us": {"selection_S1_S7": sel_us, "attention_S8": att_us, "merge_S9": mrg_us},
+        "dense": {"us_per_layer_step": dense_ms * 1e3, "gbs": dense_bytes / (dense_ms * 1e-3) / 1e9,
+                  "frac": dense_bytes / (dense_ms * 1e-3) / 1e9 / hbm, "bytes": dense_bytes},
+        "speedup_vs_dense": dense_ms / ms,
+        "select_cluster_size": index.info()["select_cluster_size"],
+        "build": {"ms": build_ms, "iters_run": iters_run, "alg_tflop": alg_tflop,
+                  "alg_tflops": alg_tflop / (build_ms * 1e-3),
+                  "exec_tflops_split_bf16": 2 * alg_tflop / (build_ms * 1e-3)},
+        "e2e": {"value": e2e_ms * 1e3 / world, "unit": UNIT, "h2d_bytes_per_step": int(qd.numel() * 2),
+                "d2h_bytes_per_step": int(qd.numel() * 2)},
+        "clocks": clk.summary(),
+        "context": PAPER_CONTEXT,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--p", type=float, default=0.9)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpu(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -77,6 +77,8 @@ typedef struct {
 typedef struct {
   int32_t units, batch, num_kv_heads, group_size, seq_len, n_clusters;
   int32_t iters_requested;
+  int32_t select_cluster_size;  /* CTAs per unit of the fused S1-S7 cluster kernel (0 = the
+                                   multi-kernel selection path)                          */
   int64_t device_bytes;         /* bytes the index holds on the device                   */
 } tactic_index_info_t;
 
@@ -119,6 +121,10 @@ tactic_status_t tactic_index_export(tactic_index_t idx, float* centroids, int32_
                                     double* inertia, int32_t* iters_run, void* stream);
 
 tactic_status_t tactic_index_info(tactic_index_t idx, tactic_index_info_t* info);
+/* Debug: per-phase %globaltimer stamps of the fused selection kernel's last launch,
+ * host uint64 [units][16][8] (CTA rank < 16, phase < 8).  Only for indices created with
+ * the environment variable TACTIC_TLOG=1; synchronises the device.                   */
+tactic_status_t tactic_index_debug_timing(tactic_index_t idx, uint64_t* host, int32_t count);
 void tactic_index_destroy(tactic_index_t idx);
 
 /* ---------------------------------------------------------------------------------------
@@ -155,10 +161,20 @@ tactic_status_t tactic_decode_debug(const void* q, tactic_index_t idx, float p, 
                                     float* lse, int32_t* order, int32_t* J, double* fit,
                                     uint8_t* union_mask, void* stream);
 
+/* Per-stage timing (Fig. 9-style breakdown): same work as tactic_decode_ex, but
+ * records the caller's CUDA events (cudaEvent_t passed as void*) on `stream`:
+ *   events[0] before S1, events[1] after S7 (selection), events[2] after S8 + S9 (the
+ *   merge is fused into the attention kernel), events[3] right after events[2].
+ *   n_events must be 4.  Stage boundaries are serialised.  */
+tactic_status_t tactic_decode_profiled(const void* q, tactic_index_t idx, float p, void* out,
+                                       void* const* events, int32_t n_events, void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * The library's own dense baseline (full attention, Eq. 1-2):
  * split-KV flash-decode over all n tokens of every unit of the caller's K/V, then LSE
- * merge.  Needs a caller workspace of tactic_dense_workspace_size() bytes.            */
+ * merge.  Needs a caller workspace of tactic_dense_workspace_size() bytes, zero-filled
+ * once when allocated (it holds self-resetting arrival counters; the library leaves it
+ * zeroed after every call).                                                           */
 tactic_status_t tactic_dense_workspace_size(const tactic_kv_desc_t* kv, int32_t num_ctas,
                                             size_t* bytes);
 tactic_status_t tactic_dense_decode(const void* q, const void* K, const void* V,

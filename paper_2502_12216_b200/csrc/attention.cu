@@ -1,4 +1,5 @@
-// attention.cu -- S8/S10 split-KV flash-decode over a token work list and S9 LSE merge.
+// attention.cu -- S8/S10 split-KV flash-decode over a token work list, with the S9 LSE
+// merge fused in (the last CTA to finish a unit merges that unit's partials).
 //
 // One kernel serves the sparse path (the GQA union of selected clusters) and
 // the dense baseline (all n tokens of the caller's K/V, Eq. 1-2).
@@ -9,7 +10,8 @@
 // Per CTA: 1 producer warp streams 64-token stages of K and V into shared memory
 //   sparse: cp.async.bulk (1-D TMA, UBLKCP) of contiguous cluster runs from the
 //           cluster-permuted, row-swizzled index layout; a run is placed at a slot
-//           congruent to its row mod 8 so the swizzle survives the copy.
+//           congruent to its row mod 8 so the swizzle survives the copy.  The run table
+//           (row start, token prefix) is read 32 segments at a time into registers.
 //   dense : cp.async.bulk.tensor (UTMALDG) 64x64 boxes, SWIZZLE_128B, from the caller's
 //           [B][Hkv][n][128] cache.
 // 4 consumer warps each own 16 token slots of a stage:
@@ -17,7 +19,8 @@
 //   the G<=8 query heads sit in the n=8 dimension), online softmax in the exp2 domain,
 //   P^T transposed in registers with movmatrix, O^T(128 x 8) += V^T P^T.
 // A piece (the part of one unit inside a CTA's range) ends with a cross-warp LSE
-// combine and one partial (o, lse) per head written to slot blockIdx.x + unit.
+// combine and one partial (o, lse) per head written to slot blockIdx.x + unit; a per-unit
+// arrival counter elects the last CTA of the unit, which merges its pieces (S9).
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -39,12 +42,6 @@ struct __align__(16) StageMeta {
   int flags;
 };
 
-struct AttnSmem {
-  // stage buffers first (1024-aligned for SWIZZLE_128B TMA destinations)
-  // [ATT_STAGES][K 16KB | V 16KB]
-  // then: meta, barriers, combine scratch
-};
-
 constexpr int SCRATCH_FLOATS = ATT_CWARPS * (8 * 128 + 16);
 constexpr size_t ATT_SMEM = (size_t)ATT_STAGES * ATT_STAGE_BYTES + ATT_STAGES * sizeof(StageMeta) +
                             2 * ATT_STAGES * sizeof(uint64_t) + SCRATCH_FLOATS * sizeof(float) + 1024;
@@ -58,6 +55,38 @@ __device__ __forceinline__ uint32_t tile_off(int s, int c) {
   return (uint32_t)(s * 256 + (swz_chunk(c, s) << 4));
 }
 
+__device__ __forceinline__ int pieces_of_unit(long long us, long long ue, long long T, int P, int* c0) {
+  const int a = cta_of(us, T, P), b = cta_of(ue - 1, T, P);
+  *c0 = a;
+  if (T >= P) return b - a + 1;
+  int cnt = 0;
+  for (int c = a; c <= b; ++c) cnt += range_start(c, T, P) != range_start(c + 1, T, P);
+  return cnt;
+}
+
+// Warp-cooperative search (all 32 lanes call it): largest index i in [0, count) with
+// arr[i] <= key, for a non-decreasing arr with arr[0] <= key.  One coalesced probe of
+// 32 entries per round: 2 round trips for count <= 1024 instead of a 10-step chain.
+template <typename T>
+__device__ __forceinline__ int warp_floor_search(const T* arr, int count, T key) {
+  const int lane = threadIdx.x & 31;
+  int base = 0, len = count;
+  while (len > 32) {
+    const int stride = (len + 31) >> 5;
+    const int idx = base + lane * stride;
+    const bool ok = idx < base + len && arr[idx] <= key;
+    const unsigned bal = __ballot_sync(0xffffffffu, ok);
+    const int h = 31 - __clz(bal);
+    const int nb = base + h * stride;
+    const int end = base + len;
+    base = nb;
+    len = (nb + stride < end ? nb + stride : end) - nb;
+  }
+  const bool ok = lane < len && arr[base + lane] <= key;
+  const unsigned bal = __ballot_sync(0xffffffffu, ok);
+  return base + (31 - __clz(bal));
+}
+
 template <int G, bool DENSE>
 __global__ void __launch_bounds__(ATT_THREADS, 1)
     attention_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tmK,
@@ -69,6 +98,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   uint64_t* full = (uint64_t*)(meta + ATT_STAGES);
   uint64_t* empty = full + ATT_STAGES;
   float* scratch = (float*)(empty + ATT_STAGES);
+  __shared__ int s_merge;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // zero the stage buffers once: never-written slots must hold finite values (0 * NaN)
@@ -83,128 +113,140 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   }
   fence_proxy_async_smem();
   __syncthreads();
+  if (DENSE && threadIdx.x == 0) {
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+  }
   pdl_wait();  // inputs (work list, q) are produced by the previous kernel
 
   const int P = gridDim.x, cta = blockIdx.x;
+  // debug stamps of CTA 0 (tlog != nullptr): [0] after pdl_wait, [2+t] tile t issued,
+  // [18+t] tile t consumed, [34] kernel end
+  auto stamp = [&](int i) {
+    if (a.tlog && cta == 0) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      a.tlog[192 + i] = t_;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
+  int ntile_dbg = 0;
+  const long long T = DENSE ? dense_total : a.unit_prefix[a.units];
 
   if (warp == 0) {
-    // ============================ producer ============================
-    if (lane == 0) {
+    // ============================ producer (warp-uniform control flow) ============================
+    const bool leader = lane == 0;
+    long long t = range_start(cta, T, P);
+    const long long t_end = range_start(cta + 1, T, P);
+    int stage = 0;
+    uint32_t phase = 0;
+    int u = 0;
+    if (t < t_end) {
       if (DENSE) {
-        prefetch_tmap(&tmK);
-        prefetch_tmap(&tmV);
+        u = (int)(t / a.n);
+      } else {  // largest u with unit_prefix[u] <= t
+        u = warp_floor_search<long long>(a.unit_prefix, a.units, t);
       }
-      const long long T = DENSE ? dense_total : a.unit_prefix[a.units];
-      long long t = range_start(cta, T, P);
-      const long long t_end = range_start(cta + 1, T, P);
-      int stage = 0;
-      uint32_t phase = 0;
-      int u = 0;
-      if (t < t_end) {
+    }
+    while (t < t_end) {
+      const long long ubase = DENSE ? (long long)u * a.n : a.unit_prefix[u];
+      const long long uend = DENSE ? ubase + a.n : a.unit_prefix[u + 1];
+      const long long pend = uend < t_end ? uend : t_end;
+      int lt = (int)(t - ubase);
+      const int le = (int)(pend - ubase);
+      // sparse: run table window of 32 segments (lane i holds segment k0 + i)
+      const int* seg_row = a.seg_row + (size_t)u * a.C;
+      const int* seg_pref = a.seg_prefix + (size_t)u * (a.C + 1);
+      int k = 0, k0 = 0, row = 0, left = 0, w_row = 0, w_end = 0;
+      if (!DENSE) {
+        k = k0 = warp_floor_search<int>(seg_pref, a.C, lt);  // largest k with seg_pref[k] <= lt
+        w_row = (k0 + lane < a.C) ? seg_row[k0 + lane] : 0;
+        w_end = (k0 + lane < a.C) ? seg_pref[k0 + lane + 1] : 0;
+        const int sp = seg_pref[k];
+        row = __shfl_sync(0xffffffffu, w_row, 0) + (lt - sp);
+        left = __shfl_sync(0xffffffffu, w_end, 0) - lt;
+      }
+      bool first = true;
+      while (lt < le) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sK = stages + stage * ATT_STAGE_BYTES;
+        uint8_t* sV = sK + ATT_STAGE_BYTES / 2;
+        unsigned long long mask = 0;
         if (DENSE) {
-          u = (int)(t / a.n);
-        } else {  // largest u with unit_prefix[u] <= t
-          int lo = 0, hi = a.units - 1;
-          while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (a.unit_prefix[mid] <= t) lo = mid; else hi = mid - 1;
-          }
-          u = lo;
-        }
-      }
-      while (t < t_end) {
-        const long long ubase = DENSE ? (long long)u * a.n : a.unit_prefix[u];
-        const long long uend = DENSE ? ubase + a.n : a.unit_prefix[u + 1];
-        const long long pend = uend < t_end ? uend : t_end;
-        int lt = (int)(t - ubase);
-        const int le = (int)(pend - ubase);
-        // sparse cursor: segment k of the unit's list holding local token lt
-        const int* seg_list = a.seg_list + (size_t)u * a.C;
-        const int* seg_pref = a.seg_prefix + (size_t)(u) * (a.C + 1);
-        const int* offs = a.offsets + (size_t)u * (a.C + 1);
-        int k = 0, row = 0, left = 0;
-        if (!DENSE) {
-          int lo = 0, hi = a.C - 1;  // largest k with seg_pref[k] <= lt
-          while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (seg_pref[mid] <= lt) lo = mid; else hi = mid - 1;
-          }
-          k = lo;
-          const int cid = seg_list[k];
-          row = offs[cid] + (lt - seg_pref[k]);
-          left = seg_pref[k + 1] - lt;
-        }
-        bool first = true;
-        while (lt < le) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sK = stages + stage * ATT_STAGE_BYTES;
-          uint8_t* sV = sK + ATT_STAGE_BYTES / 2;
-          unsigned long long mask = 0;
-          uint32_t bytes = 0;
-          if (DENSE) {
-            const int cnt = (le - lt) < ATT_TILE ? (le - lt) : ATT_TILE;
-            mask = cnt == 64 ? ~0ull : ((1ull << cnt) - 1ull);
-            bytes = ATT_STAGE_BYTES;
+          const int cnt = (le - lt) < ATT_TILE ? (le - lt) : ATT_TILE;
+          mask = cnt == 64 ? ~0ull : ((1ull << cnt) - 1ull);
+          if (leader) {
             meta[stage].mask = mask;
             meta[stage].unit = u;
             meta[stage].flags = (first ? FLAG_FIRST : 0) | (lt + cnt >= le ? FLAG_LAST : 0);
-            mbar_arrive_expect_tx(&full[stage], bytes);
+            mbar_arrive_expect_tx(&full[stage], ATT_STAGE_BYTES);
             const int b = u / a.Hkv, h = u % a.Hkv;
             tma_load_4d(sK, &tmK, 0, lt, h, b, &full[stage]);
             tma_load_4d(sK + 8192, &tmK, 64, lt, h, b, &full[stage]);
             tma_load_4d(sV, &tmV, 0, lt, h, b, &full[stage]);
             tma_load_4d(sV + 8192, &tmV, 64, lt, h, b, &full[stage]);
-            lt += cnt;
-          } else {
-            // place runs: first compute the run list (slot, row, len), then one
-            // arrive.expect_tx, then the copies
-            int rs_slot[ATT_TILE / 8 + 8], rs_row[ATT_TILE / 8 + 8], rs_len[ATT_TILE / 8 + 8];
-            int nr = 0, s = 0;
-            while (s < ATT_TILE && lt < le) {
-              int avail = left < (le - lt) ? left : (le - lt);
-              int s0 = s + ((row - s) & 7);
-              if (s0 >= ATT_TILE) break;
-              int L = avail < (ATT_TILE - s0) ? avail : (ATT_TILE - s0);
-              if (nr > 0 && rs_slot[nr - 1] + rs_len[nr - 1] == s0 && rs_row[nr - 1] + rs_len[nr - 1] == row) {
-                rs_len[nr - 1] += L;  // contiguous with the previous run
-              } else {
-                rs_slot[nr] = s0; rs_row[nr] = row; rs_len[nr] = L; ++nr;
+          }
+          lt += cnt;
+        } else {
+          uint32_t bytes = 0;
+          int s = 0;
+          int r_slot = -1, r_row = 0, r_len = 0;  // pending run (merged while contiguous)
+          const size_t ubytes = (size_t)u * a.n * 256;
+          while (s < ATT_TILE && lt < le) {
+            const int avail = left < (le - lt) ? left : (le - lt);
+            const int s0 = s + ((row - s) & 7);
+            if (s0 >= ATT_TILE) break;
+            const int L = avail < (ATT_TILE - s0) ? avail : (ATT_TILE - s0);
+            if (r_slot >= 0 && r_slot + r_len == s0 && r_row + r_len == row) {
+              r_len += L;
+            } else {
+              if (r_slot >= 0 && leader) {
+                bulk_g2s(sK + r_slot * 256, (const uint8_t*)a.Kp + ubytes + (size_t)r_row * 256, r_len * 256u,
+                         &full[stage]);
+                bulk_g2s(sV + r_slot * 256, (const uint8_t*)a.Vp + ubytes + (size_t)r_row * 256, r_len * 256u,
+                         &full[stage]);
               }
-              mask |= (L == 64 ? ~0ull : ((1ull << L) - 1ull)) << s0;
-              s = s0 + L;
-              row += L;
-              lt += L;
-              left -= L;
-              if (left == 0 && lt < le) {
-                ++k;
-                const int cid = seg_list[k];
-                row = offs[cid];
-                left = seg_pref[k + 1] - seg_pref[k];
-              }
-              if (nr == ATT_TILE / 8 + 8) break;
+              r_slot = s0; r_row = row; r_len = L;
             }
-            for (int i = 0; i < nr; ++i) bytes += (uint32_t)rs_len[i] * 512u;
+            mask |= (L == 64 ? ~0ull : ((1ull << L) - 1ull)) << s0;
+            bytes += (uint32_t)L * 512u;
+            s = s0 + L;
+            row += L;
+            lt += L;
+            left -= L;
+            if (left == 0 && lt < le) {
+              ++k;
+              if (k - k0 == 32) {
+                k0 = k;
+                w_row = (k0 + lane < a.C) ? seg_row[k0 + lane] : 0;
+                w_end = (k0 + lane < a.C) ? seg_pref[k0 + lane + 1] : 0;
+              }
+              row = __shfl_sync(0xffffffffu, w_row, k - k0);
+              left = __shfl_sync(0xffffffffu, w_end, k - k0) - lt;
+            }
+          }
+          if (leader) {
+            bulk_g2s(sK + r_slot * 256, (const uint8_t*)a.Kp + ubytes + (size_t)r_row * 256, r_len * 256u,
+                     &full[stage]);
+            bulk_g2s(sV + r_slot * 256, (const uint8_t*)a.Vp + ubytes + (size_t)r_row * 256, r_len * 256u,
+                     &full[stage]);
             meta[stage].mask = mask;
             meta[stage].unit = u;
             meta[stage].flags = (first ? FLAG_FIRST : 0) | (lt >= le ? FLAG_LAST : 0);
             mbar_arrive_expect_tx(&full[stage], bytes);
-            const size_t ubytes = (size_t)u * a.n * 256;
-            for (int i = 0; i < nr; ++i) {
-              const uint32_t nb = (uint32_t)rs_len[i] * 256u;
-              bulk_g2s(sK + rs_slot[i] * 256, (const uint8_t*)a.Kp + ubytes + (size_t)rs_row[i] * 256, nb,
-                       &full[stage]);
-              bulk_g2s(sV + rs_slot[i] * 256, (const uint8_t*)a.Vp + ubytes + (size_t)rs_row[i] * 256, nb,
-                       &full[stage]);
-            }
           }
-          first = false;
-          if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
         }
-        t = pend;
-        ++u;
+        first = false;
+        if (leader && ntile_dbg < 16) stamp(2 + ntile_dbg);
+        ++ntile_dbg;
+        if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
       }
-      // end marker
-      mbar_wait(&empty[stage], phase ^ 1);
+      t = pend;
+      ++u;
+    }
+    // end marker
+    mbar_wait(&empty[stage], phase ^ 1);
+    if (leader) {
       meta[stage].flags = FLAG_END;
       meta[stage].mask = 0;
       meta[stage].unit = -1;
@@ -215,6 +257,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
 
   // ============================ consumers ============================
   const int cw = warp - 1;
+  const int ct = threadIdx.x - 32;          // 0..127 consumer thread index
   const int h0 = 2 * (lane & 3);            // heads held by this lane in C fragments
   const int r0 = lane >> 2;                 // token row (S^T) / dim row (O^T) in fragment
   const float scale_log2 = 1.4426950408889634f * 0.08838834764831845f;  // log2(e)/sqrt(128)
@@ -226,15 +269,16 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   uint32_t phase = 0;
 
   const uint32_t sbase = smem_u32(stages);
-  // ldmatrix lane -> (slot, chunk) mapping
-  const int a_slot = cw * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;  // K, non-trans
-  const int a_chi = lane >> 4;                                      // +0 / +1 chunk
-  const int v_slot = cw * 16 + (lane & 7) + (lane >> 4) * 8;         // V, trans
+  const int a_slot = cw * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;  // K, ldmatrix non-trans
+  const int a_chi = lane >> 4;
+  const int v_slot = cw * 16 + (lane & 7) + (lane >> 4) * 8;         // V, ldmatrix trans
   const int v_chi = (lane >> 3) & 1;
 
   while (true) {
     mbar_wait(&full[stage], phase);
     const StageMeta md = meta[stage];
+    if (ct == 0 && ntile_dbg < 16) stamp(18 + ntile_dbg);
+    ++ntile_dbg;
     if (md.flags & FLAG_END) break;
     if (md.flags & FLAG_FIRST) {
       if (md.unit != cur_unit) {
@@ -242,9 +286,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         const __nv_bfloat16* qu = a.q + (size_t)cur_unit * G * 128;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
-          const int hh = r0;  // B fragment: n = lane/4 (head), k = 2*(lane%4)
-          if (hh < G) {
-            const uint32_t* qrow = reinterpret_cast<const uint32_t*>(qu + hh * 128);
+          if (r0 < G) {  // B fragment: n = lane/4 (head), k = 2*(lane%4)
+            const uint32_t* qrow = reinterpret_cast<const uint32_t*>(qu + r0 * 128);
             qb[ks][0] = qrow[(ks * 16 + h0) >> 1];
             qb[ks][1] = qrow[(ks * 16 + 8 + h0) >> 1];
           } else {
@@ -271,10 +314,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       }
       // s[0],s[1]: token r0, heads h0,h0+1 ; s[2],s[3]: token r0+8
       const bool v_lo = (mym >> r0) & 1u, v_hi = (mym >> (r0 + 8)) & 1u;
-      float x0 = v_lo ? s[0] * scale_log2 : -INFINITY;
-      float x1 = v_lo ? s[1] * scale_log2 : -INFINITY;
-      float x2 = v_hi ? s[2] * scale_log2 : -INFINITY;
-      float x3 = v_hi ? s[3] * scale_log2 : -INFINITY;
+      const float x0 = v_lo ? s[0] * scale_log2 : -INFINITY;
+      const float x1 = v_lo ? s[1] * scale_log2 : -INFINITY;
+      const float x2 = v_hi ? s[2] * scale_log2 : -INFINITY;
+      const float x3 = v_hi ? s[3] * scale_log2 : -INFINITY;
       float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
 #pragma unroll
       for (int off = 4; off < 32; off <<= 1) {
@@ -307,7 +350,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
 
     if (md.flags & FLAG_LAST) {
-      // ---- cross-warp combine of this piece
+      // ---- cross-warp combine of this piece -> partial slot (cta + unit)
       float L0 = l0, L1 = l1;
 #pragma unroll
       for (int off = 4; off < 32; off <<= 1) {
@@ -330,8 +373,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         sw[(h0 + 1) * 128 + d0 + 8] = o[mt][3];
       }
       asm volatile("bar.sync 1, %0;" ::"n"(ATT_CWARPS * 32));
-      const int dim = threadIdx.x - 32;
-      const size_t slot = (size_t)cta + md.unit;
+      const int u = md.unit;
+      const size_t slot = (size_t)cta + u;
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         float mf = -INFINITY;
@@ -343,67 +386,85 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           const float* sww = scratch + w * (8 * 128 + 16);
           const float e = exp2f(sww[8 * 128 + g] - mf);
           lf += sww[8 * 128 + 8 + g] * e;
-          of += sww[g * 128 + dim] * e;
+          of += sww[g * 128 + ct] * e;
         }
-        a.part_o[(slot * G + g) * 128 + dim] = of / lf;
-        if (dim == 0) a.part_lse[slot * G + g] = (mf + log2f(lf)) * 0.6931471805599453f;
+        a.part_o[(slot * G + g) * 128 + ct] = of / lf;
+        if (ct == 0) a.part_lse[slot * G + g] = (mf + log2f(lf)) * 0.6931471805599453f;
+      }
+      // ---- arrival: is this the unit's last piece?
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"n"(ATT_CWARPS * 32));
+      const long long us = DENSE ? (long long)u * a.n : a.unit_prefix[u];
+      const long long ue = DENSE ? us + a.n : a.unit_prefix[u + 1];
+      int c0 = 0;
+      const int np = pieces_of_unit(us, ue, T, P, &c0);
+      if (ct == 0) {
+        const int prev = atomicAdd(&a.unit_cnt[u], 1);
+        s_merge = (prev == np - 1);
       }
       asm volatile("bar.sync 1, %0;" ::"n"(ATT_CWARPS * 32));
+      if (s_merge) {
+        // ---- S9: merge this unit's pieces (slots c + u), LSE-weighted
+        __threadfence();
+        // warp w merges heads w, w+4, ...; lanes hold 4 dims; piece weights are computed
+        // 32 at a time (one per lane) and broadcast, so the o loads are independent.
+        const int c1 = cta_of(ue - 1, T, P);
+        const int span = c1 - c0 + 1;
+        for (int g = cw; g < G; g += ATT_CWARPS) {
+          float mx = -INFINITY;
+          for (int i = lane; i < span; i += 32) {
+            const int c = c0 + i;
+            if (T >= P || range_start(c, T, P) != range_start(c + 1, T, P))
+              mx = fmaxf(mx, __ldcg(a.part_lse + ((size_t)c + u) * G + g));
+          }
+          mx = warp_max(mx);
+          float sum = 0.f;
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int i0 = 0; i0 < span; i0 += 32) {
+            const int i = i0 + lane;
+            float wl = 0.f;
+            if (i < span && (T >= P || range_start(c0 + i, T, P) != range_start(c0 + i + 1, T, P)))
+              wl = __expf(__ldcg(a.part_lse + ((size_t)(c0 + i) + u) * G + g) - mx);
+            sum += wl;
+            const int cnt = span - i0 < 32 ? span - i0 : 32;
+#pragma unroll 8
+            for (int j = 0; j < cnt; ++j) {
+              const float w = __shfl_sync(0xffffffffu, wl, j);
+              const float4* src =
+                  reinterpret_cast<const float4*>(a.part_o + (((size_t)(c0 + i0 + j) + u) * G + g) * 128) + lane;
+              const float4 v = w != 0.f ? __ldcg(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+              acc.x = fmaf(w, v.x, acc.x);
+              acc.y = fmaf(w, v.y, acc.y);
+              acc.z = fmaf(w, v.z, acc.z);
+              acc.w = fmaf(w, v.w, acc.w);
+            }
+          }
+          sum = warp_sum(sum);
+          const float inv = 1.f / sum;
+          const size_t orow = ((size_t)u * G + g) * 128 + lane * 4;
+          if (a.out) {
+            __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(a.out + orow);
+            ob[0] = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+            ob[1] = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+          }
+          if (a.out_f32)
+            *reinterpret_cast<float4*>(a.out_f32 + orow) =
+                make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+          if (a.lse && lane == 0) a.lse[(size_t)u * G + g] = mx + logf(sum);
+        }
+        if (ct == 0) a.unit_cnt[u] = 0;  // self-reset for the next call
+      }
       m0 = m1 = -INFINITY;
       l0 = l1 = 0.f;
 #pragma unroll
       for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
     }
   }
+  if (ct == 0) stamp(34);
   pdl_launch_dependents();
 }
 
-// ---------------------------------------------------------------------------- merge (S9)
-// One warp per (unit, head): pieces are slots c + u for the CTAs c whose range meets the
-// unit; lse = logsumexp lse_s, o = sum_s exp(lse_s - lse) o_s.
-__global__ void merge_kernel(const float* __restrict__ part_o, const float* __restrict__ part_lse,
-                             const long long* __restrict__ unit_prefix, int n, int units, int G, int P,
-                             __nv_bfloat16* __restrict__ out, float* __restrict__ out_f32,
-                             float* __restrict__ lse_out) {
-  pdl_wait();
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= units * G) return;
-  const int u = warp / G, g = warp % G;
-  const long long T = unit_prefix ? unit_prefix[units] : (long long)units * n;
-  const long long us = unit_prefix ? unit_prefix[u] : (long long)u * n;
-  const long long ue = unit_prefix ? unit_prefix[u + 1] : (long long)(u + 1) * n;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  float mx = -INFINITY, sum = 0.f;
-  if (ue > us) {
-    const int c0 = cta_of(us, T, P), c1 = cta_of(ue - 1, T, P);
-    for (int c = c0; c <= c1; ++c) {
-      if (range_start(c, T, P) == range_start(c + 1, T, P)) continue;
-      const size_t slot = (size_t)c + u;
-      const float l = part_lse[slot * G + g];
-      if (l == -INFINITY) continue;
-      const float4 ov = *reinterpret_cast<const float4*>(part_o + (slot * G + g) * 128 + lane * 4);
-      const float mn = fmaxf(mx, l);
-      const float sc = expf(mx - mn), w = expf(l - mn);
-      acc[0] = acc[0] * sc + w * ov.x;
-      acc[1] = acc[1] * sc + w * ov.y;
-      acc[2] = acc[2] * sc + w * ov.z;
-      acc[3] = acc[3] * sc + w * ov.w;
-      sum = sum * sc + w;
-      mx = mn;
-    }
-  }
-  const float inv = sum > 0.f ? 1.f / sum : 0.f;
-  if (out) {
-    __nv_bfloat162* orow = reinterpret_cast<__nv_bfloat162*>(out + ((size_t)u * G + g) * 128 + lane * 4);
-    orow[0] = __floats2bfloat162_rn(acc[0] * inv, acc[1] * inv);
-    orow[1] = __floats2bfloat162_rn(acc[2] * inv, acc[3] * inv);
-  }
-  if (out_f32)
-    *reinterpret_cast<float4*>(out_f32 + ((size_t)u * G + g) * 128 + lane * 4) =
-        make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-  if (lse_out && lane == 0) lse_out[u * G + g] = sum > 0.f ? mx + logf(sum) : -INFINITY;
-}
-
+// ---------------------------------------------------------------------------- plain merge
 __global__ void lse_merge_plain_kernel(const float* __restrict__ o_parts, const float* __restrict__ lse_parts,
                                        int n_parts, int n_rows, __nv_bfloat16* __restrict__ out,
                                        float* __restrict__ lse_out) {
@@ -476,23 +537,6 @@ cudaError_t launch_attention_sparse(const AttnArgs& a, int G, int num_ctas, cuda
 cudaError_t launch_attention_dense(const AttnArgs& a, const CUtensorMap* tmK, const CUtensorMap* tmV, int G,
                                    int num_ctas, cudaStream_t s, bool pdl) {
   return launch_attn_g<true>(a, tmK, tmV, G, num_ctas, s, pdl);
-}
-
-cudaError_t launch_merge(const float* part_o, const float* part_lse, const long long* unit_prefix, int n,
-                         int units, int G, int num_ctas, __nv_bfloat16* out, float* out_f32, float* lse,
-                         cudaStream_t s, bool pdl) {
-  const int warps = units * G;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((warps + 7) / 8);
-  cfg.blockDim = dim3(256);
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, merge_kernel, part_o, part_lse, unit_prefix, n, units, G, num_ctas, out, out_f32,
-                            lse);
 }
 
 cudaError_t launch_lse_merge_plain(const float* o_parts, const float* lse_parts, int n_parts, int n_rows,

@@ -47,19 +47,23 @@ struct tactic_index_s {
   int* perm = nullptr;           // [units][n] original token ids in layout order
   int* assign = nullptr;         // [units][n]
   int* iters_run = nullptr;      // [units]
-  int* all_list = nullptr;       // [units][C]  non-empty clusters (p >= 1 work list)
+  int* all_list = nullptr;       // [units][C]  rows of non-empty clusters (p >= 1 work list)
+  int* unit_cnt = nullptr;       // [units] attention arrival counters
   int* all_prefix = nullptr;     // [units][C+1]
   long long* all_unit_prefix = nullptr;  // [units+1]
   // decode workspace
   double* crit = nullptr;        // [units][G][C]
   int* order = nullptr;          // [units][G][C]
   int* ends = nullptr;           // [units][G][C]
+  int* rowstart = nullptr;       // [units][G][C] first layout row of the r-th ranked cluster
+  uint8_t* mask_acc = nullptr;   // [units][C] union accumulator (zero between calls)
+  unsigned int* head_cnt = nullptr;  // [units] selection arrival counters
   float* logits = nullptr;       // [units][G][slots]
   double* fit = nullptr;         // [units][G][6]
   double* cumend = nullptr;      // [units][G][C] (sharded stage 1)
   int* J = nullptr;              // [units][G]
   uint8_t* umask = nullptr;      // [units][C]
-  int* union_list = nullptr;     // [units][C]
+  int* union_list = nullptr;     // [units][C] first layout row of each union segment
   int* union_prefix = nullptr;   // [units][C+1]
   long long* unit_prefix = nullptr;  // [units+1]
   unsigned int* counter = nullptr;   // last-block counter (self-resetting)
@@ -69,6 +73,8 @@ struct tactic_index_s {
   __nv_bfloat16* q_stage = nullptr;  // [units][G][128] (host-buffer decode)
   __nv_bfloat16* o_stage = nullptr;
   long long device_bytes = 0;
+  int fused_R = 0;               // CTAs per unit of the fused selection kernel (0: multi-kernel path)
+  unsigned long long* tlog = nullptr;  // [units][16][8] phase timestamps (TACTIC_TLOG=1)
 };
 
 namespace tactic {
@@ -78,21 +84,21 @@ struct AttnArgs {
   const __nv_bfloat16* q;          // [units][G][128]
   const __nv_bfloat16* Kp;         // sparse mode: swizzled [units][n][128]
   const __nv_bfloat16* Vp;
-  const int* seg_list;             // [units][C]
-  const int* seg_prefix;           // [units][C+1]
-  const int* offsets;              // [units][C+1]
+  const int* seg_row;              // [units][C] first layout row of each work-list segment
+  const int* seg_prefix;           // [units][C+1] token prefix over the segments
   const long long* unit_prefix;    // [units+1] (sparse)
   int n, C, units, Hkv;
-  float* part_o;
-  float* part_lse;
+  float* part_o;                   // [num_ctas + units][G][128]
+  float* part_lse;                 // [num_ctas + units][G]
+  int* unit_cnt;                   // [units] arrival counters, zero between calls
+  __nv_bfloat16* out;              // nullable [units][G][128]
+  float* out_f32;                  // nullable
+  float* lse;                      // nullable [units][G]
+  unsigned long long* tlog;        // nullable debug timestamps (CTA 0)
 };
 cudaError_t launch_attention_sparse(const AttnArgs& a, int G, int num_ctas, cudaStream_t s, bool pdl);
 cudaError_t launch_attention_dense(const AttnArgs& a, const CUtensorMap* tmK, const CUtensorMap* tmV, int G,
                                    int num_ctas, cudaStream_t s, bool pdl);
-// merge: unit_prefix == nullptr means dense (u * n)
-cudaError_t launch_merge(const float* part_o, const float* part_lse, const long long* unit_prefix, int n,
-                         int units, int G, int num_ctas, __nv_bfloat16* out, float* out_f32, float* lse,
-                         cudaStream_t s, bool pdl);
 cudaError_t launch_lse_merge_plain(const float* o_parts, const float* lse_parts, int n_parts, int n_rows,
                                    __nv_bfloat16* out, float* lse, cudaStream_t s);
 size_t attention_smem_bytes();
@@ -113,6 +119,9 @@ cudaError_t launch_sort(const SelArgs& a, cudaStream_t s, bool pdl);
 cudaError_t launch_sample(const SelArgs& a, cudaStream_t s, bool pdl);
 cudaError_t launch_select(const SelArgs& a, cudaStream_t s, bool pdl);
 cudaError_t launch_stage1b(const SelArgs& a, cudaStream_t s);
+// fused S1-S7 (select_fused.cu)
+cudaError_t launch_select_fused(const __nv_bfloat16* q, tactic_index_s* x, double p, cudaStream_t s, bool pdl);
+int choose_fused_R(tactic_index_s* x);
 
 // ---- k-means / layout (kmeans.cu)
 struct KmArgs {

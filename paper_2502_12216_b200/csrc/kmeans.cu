@@ -448,7 +448,7 @@ __global__ void km_all_list_kernel(const KmArgs a, int iters) {
   int cb = bases[0], tb = bases[1];
   for (int j = j0; j < j0 + per && j < a.C; ++j)
     if (off[j + 1] > off[j]) {
-      ul[cb] = j;
+      ul[cb] = off[j];  // segment = first layout row of the cluster
       up[cb] = tb;
       ++cb;
       tb += off[j + 1] - off[j];

@@ -2,18 +2,25 @@
 //
 //  score_kernel   S1  crit[u][g][j] = q_g . c_j in float64 (products of a
 //                     bf16 query and a float32 centroid are exact in fp64, so only the
-//                     summation order differs from the oracle).
-//  sort_kernel    S2  bitonic sort of (-crit, j) per (unit, head) in shared memory;
-//                 S3  inclusive scan of cluster sizes in rank order -> end ranks e_r.
+//                     summation order differs from the oracle).  A warp scores 32/G
+//                     centroids for all G heads and reduce-scatters the 32 partial sums
+//                     with a shuffle butterfly (31 exchanges instead of 5 per value).
+//  rank_kernel    S2+S3 rank of every cluster in the order (-crit, id) and the token
+//                     rank where it starts, without a comparison sort: clusters are
+//                     bucketed by a monotone map of crit (1024 buckets), bucket counts /
+//                     token sums are scanned, and only clusters sharing a bucket are
+//                     compared.  Writes order (rank -> id), end ranks e_r, first layout
+//                     row of the r-th cluster.
 //  sample_kernel  S4  exact logits q.k/sqrt(d) of the sampled ranks: the first N ranks
 //                     and two windows of 2w+1 ranks around x1, x2 (Alg. 1 l.4,
-//                     readings 8-11); rank -> row through e_r, order, offsets.
-//  select_kernel  S4-S6 shift m, exact head weights + prefix, window means, two-point
-//                     fit y = a/x + b, estimated total W, minimal k with
-//                     cum(k) >= p W (Alg. 1 l.10) at cluster granularity
-//                     (reading 14); S7 union over the G heads, compacted work
-//                     list, and a global token prefix over units (sub-requests)
-//                     computed by the last block to finish.
+//                     readings 8-11); 16 rows in flight per warp.
+//  select_kernel  S4-S6 per (unit, head): shift m, exact head weights + prefix, window
+//                     means, two-point fit y = a/x + b, estimated total W,
+//                     minimal k with cum(k) >= p W (Alg. 1 l.10) at cluster
+//                     granularity (reading 14); marks the selected clusters.
+//                 S7  the last head of a unit to finish compacts the GQA union
+//                     into the attention work list; the last unit to finish writes the
+//                     global token prefix over units (sub-requests).
 // The clamp-aware tail sum  sum_{i=N+1}^{k} max(0, a/i + b)  uses harmonic numbers
 // from the asymptotic digamma series (exact sums below 20) instead of a table.
 #include <cuda_bf16.h>
@@ -26,15 +33,10 @@
 namespace tactic {
 
 constexpr int SEL_THREADS = 512;
+constexpr int RANK_THREADS = 512;
+constexpr int NBUCKET = 1024;
 
 // ------------------------------------------------------------------ helpers
-__device__ __forceinline__ unsigned long long desc_key(double x) {
-  if (x == 0.0) x = 0.0;  // -0 == +0
-  unsigned long long u = (unsigned long long)__double_as_longlong(x);
-  u = (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);  // ascending order
-  return ~u;                                                           // descending
-}
-
 __device__ double harmonic(long long k) {
   if (k <= 0) return 0.0;
   if (k < 20) {
@@ -75,26 +77,31 @@ template <typename T> __device__ __forceinline__ T lowest();
 template <> __device__ __forceinline__ float lowest<float>() { return -INFINITY; }
 template <> __device__ __forceinline__ double lowest<double>() { return -INFINITY; }
 template <> __device__ __forceinline__ int lowest<int>() { return INT_MIN; }
+template <typename T> __device__ __forceinline__ T highest();
+template <> __device__ __forceinline__ double highest<double>() { return INFINITY; }
 
-template <typename T>
-__device__ T block_reduce(T v, T* red, bool is_max) {
-  const T ident = is_max ? lowest<T>() : (T)0;
+enum { RED_SUM = 0, RED_MAX = 1, RED_MIN = 2 };
+
+template <typename T, int OP>
+__device__ __forceinline__ T red_op(T a, T b) {
+  if (OP == RED_SUM) return a + b;
+  if (OP == RED_MAX) return a > b ? a : b;
+  return a < b ? a : b;
+}
+
+template <typename T, int OP>
+__device__ T block_reduce(T v, T* red) {
+  const T ident = OP == RED_SUM ? (T)0 : (OP == RED_MAX ? lowest<T>() : highest<T>());
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    T x = __shfl_xor_sync(0xffffffffu, v, o);
-    v = is_max ? (x > v ? x : v) : v + x;
-  }
+  for (int o = 16; o > 0; o >>= 1) v = red_op<T, OP>(v, __shfl_xor_sync(0xffffffffu, v, o));
   __syncthreads();
   if (lane == 0) red[w] = v;
   __syncthreads();
   if (w == 0) {
     v = lane < nw ? red[lane] : ident;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      T x = __shfl_xor_sync(0xffffffffu, v, o);
-      v = is_max ? (x > v ? x : v) : v + x;
-    }
+    for (int o = 16; o > 0; o >>= 1) v = red_op<T, OP>(v, __shfl_xor_sync(0xffffffffu, v, o));
     if (lane == 0) red[0] = v;
   }
   __syncthreads();
@@ -157,95 +164,143 @@ __device__ long long block_lower_bound(long long lo, long long hi, Pred pred, lo
 }
 
 // ------------------------------------------------------------------ S1
+// Each warp scores CPW = 32/G centroids; value index v = jj*G + g ends on lane v.
 template <int G>
-__global__ void __launch_bounds__(128) score_kernel(const __nv_bfloat16* __restrict__ q,
+__global__ void __launch_bounds__(256) score_kernel(const __nv_bfloat16* __restrict__ q,
                                                     const float* __restrict__ cent, int C,
                                                     double* __restrict__ crit) {
+  constexpr int CPW = 32 / G;
   pdl_wait();
   const int u = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double qd[G][4];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    const __nv_bfloat16* qq = q + ((size_t)u * G + g) * 128 + lane * 4;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) qd[g][i] = (double)__bfloat162float(qq[i]);
+    const uint2 raw = *reinterpret_cast<const uint2*>(q + ((size_t)u * G + g) * 128 + lane * 4);
+    const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+    const float2 a = __bfloat1622float2(q2[0]), b = __bfloat1622float2(q2[1]);
+    qd[g][0] = a.x; qd[g][1] = a.y; qd[g][2] = b.x; qd[g][3] = b.y;
   }
-  const int j0 = blockIdx.x * 32 + warp * 8;
-  for (int jj = 0; jj < 8; ++jj) {
-    const int j = j0 + jj;
-    if (j >= C) break;
-    const float4 c = *reinterpret_cast<const float4*>(cent + ((size_t)u * C + j) * 128 + lane * 4);
+  const int j0 = (blockIdx.x * (blockDim.x >> 5) + warp) * CPW;
+  if (j0 >= C) return;
+  float4 c[CPW];
+#pragma unroll
+  for (int jj = 0; jj < CPW; ++jj)
+    c[jj] = j0 + jj < C ? *reinterpret_cast<const float4*>(cent + ((size_t)u * C + j0 + jj) * 128 + lane * 4)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+  double v[32];
+#pragma unroll
+  for (int jj = 0; jj < CPW; ++jj)
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      double s = qd[g][0] * (double)c.x;
-      s = fma(qd[g][1], (double)c.y, s);
-      s = fma(qd[g][2], (double)c.z, s);
-      s = fma(qd[g][3], (double)c.w, s);
-      s = warp_sum_d(s);
-      if (lane == 0) crit[((size_t)u * G + g) * C + j] = s;
+      double s = qd[g][0] * (double)c[jj].x;
+      s = fma(qd[g][1], (double)c[jj].y, s);
+      s = fma(qd[g][2], (double)c[jj].z, s);
+      s = fma(qd[g][3], (double)c[jj].w, s);
+      v[jj * G + g] = s;
+    }
+  // butterfly reduce-scatter: after the level with offset o, lanes keep the half of the
+  // values selected by their bit o; after 5 levels lane L holds the total of value L.
+#pragma unroll
+  for (int o = 16, half = 16; o >= 1; o >>= 1, half >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double send = upper ? v[i] : v[i + half];
+      const double keep = upper ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
     }
   }
+  const int jj = lane / G, g = lane % G;
+  if (j0 + jj < C) crit[((size_t)u * G + g) * C + j0 + jj] = v[0];
   pdl_launch_dependents();
 }
 
-// ------------------------------------------------------------------ S2 + S3
-__global__ void __launch_bounds__(SEL_THREADS) sort_kernel(const double* __restrict__ crit,
-                                                           const int* __restrict__ offsets, int C, int Cp,
-                                                           int G, int* __restrict__ order,
-                                                           int* __restrict__ ends) {
+// ------------------------------------------------------------------ S2 + S3 (bucket ranking)
+__global__ void __launch_bounds__(RANK_THREADS) rank_kernel(const double* __restrict__ crit,
+                                                            const int* __restrict__ offsets, int C, int G,
+                                                            int* __restrict__ order, int* __restrict__ ends,
+                                                            int* __restrict__ rowstart) {
   extern __shared__ uint8_t sm[];
-  unsigned long long* key = (unsigned long long*)sm;
-  int* id = (int*)(key + Cp);
-  __shared__ int red[32];
+  double* key = (double*)sm;                       // [C]
+  int* size = (int*)(key + C);                     // [C]
+  int* bkt = size + C;                             // [C]
+  int* members = bkt + C;                          // [C]
+  int* bcnt = members + C;                         // [NBUCKET]
+  int* btok = bcnt + NBUCKET;                      // [NBUCKET]
+  int* bpos = btok + NBUCKET;                      // [NBUCKET] count prefix
+  int* btp = bpos + NBUCKET;                       // [NBUCKET] token prefix
+  int* bcur = btp + NBUCKET;                       // [NBUCKET]
+  __shared__ double redd[32];
+  __shared__ int redi[32];
   pdl_wait();
-  const int g = blockIdx.x, u = blockIdx.y;
+  const int g = blockIdx.x, u = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
   const double* cr = crit + ((size_t)u * G + g) * C;
-  for (int i = threadIdx.x; i < Cp; i += blockDim.x) {
-    if (i < C) {
-      key[i] = desc_key(cr[i]);
-      id[i] = i;
-    } else {
-      key[i] = ~0ull;
-      id[i] = 0x7fffffff;
+  const int* off = offsets + (size_t)u * (C + 1);
+  double mn = INFINITY, mx = -INFINITY;
+  for (int j = tid; j < C; j += nt) {
+    double x = cr[j];
+    if (x == 0.0) x = 0.0;  // -0 == +0
+    key[j] = x;
+    size[j] = off[j + 1] - off[j];
+    mn = fmin(mn, x);
+    mx = fmax(mx, x);
+  }
+  for (int b = tid; b < NBUCKET; b += nt) { bcnt[b] = 0; btok[b] = 0; bcur[b] = 0; }
+  mn = block_reduce<double, RED_MIN>(mn, redd);
+  mx = block_reduce<double, RED_MAX>(mx, redd);
+  // monotone bucket map: higher crit -> lower-or-equal bucket (fl(), floor and min are
+  // monotone), so a strict crit order never contradicts the bucket order.
+  const double scale = mx > mn ? (double)NBUCKET / (mx - mn) : 0.0;
+  for (int j = tid; j < C; j += nt) {
+    int b = (int)((mx - key[j]) * scale);
+    b = b < NBUCKET - 1 ? b : NBUCKET - 1;
+    bkt[j] = b;
+    atomicAdd(&bcnt[b], 1);
+    atomicAdd(&btok[b], size[j]);
+  }
+  __syncthreads();
+  {
+    constexpr int PER = NBUCKET / RANK_THREADS;
+    int lc = 0, lt = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) { lc += bcnt[tid * PER + i]; lt += btok[tid * PER + i]; }
+    int cb = block_exclusive_scan<int>(lc, redi, (int*)nullptr);
+    int tb = block_exclusive_scan<int>(lt, redi, (int*)nullptr);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      bpos[tid * PER + i] = cb;
+      btp[tid * PER + i] = tb;
+      cb += bcnt[tid * PER + i];
+      tb += btok[tid * PER + i];
     }
   }
   __syncthreads();
-  for (int k = 2; k <= Cp; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < Cp; i += blockDim.x) {
-        const int l = i ^ j;
-        if (l > i) {
-          const unsigned long long ki = key[i], kl = key[l];
-          const int ii = id[i], il = id[l];
-          const bool gt = (ki > kl) || (ki == kl && ii > il);
-          const bool asc = (i & k) == 0;
-          if (gt == asc) {
-            key[i] = kl; key[l] = ki;
-            id[i] = il; id[l] = ii;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  // S3: inclusive scan of sizes in rank order
-  const int* off = offsets + (size_t)u * (C + 1);
-  const int per = (C + blockDim.x - 1) / blockDim.x;
-  const int b0 = threadIdx.x * per;
-  int loc = 0;
-  for (int r = b0; r < b0 + per && r < C; ++r) loc += off[id[r] + 1] - off[id[r]];
-  int base = block_exclusive_scan<int>(loc, red, (int*)nullptr);
+  for (int j = tid; j < C; j += nt) members[bpos[bkt[j]] + atomicAdd(&bcur[bkt[j]], 1)] = j;
+  __syncthreads();
   int* ord = order + ((size_t)u * G + g) * C;
   int* en = ends + ((size_t)u * G + g) * C;
-  for (int r = b0; r < b0 + per && r < C; ++r) {
-    base += off[id[r] + 1] - off[id[r]];
-    ord[r] = id[r];
-    en[r] = base;
+  int* rs = rowstart + ((size_t)u * G + g) * C;
+  for (int j = tid; j < C; j += nt) {
+    const int b = bkt[j];
+    const double kj = key[j];
+    int r = bpos[b], s = btp[b];
+    const int e = bpos[b] + bcnt[b];
+    for (int m = bpos[b]; m < e; ++m) {
+      const int i = members[m];
+      const double ki = key[i];
+      if (ki > kj || (ki == kj && i < j)) {
+        ++r;
+        s += size[i];
+      }
+    }
+    ord[r] = j;
+    en[r] = s + size[j];
+    rs[r] = off[j];
   }
   pdl_launch_dependents();
 }
 
-// ------------------------------------------------------------------ S4 (logits)
+// ------------------------------------------------------------------ S4 (sampled logits)
 __device__ __forceinline__ int slot_rank(int slot, const SampleConsts& sc) {
   if (sc.fallback) return slot + 1;
   const int W1 = 2 * sc.w + 1;
@@ -254,56 +309,77 @@ __device__ __forceinline__ int slot_rank(int slot, const SampleConsts& sc) {
   return sc.x2 - sc.w + (slot - sc.N - W1);
 }
 
+// block = 4 warps x 16 slots; lanes 0..15 resolve a slot's layout row, then the warp
+// loads its 16 rows (16 lanes x 16 B per row, 8 independent 16-byte loads per lane).
 __global__ void __launch_bounds__(128) sample_kernel(const __nv_bfloat16* __restrict__ q,
                                                      const __nv_bfloat16* __restrict__ Kp,
-                                                     const int* __restrict__ offsets,
-                                                     const int* __restrict__ order, const int* __restrict__ ends,
-                                                     int n, int C, int G, SampleConsts sc,
-                                                     float* __restrict__ logits) {
+                                                     const int* __restrict__ ends,
+                                                     const int* __restrict__ rowstart, int n, int C, int G,
+                                                     SampleConsts sc, float* __restrict__ logits) {
   extern __shared__ int s_ends[];
   pdl_wait();
   const int g = blockIdx.y, u = blockIdx.z;
-  const int* en = ends + ((size_t)u * G + g) * C;
+  const size_t ug = (size_t)u * G + g;
+  const int* en = ends + ug * C;
   for (int i = threadIdx.x; i < C; i += blockDim.x) s_ends[i] = en[i];
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = lane >> 4, l16 = lane & 15;
   float qf[8];
   {
-    const __nv_bfloat16* qq = q + ((size_t)u * G + g) * 128 + l16 * 8;
+    const uint4 raw = *reinterpret_cast<const uint4*>(q + ug * 128 + l16 * 8);
+    const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) qf[i] = __bfloat162float(qq[i]);
-  }
-  const int* ord = order + ((size_t)u * G + g) * C;
-  const int* off = offsets + (size_t)u * (C + 1);
-  const float inv_sqrt_d = 0.08838834764831845f;
-  const int base_slot = blockIdx.x * 64 + warp * 16;
-  for (int it = 0; it < 8; ++it) {
-    const int slot = base_slot + it * 2 + half;
-    float dot = 0.f;
-    const bool valid = slot < sc.slots;
-    if (valid) {
-      const int rank = slot_rank(slot, sc);
-      int lo = 0, hi = C - 1;  // smallest r with ends[r] >= rank
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (s_ends[mid] >= rank) hi = mid; else lo = mid + 1;
-      }
-      const int cid = ord[lo];
-      const int sr = lo ? s_ends[lo - 1] : 0;
-      const int row = off[cid] + (rank - 1 - sr);
-      const uint4 kv = *reinterpret_cast<const uint4*>(Kp + ((size_t)u * n + row) * 128 + swz_chunk(l16, row) * 8);
-      const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kv);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 f = __bfloat1622float2(k2[i]);
-        dot = fmaf(qf[2 * i], f.x, dot);
-        dot = fmaf(qf[2 * i + 1], f.y, dot);
-      }
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(q2[i]);
+      qf[2 * i] = f.x;
+      qf[2 * i + 1] = f.y;
     }
+  }
+  __syncthreads();
+  const int base_slot = blockIdx.x * 64 + warp * 16;
+  // lanes 0..15: slot -> rank -> (r, row)
+  int myrow = -1;
+  if (lane < 16 && base_slot + lane < sc.slots) {
+    const int rank = slot_rank(base_slot + lane, sc);
+    int lo = 0, hi = C - 1;  // smallest r with ends[r] >= rank
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s_ends[mid] >= rank) hi = mid; else lo = mid + 1;
+    }
+    const int sr = lo ? s_ends[lo - 1] : 0;
+    myrow = __ldg(rowstart + ug * C + lo) + (rank - 1 - sr);
+  }
+  uint4 kv[8];
+  int rows[8];
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-    if (valid && l16 == 0) logits[((size_t)u * G + g) * sc.slots + slot] = dot * inv_sqrt_d;
+  for (int it = 0; it < 8; ++it) {
+    rows[it] = __shfl_sync(0xffffffffu, myrow, it * 2 + half);
+    kv[it] = rows[it] >= 0
+                 ? __ldg(reinterpret_cast<const uint4*>(Kp + ((size_t)u * n + rows[it]) * 128 +
+                                                        swz_chunk(l16, rows[it]) * 8))
+                 : make_uint4(0, 0, 0, 0);
+  }
+  float dot[8];
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kv[it]);
+    float d = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(k2[i]);
+      d = fmaf(qf[2 * i], f.x, d);
+      d = fmaf(qf[2 * i + 1], f.y, d);
+    }
+    dot[it] = d;
+  }
+#pragma unroll
+  for (int it = 0; it < 8; ++it)
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) dot[it] += __shfl_xor_sync(0xffffffffu, dot[it], o);
+  if (l16 == 0) {
+#pragma unroll
+    for (int it = 0; it < 8; ++it)
+      if (rows[it] >= 0) logits[ug * sc.slots + base_slot + it * 2 + half] = dot[it] * 0.08838834764831845f;
   }
   pdl_launch_dependents();
 }
@@ -311,72 +387,86 @@ __global__ void __launch_bounds__(128) sample_kernel(const __nv_bfloat16* __rest
 // ------------------------------------------------------------------ S4-S7
 // mode 0: Alg. 1 selection; mode 1: sharded stage 2 (grid threshold); mode 2: sharded
 // stage 1 (fit only: local (m, theta_max) and cumulative mass at cluster ends).
-__global__ void __launch_bounds__(SEL_THREADS) select_kernel(
-    const float* __restrict__ logits, const int* __restrict__ order, const int* __restrict__ ends,
-    const int* __restrict__ offsets, const double* __restrict__ crit, int n, int C, int G, SampleConsts sc,
-    double p, int mode, const double* __restrict__ gmax, const double* __restrict__ gmass,
-    double* __restrict__ fit, int* __restrict__ Jout, uint8_t* __restrict__ umask, int* __restrict__ ulist,
-    int* __restrict__ uprefix, long long* __restrict__ unit_prefix, unsigned int* __restrict__ counter,
-    double* __restrict__ cumend, double* __restrict__ local_max, int units) {
+struct SelectParams {
+  const float* logits;
+  const int* order;
+  const int* ends;
+  const int* offsets;
+  const double* crit;
+  int n, C, G, units;
+  SampleConsts sc;
+  double p;
+  int mode;
+  const double* gmax;
+  const double* gmass;
+  double* fit;
+  int* J;
+  uint8_t* mask_acc;      // [units][C] union accumulator, all-zero between calls
+  uint8_t* umask;         // [units][C] debug copy of the union
+  int* ulist;             // [units][C] segment row starts
+  int* uprefix;           // [units][C+1]
+  long long* unit_prefix; // [units+1]
+  unsigned int* head_cnt; // [units]
+  unsigned int* unit_cnt; // [1]
+  double* cumend;
+  double* local_max;
+};
+
+__global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SelectParams P) {
   extern __shared__ uint8_t smraw[];
-  double* epref = (double*)smraw;                       // [max(N or n, 1)]
+  const int C = P.C, G = P.G, n = P.n;
+  const SampleConsts sc = P.sc;
   const int nex = sc.fallback ? n : sc.N;
+  double* epref = (double*)smraw;                       // [max(nex, 1)]
   int* s_ends = (int*)(epref + (nex > 0 ? nex : 1));     // [C]
-  uint8_t* mask = (uint8_t*)(s_ends + C);                // [C]
   __shared__ double redd[32];
   __shared__ float redf[32];
   __shared__ int redi[32];
-  __shared__ double sh_d[8];
   __shared__ long long sh_k;
   __shared__ bool s_last;
+  __shared__ int s_totc, s_tott;
   pdl_wait();
-  const int u = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
-  const int* off = offsets + (size_t)u * (C + 1);
-  for (int j = tid; j < C; j += nt) mask[j] = 0;
-  __syncthreads();
+  const int g = blockIdx.x, u = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
+  const size_t ug = (size_t)u * G + g;
+  const int* off = P.offsets + (size_t)u * (C + 1);
+  const int* ord = P.order + ug * C;
+  uint8_t* macc = P.mask_acc + (size_t)u * C;
 
-  for (int g = 0; g < G; ++g) {
-    const size_t ug = (size_t)u * G + g;
-    const int* ord = order + ug * C;
-    long long kstar = (long long)n + 1;  // p >= 1: every rank
-    if (mode == 1) {
-      // ---- sharded stage 2: theta* from the all-reduced mass vector
-      const double* gm = gmass + ug * (1 + TACTIC_SHARD_GRID_T);
-      const double thmax = gmax[ug * 2 + 1];
-      const double Wt = gm[0];
-      double thstar = -INFINITY;
-      if (p < 1.0) {
-        if (tid == 0) {
-          int t = 1;
-          for (; t <= TACTIC_SHARD_GRID_T; ++t)
-            if (gm[t] >= p * Wt) break;
-          sh_d[0] = t <= TACTIC_SHARD_GRID_T ? thmax - (double)t * TACTIC_SHARD_GRID_STEP : -INFINITY;
-        }
-        __syncthreads();
-        thstar = sh_d[0];
-        __syncthreads();
-      }
-      const double* cr = crit + ug * C;
-      const double isd = 1.0 / sqrt(128.0);
-      int cnt = 0;
-      for (int j = tid; j < C; j += nt) {
-        const bool sel = (off[j + 1] > off[j]) && (cr[j] * isd >= thstar);
-        if (sel) { mask[j] = 1; ++cnt; }
-      }
-      cnt = block_reduce<int>(cnt, redi, false);
-      if (tid == 0) {
-        Jout[ug] = cnt;
-        double* f = fit + ug * 6;
-        f[0] = thstar; f[1] = Wt; f[2] = gmax[ug * 2]; f[3] = thmax; f[4] = 0; f[5] = 0;
-      }
-      continue;
+  if (P.mode == 1) {
+    // ---- sharded stage 2: theta* from the all-reduced mass vector
+    const double* gm = P.gmass + ug * (1 + TACTIC_SHARD_GRID_T);
+    const double thmax = P.gmax[ug * 2 + 1];
+    const double Wt = gm[0];
+    double thstar = -INFINITY;
+    if (P.p < 1.0) {
+      int tmin = INT_MAX;
+      for (int t = 1 + tid; t <= TACTIC_SHARD_GRID_T; t += nt)
+        if (gm[t] >= P.p * Wt) tmin = min(tmin, t);
+      tmin = -block_reduce<int, RED_MAX>(-tmin, redi);
+      if (tmin <= TACTIC_SHARD_GRID_T) thstar = thmax - (double)tmin * TACTIC_SHARD_GRID_STEP;
     }
-    for (int r = tid; r < C; r += nt) s_ends[r] = ends[ug * C + r];
-    const float* L = logits + ug * sc.slots;
+    const double* cr = P.crit + ug * C;
+    const double isd = 1.0 / sqrt(128.0);
+    int cnt = 0;
+    for (int j = tid; j < C; j += nt) {
+      if ((off[j + 1] > off[j]) && (cr[j] * isd >= thstar)) {
+        macc[j] = 1;
+        ++cnt;
+      }
+    }
+    cnt = block_reduce<int, RED_SUM>(cnt, redi);
+    if (tid == 0) {
+      P.J[ug] = cnt;
+      double* f = P.fit + ug * 6;
+      f[0] = thstar; f[1] = Wt; f[2] = P.gmax[ug * 2]; f[3] = thmax; f[4] = 0; f[5] = 0;
+    }
+  } else {
+    for (int r = tid; r < C; r += nt) s_ends[r] = P.ends[ug * C + r];
+    const float* L = P.logits + ug * sc.slots;
     // shift m = max sampled logit (reading 13)
     float mf = -INFINITY;
     for (int i = tid; i < sc.slots; i += nt) mf = fmaxf(mf, L[i]);
-    mf = block_reduce<float>(mf, redf, true);
+    mf = block_reduce<float, RED_MAX>(mf, redf);
     const double m = (double)mf;
     // exact head weights e_i = exp(l_i - m), i <= nex, and their inclusive prefix
     const int per = (nex + nt - 1) / nt;
@@ -400,18 +490,22 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
         s1 += exp((double)L[sc.N + i] - m);
         s2 += exp((double)L[sc.N + W1 + i] - m);
       }
-      s1 = block_reduce<double>(s1, redd, false);
-      s2 = block_reduce<double>(s2, redd, false);
+      s1 = block_reduce<double, RED_SUM>(s1, redd);
+      s2 = block_reduce<double, RED_SUM>(s2, redd);
       mu1 = s1 / (double)W1;
       mu2 = s2 / (double)W1;
       const double x1 = (double)sc.x1, x2 = (double)sc.x2;
-      a = (mu1 - mu2) * x1 * x2 / (x2 - x1);   // O8 / Alg. 1 l.4
+      a = (mu1 - mu2) * x1 * x2 / (x2 - x1);  // O8 / Alg. 1 l.4
       b = mu1 - a / x1;
       W = EN + tail_mass(a, b, sc.N, n);
     }
-    if (mode == 2) {
+    if (tid == 0) {
+      double* f = P.fit + ug * 6;
+      f[0] = a; f[1] = b; f[2] = m; f[3] = W; f[4] = mu1; f[5] = mu2;
+    }
+    if (P.mode == 2) {
       // sharded stage 1: cumulative estimated mass at every cluster end (local frame)
-      double* ce = cumend + ug * C;
+      double* ce = P.cumend + ug * C;
       for (int r = tid; r < C; r += nt) {
         const long long e = s_ends[r];
         double v;
@@ -421,16 +515,14 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
         ce[r] = v;
       }
       if (tid == 0) {
-        double* f = fit + ug * 6;
-        f[0] = a; f[1] = b; f[2] = m; f[3] = W; f[4] = mu1; f[5] = mu2;
-        local_max[ug * 2] = m;
-        local_max[ug * 2 + 1] = crit[ug * C + ord[0]] / sqrt(128.0);
+        P.local_max[ug * 2] = m;
+        P.local_max[ug * 2 + 1] = P.crit[ug * C + ord[0]] / sqrt(128.0);
       }
-      __syncthreads();
-      continue;
+      return;
     }
-    if (p < 1.0) {
-      const double target = p * W;
+    long long kstar = (long long)n + 1;  // p >= 1: every rank (reading 15)
+    if (P.p < 1.0) {
+      const double target = P.p * W;
       if (EN >= target) {
         kstar = 1 + block_lower_bound(0, nex - 1, [&](long long i) { return epref[i] >= target; }, &sh_k);
       } else {
@@ -447,36 +539,40 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
       if (sr < kstar) {
         ++cnt;
         const int cid = ord[r];
-        if (off[cid + 1] > off[cid]) mask[cid] = 1;
+        if (off[cid + 1] > off[cid]) macc[cid] = 1;
       }
     }
-    cnt = block_reduce<int>(cnt, redi, false);
-    if (tid == 0) {
-      Jout[ug] = cnt;
-      double* f = fit + ug * 6;
-      f[0] = a; f[1] = b; f[2] = m; f[3] = W; f[4] = mu1; f[5] = mu2;
-    }
-    __syncthreads();
+    cnt = block_reduce<int, RED_SUM>(cnt, redi);
+    if (tid == 0) P.J[ug] = cnt;
   }
 
-  if (mode == 2) return;
-  // ---- S7: compact the union (cluster-id order) into the work list
+  // ---- S7: the last head of the unit compacts the union (cluster-id order)
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&P.head_cnt[u], 1u);
+    s_last = (prev == (unsigned)G - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
   {
-    __shared__ int s_totc, s_tott;
     const int per = (C + nt - 1) / nt;
     const int b0 = tid * per;
     int lc = 0, lt = 0;
     for (int j = b0; j < b0 + per && j < C; ++j)
-      if (mask[j]) { ++lc; lt += off[j + 1] - off[j]; }
+      if (__ldcg(macc + j)) { ++lc; lt += off[j + 1] - off[j]; }
     int cbase = block_exclusive_scan<int>(lc, redi, &s_totc);
     int tbase = block_exclusive_scan<int>(lt, redi, &s_tott);
-    int* ul = ulist + (size_t)u * C;
-    int* up = uprefix + (size_t)u * (C + 1);
-    uint8_t* um = umask + (size_t)u * C;
+    int* ul = P.ulist + (size_t)u * C;
+    int* up = P.uprefix + (size_t)u * (C + 1);
+    uint8_t* um = P.umask + (size_t)u * C;
     for (int j = b0; j < b0 + per && j < C; ++j) {
-      um[j] = mask[j];
-      if (mask[j]) {
-        ul[cbase] = j;
+      const uint8_t mk = __ldcg(macc + j);
+      um[j] = mk;
+      macc[j] = 0;  // reset the accumulator for the next call
+      if (mk) {
+        ul[cbase] = off[j];  // work-list segment = first layout row of the cluster
         up[cbase] = tbase;
         ++cbase;
         tbase += off[j + 1] - off[j];
@@ -488,28 +584,29 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(
       if (k < C) ul[k] = 0;
     }
   }
-  // ---- global token prefix over units: done by the last block to finish
+  if (tid == 0) P.head_cnt[u] = 0;
+  // ---- global token prefix over units: done by the last unit to finish
   __syncthreads();
   if (tid == 0) {
     __threadfence();
-    const unsigned prev = atomicAdd(counter, 1u);
-    s_last = (prev == (unsigned)units - 1);
+    const unsigned prev = atomicAdd(P.unit_cnt, 1u);
+    s_last = (prev == (unsigned)P.units - 1);
   }
   __syncthreads();
   if (s_last) {
     __threadfence();
+    const int units = P.units;
     const int per = (units + nt - 1) / nt;
     const int b0 = tid * per;
     long long loc = 0;
-    for (int v = b0; v < b0 + per && v < units; ++v) loc += __ldcg(uprefix + (size_t)v * (C + 1) + C);
+    for (int v = b0; v < b0 + per && v < units; ++v) loc += __ldcg(P.uprefix + (size_t)v * (C + 1) + C);
     long long run = block_exclusive_scan<long long>(loc, (long long*)redd, (long long*)nullptr);
     for (int v = b0; v < b0 + per && v < units; ++v) {
-      unit_prefix[v] = run;
-      run += __ldcg(uprefix + (size_t)v * (C + 1) + C);
+      P.unit_prefix[v] = run;
+      run += __ldcg(P.uprefix + (size_t)v * (C + 1) + C);
     }
-    if (b0 < units && b0 + per >= units) unit_prefix[units] = run;
-    if (units <= b0 && tid == 0 && units == 0) unit_prefix[0] = 0;
-    if (tid == 0) *counter = 0u;
+    if (b0 < units && b0 + per >= units) P.unit_prefix[units] = run;
+    if (tid == 0) *P.unit_cnt = 0u;
   }
   pdl_launch_dependents();
 }
@@ -560,7 +657,8 @@ static cudaLaunchConfig_t make_cfg(dim3 grid, dim3 block, size_t smem, cudaStrea
 cudaError_t launch_score(const SelArgs& a, cudaStream_t s, bool pdl) {
   tactic_index_s* x = a.idx;
   cudaLaunchAttribute attr[1];
-  auto cfg = make_cfg(dim3((x->C + 31) / 32, x->units), dim3(128), 0, s, pdl, attr);
+  const int per_block = 8 * (32 / x->G);
+  auto cfg = make_cfg(dim3((x->C + per_block - 1) / per_block, x->units), dim3(256), 0, s, pdl, attr);
   switch (x->G) {
     case 1: return cudaLaunchKernelEx(&cfg, score_kernel<1>, a.q, (const float*)x->cent, x->C, x->crit);
     case 2: return cudaLaunchKernelEx(&cfg, score_kernel<2>, a.q, (const float*)x->cent, x->C, x->crit);
@@ -570,56 +668,71 @@ cudaError_t launch_score(const SelArgs& a, cudaStream_t s, bool pdl) {
   return cudaErrorInvalidValue;
 }
 
-static int pow2_at_least(int c) {
-  int p = 2;
-  while (p < c) p <<= 1;
-  return p;
+static cudaError_t ensure_smem(const void* fn, size_t smem, size_t* done) {
+  if (smem > 48 * 1024 && smem > *done) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    *done = smem;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_sort(const SelArgs& a, cudaStream_t s, bool pdl) {
   tactic_index_s* x = a.idx;
-  const int Cp = pow2_at_least(x->C);
-  const size_t smem = (size_t)Cp * (8 + 4);
-  static size_t set_smem = 0;
-  if (smem > 48 * 1024 && smem > set_smem) {
-    cudaError_t e = cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set_smem = smem;
-  }
+  const size_t smem = (size_t)x->C * (8 + 4 * 3) + (size_t)NBUCKET * 4 * 5;
+  static size_t done = 0;
+  cudaError_t e = ensure_smem((const void*)rank_kernel, smem, &done);
+  if (e != cudaSuccess) return e;
   cudaLaunchAttribute attr[1];
-  auto cfg = make_cfg(dim3(x->G, x->units), dim3(SEL_THREADS), smem, s, pdl, attr);
-  return cudaLaunchKernelEx(&cfg, sort_kernel, (const double*)x->crit, (const int*)x->offsets, x->C, Cp, x->G,
-                            x->order, x->ends);
+  auto cfg = make_cfg(dim3(x->G, x->units), dim3(RANK_THREADS), smem, s, pdl, attr);
+  return cudaLaunchKernelEx(&cfg, rank_kernel, (const double*)x->crit, (const int*)x->offsets, x->C, x->G,
+                            x->order, x->ends, x->rowstart);
 }
 
 cudaError_t launch_sample(const SelArgs& a, cudaStream_t s, bool pdl) {
   tactic_index_s* x = a.idx;
   cudaLaunchAttribute attr[1];
   auto cfg = make_cfg(dim3((x->sc.slots + 63) / 64, x->G, x->units), dim3(128), (size_t)x->C * 4, s, pdl, attr);
-  return cudaLaunchKernelEx(&cfg, sample_kernel, a.q, (const __nv_bfloat16*)x->Kp, (const int*)x->offsets,
-                            (const int*)x->order, (const int*)x->ends, x->n, x->C, x->G, x->sc, x->logits);
-}
-
-static size_t select_smem(const tactic_index_s* x) {
-  const int nex = x->sc.fallback ? x->n : x->sc.N;
-  return (size_t)(nex > 0 ? nex : 1) * 8 + (size_t)x->C * 4 + (size_t)x->C + 16;
+  return cudaLaunchKernelEx(&cfg, sample_kernel, a.q, (const __nv_bfloat16*)x->Kp, (const int*)x->ends,
+                            (const int*)x->rowstart, x->n, x->C, x->G, x->sc, x->logits);
 }
 
 cudaError_t launch_select(const SelArgs& a, cudaStream_t s, bool pdl) {
   tactic_index_s* x = a.idx;
-  const size_t smem = select_smem(x);
-  static size_t set_smem = 0;
-  if (smem > 48 * 1024 && smem > set_smem) {
-    cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set_smem = smem;
-  }
+  const int nex = x->sc.fallback ? x->n : x->sc.N;
+  const size_t smem = (size_t)(nex > 0 ? nex : 1) * 8 + (size_t)x->C * 4 + 16;
+  static size_t done = 0;
+  cudaError_t e = ensure_smem((const void*)select_kernel, smem, &done);
+  if (e != cudaSuccess) return e;
+  SelectParams P = {};
+  P.logits = x->logits;
+  P.order = x->order;
+  P.ends = x->ends;
+  P.offsets = x->offsets;
+  P.crit = x->crit;
+  P.n = x->n;
+  P.C = x->C;
+  P.G = x->G;
+  P.units = x->units;
+  P.sc = x->sc;
+  P.p = a.p;
+  P.mode = a.mode;
+  P.gmax = a.gmax;
+  P.gmass = a.gmass;
+  P.fit = x->fit;
+  P.J = x->J;
+  P.mask_acc = x->mask_acc;
+  P.umask = x->umask;
+  P.ulist = x->union_list;
+  P.uprefix = x->union_prefix;
+  P.unit_prefix = x->unit_prefix;
+  P.head_cnt = x->head_cnt;
+  P.unit_cnt = x->counter;
+  P.cumend = x->cumend;
+  P.local_max = a.local_max;
   cudaLaunchAttribute attr[1];
-  auto cfg = make_cfg(dim3(x->units), dim3(SEL_THREADS), smem, s, pdl, attr);
-  return cudaLaunchKernelEx(&cfg, select_kernel, (const float*)x->logits, (const int*)x->order,
-                            (const int*)x->ends, (const int*)x->offsets, (const double*)x->crit, x->n, x->C, x->G,
-                            x->sc, a.p, a.mode, a.gmax, a.gmass, x->fit, x->J, x->umask, x->union_list,
-                            x->union_prefix, x->unit_prefix, x->counter, x->cumend, a.local_max, x->units);
+  auto cfg = make_cfg(dim3(x->G, x->units), dim3(SEL_THREADS), smem, s, pdl, attr);
+  return cudaLaunchKernelEx(&cfg, select_kernel, P);
 }
 
 cudaError_t launch_stage1b(const SelArgs& a, cudaStream_t s) {

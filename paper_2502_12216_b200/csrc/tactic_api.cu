@@ -186,13 +186,31 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_
   x->stage = A.get<double>(U * G * 2);
   x->q_stage = A.get<__nv_bfloat16>(U * G * 128);
   x->o_stage = A.get<__nv_bfloat16>(U * G * 128);
+  x->unit_cnt = A.get<int>(U);
+  x->rowstart = A.get<int>(U * G * C);
+  x->mask_acc = A.get<uint8_t>(U * C);
+  x->head_cnt = A.get<unsigned int>(U);
   if (A.err != cudaSuccess) {
     for (void* p : A.ptrs) cudaFree(p);
     delete x;
     return cuda_fail(A.err, "index allocation");
   }
   x->device_bytes = A.bytes;
+  {
+    // selection path: TACTIC_SELECT=fused (cluster kernel) | multi (default, 4 kernels)
+    const char* sel = getenv("TACTIC_SELECT");
+    x->fused_R = (sel && strcmp(sel, "fused") == 0) ? choose_fused_R(x) : 0;
+    const char* tl = getenv("TACTIC_TLOG");
+    if (tl && tl[0] == '1' && cudaMalloc((void**)&x->tlog, U * 16 * 8 * 8) == cudaSuccess) {
+      cudaMemset(x->tlog, 0, U * 16 * 8 * 8);
+      std::lock_guard<std::mutex> lk(g_mu);
+      A.ptrs.push_back(x->tlog);
+    }
+  }
   cudaMemset(x->counter, 0, sizeof(unsigned int));
+  cudaMemset(x->unit_cnt, 0, U * sizeof(int));
+  cudaMemset(x->mask_acc, 0, U * C);
+  cudaMemset(x->head_cnt, 0, U * sizeof(unsigned int));
   std::vector<long long> up(U + 1);
   for (size_t u = 0; u <= U; ++u) up[u] = (long long)u * (long long)n;
   cudaMemcpy(x->all_unit_prefix, up.data(), (U + 1) * sizeof(long long), cudaMemcpyHostToDevice);
@@ -383,6 +401,15 @@ void tactic_index_destroy(tactic_index_t idx) {
   free_index(idx, &ptrs);
 }
 
+tactic_status_t tactic_index_debug_timing(tactic_index_t idx, uint64_t* host, int32_t count) {
+  if (!idx || !host) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!idx->tlog) return fail(TACTIC_ERR_UNSUPPORTED, "index created without TACTIC_TLOG=1");
+  const size_t n = (size_t)idx->units * 16 * 8;
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(host, idx->tlog, (count < (int32_t)n ? (size_t)count : n) * 8, cudaMemcpyDeviceToHost));
+  return TACTIC_OK;
+}
+
 tactic_status_t tactic_index_info(tactic_index_t idx, tactic_index_info_t* info) {
   if (!idx || !info) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
   info->units = idx->units;
@@ -393,6 +420,7 @@ tactic_status_t tactic_index_info(tactic_index_t idx, tactic_index_info_t* info)
   info->n_clusters = idx->C;
   info->iters_requested = idx->iters_req;
   info->device_bytes = idx->device_bytes;
+  info->select_cluster_size = idx->fused_R;
   return TACTIC_OK;
 }
 
@@ -441,6 +469,10 @@ static tactic_status_t run_selection(const void* q, tactic_index_t idx, double p
   sa.gmass = gmass;
   sa.local_max = local_max;
   const bool pdl = true;
+  if (mode == 0 && idx->fused_R > 0) {  // one cluster-launched kernel for S1-S7
+    CK(launch_select_fused((const __nv_bfloat16*)q, idx, p, s, pdl));
+    return TACTIC_OK;
+  }
   if (mode != 1) {
     CK(launch_score(sa, s, pdl));
     CK(launch_sort(sa, s, pdl));
@@ -453,14 +485,13 @@ static tactic_status_t run_selection(const void* q, tactic_index_t idx, double p
 }
 
 static tactic_status_t run_attention(const void* q, tactic_index_t idx, bool all, cudaStream_t s, void* out,
-                                     float* out_f32, float* lse) {
+                                     float* out_f32, float* lse, cudaEvent_t ev_mid = nullptr) {
   AttnArgs aa = {};
   aa.q = (const __nv_bfloat16*)q;
   aa.Kp = idx->Kp;
   aa.Vp = idx->Vp;
-  aa.seg_list = all ? idx->all_list : idx->union_list;
+  aa.seg_row = all ? idx->all_list : idx->union_list;
   aa.seg_prefix = all ? idx->all_prefix : idx->union_prefix;
-  aa.offsets = idx->offsets;
   aa.unit_prefix = all ? idx->all_unit_prefix : idx->unit_prefix;
   aa.n = idx->n;
   aa.C = idx->C;
@@ -468,9 +499,13 @@ static tactic_status_t run_attention(const void* q, tactic_index_t idx, bool all
   aa.Hkv = idx->Hkv;
   aa.part_o = idx->part_o;
   aa.part_lse = idx->part_lse;
-  CK(launch_attention_sparse(aa, idx->G, idx->num_ctas, s, true));
-  CK(launch_merge(idx->part_o, idx->part_lse, aa.unit_prefix, idx->n, idx->units, idx->G, idx->num_ctas,
-                  (__nv_bfloat16*)out, out_f32, lse, s, true));
+  aa.unit_cnt = idx->unit_cnt;
+  aa.out = (__nv_bfloat16*)out;
+  aa.out_f32 = out_f32;
+  aa.lse = lse;
+  aa.tlog = idx->tlog;
+  CK(launch_attention_sparse(aa, idx->G, idx->num_ctas, s, ev_mid == nullptr));  // S8 + fused S9
+  if (ev_mid) CK(cudaEventRecord(ev_mid, s));
   return TACTIC_OK;
 }
 
@@ -487,6 +522,21 @@ tactic_status_t tactic_decode_ex(const void* q, tactic_index_t idx, float p, voi
   if (p >= 1.0f) return run_attention(q, idx, true, s, out, nullptr, lse);  // reading 15
   if ((st = run_selection(q, idx, (double)p, 0, s, nullptr, nullptr, nullptr))) return st;
   return run_attention(q, idx, false, s, out, nullptr, lse);
+}
+
+tactic_status_t tactic_decode_profiled(const void* q, tactic_index_t idx, float p, void* out,
+                                       void* const* events, int32_t n_events, void* stream) {
+  if (!q || !idx || !out || !events || n_events != 4) return fail(TACTIC_ERR_INVALID_ARGUMENT, "bad arguments");
+  tactic_status_t st = check_p(p);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaEvent_t* ev = (cudaEvent_t*)events;
+  CK(cudaEventRecord(ev[0], s));
+  if (p < 1.0f && (st = run_selection(q, idx, (double)p, 0, s, nullptr, nullptr, nullptr))) return st;
+  CK(cudaEventRecord(ev[1], s));
+  if ((st = run_attention(q, idx, p >= 1.0f, s, out, nullptr, nullptr, ev[2]))) return st;
+  CK(cudaEventRecord(ev[3], s));  // S9 is fused into the attention kernel: ev[3] == ev[2]
+  return TACTIC_OK;
 }
 
 tactic_status_t tactic_decode(const void* q, tactic_index_t idx, float p, void* out, void* stream) {
@@ -530,7 +580,7 @@ tactic_status_t tactic_dense_workspace_size(const tactic_kv_desc_t* kv, int32_t 
   if (!bytes) return fail(TACTIC_ERR_INVALID_ARGUMENT, "bytes is NULL");
   const int P = num_ctas > 0 ? num_ctas : device_sms();
   const size_t slots = (size_t)P + (size_t)r.B * r.Hkv;
-  *bytes = slots * r.G * 129 * 4 + 256;
+  *bytes = slots * r.G * 129 * 4 + (size_t)r.B * r.Hkv * 4 + 256;  // partials + arrival counters
   return TACTIC_OK;
 }
 
@@ -584,6 +634,7 @@ tactic_status_t tactic_dense_decode(const void* q, const void* K, const void* V,
   const size_t slots = (size_t)P + units;
   float* part_o = (float*)workspace;
   float* part_lse = part_o + slots * r.G * 128;
+  int* unit_cnt = (int*)(part_lse + slots * r.G);
   AttnArgs aa = {};
   aa.q = (const __nv_bfloat16*)q;
   aa.n = r.n;
@@ -592,8 +643,10 @@ tactic_status_t tactic_dense_decode(const void* q, const void* K, const void* V,
   aa.part_o = part_o;
   aa.part_lse = part_lse;
   cudaStream_t s = (cudaStream_t)stream;
-  CK(launch_attention_dense(aa, &mk, &mv, r.G, P, s, true));
-  CK(launch_merge(part_o, part_lse, nullptr, r.n, (int)units, r.G, P, (__nv_bfloat16*)out, nullptr, lse, s, true));
+  aa.unit_cnt = unit_cnt;
+  aa.out = (__nv_bfloat16*)out;
+  aa.lse = lse;
+  CK(launch_attention_dense(aa, &mk, &mv, r.G, P, s, true));  // S10 + fused merge
   return TACTIC_OK;
 }
 

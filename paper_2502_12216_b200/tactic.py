@@ -45,7 +45,8 @@ class Params(ctypes.Structure):
 class IndexInfo(ctypes.Structure):
     _fields_ = [("units", ctypes.c_int32), ("batch", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
                 ("group_size", ctypes.c_int32), ("seq_len", ctypes.c_int32), ("n_clusters", ctypes.c_int32),
-                ("iters_requested", ctypes.c_int32), ("device_bytes", ctypes.c_int64)]
+                ("iters_requested", ctypes.c_int32), ("select_cluster_size", ctypes.c_int32),
+                ("device_bytes", ctypes.c_int64)]
 
 
 _lib = None
@@ -63,6 +64,7 @@ _SIGS = {
     "tactic_decode_ex": [_P, _P, _F, _P, _P, _P],
     "tactic_decode_host": [_P, _P, _F, _P, _P],
     "tactic_decode_debug": [_P, _P, _F, _P, _P, _P, _P, _P, _P, _P],
+    "tactic_decode_profiled": [_P, _P, _F, _P, ctypes.POINTER(_P), _I, _P],
     "tactic_dense_workspace_size": [ctypes.POINTER(KvDesc), _I, ctypes.POINTER(ctypes.c_size_t)],
     "tactic_dense_decode": [_P, _P, _P, ctypes.POINTER(KvDesc), _P, _P, _P, ctypes.c_size_t, _I, _P],
     "tactic_lse_merge": [_P, _P, _I, _I, _P, _P, _P],
@@ -70,6 +72,7 @@ _SIGS = {
     "tactic_decode_stage1b": [_P, _P, _P, _P],
     "tactic_decode_stage2": [_P, _P, _F, _P, _P, _P, _P, _P],
     "tactic_device_check": [ctypes.POINTER(_I)],
+    "tactic_index_debug_timing": [_P, _P, _I],
 }
 
 
@@ -175,6 +178,12 @@ class Index:
         _check(lib().tactic_index_info(self.handle, ctypes.byref(i)))
         return {f: getattr(i, f) for f, _ in IndexInfo._fields_}
 
+    def debug_timing(self) -> np.ndarray:
+        """Phase timestamps (ns) of the fused selection kernel: [units][16 ranks][8 phases]."""
+        buf = np.zeros((self.units, 16, 8), dtype=np.uint64)
+        _check(lib().tactic_index_debug_timing(self.handle, buf.ctypes.data, buf.size))
+        return buf
+
     def export(self, stream=None) -> dict:
         cent = np.empty((self.units, self.C, HEAD_DIM), dtype=np.float32)
         assign = np.empty((self.units, self.n), dtype=np.int32)
@@ -266,6 +275,21 @@ def decode_debug(q: torch.Tensor, index: Index, p: float, stream=None) -> dict:
     return {"out": out, "lse": lse, "order": order, "J": J, "fit": fit, "union_mask": um.astype(bool)}
 
 
+def decode_profiled(q: torch.Tensor, index: Index, p: float, events, out: Optional[torch.Tensor] = None,
+                    stream=None) -> torch.Tensor:
+    """tactic_decode_profiled: records 4 torch.cuda.Event objects at the stage boundaries
+    (before S1, after S7, after S8, after S9)."""
+    _q_check(q, index)
+    if out is None:
+        out = torch.empty_like(q)
+    for e in events:          # torch creates the cudaEvent lazily on first record
+        if not e.cuda_event:
+            e.record(stream if stream is not None else torch.cuda.current_stream())
+    arr = (_P * 4)(*[ctypes.c_void_p(e.cuda_event) for e in events])
+    _check(lib().tactic_decode_profiled(_ptr(q), index.handle, float(p), _ptr(out), arr, 4, _stream(stream)))
+    return out
+
+
 _ws_cache = {}
 
 
@@ -281,7 +305,7 @@ def dense_decode(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, out: Optiona
         key = (q.device.index, sz.value)
         workspace = _ws_cache.get(key)
         if workspace is None:
-            workspace = torch.empty(sz.value, dtype=torch.uint8, device=q.device)
+            workspace = torch.zeros(sz.value, dtype=torch.uint8, device=q.device)
             _ws_cache[key] = workspace
     if out is None:
         out = torch.empty_like(q)
