@@ -37,8 +37,13 @@ __device__ __forceinline__ float warp_max(float v) {
 __device__ __forceinline__ int swz_chunk(int c, int r) { return (c & 8) | ((c ^ r) & 7); }
 
 // --------------------------------------------------------------------------- PDL
+// Wait for the preceding kernel (programmatic dependent launch), then immediately allow
+// the next kernel in the stream to launch: its prologue (barrier init, smem zeroing,
+// static-data prefetch) overlaps this kernel; it cannot read our outputs before its own
+// griddepcontrol.wait, which waits for this grid to complete.
 __device__ __forceinline__ void pdl_wait() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -56,6 +56,8 @@ struct tactic_index_s {
   int* order = nullptr;          // [units][G][C]
   int* ends = nullptr;           // [units][G][C]
   int* rowstart = nullptr;       // [units][G][C] first layout row of the r-th ranked cluster
+  int* rowmap = nullptr;         // [units][G][slots] layout row of every sampled slot
+  double* summ = nullptr;        // [units][G][nb][4] per-sample-block fit summaries
   uint8_t* mask_acc = nullptr;   // [units][C] union accumulator (zero between calls)
   unsigned int* head_cnt = nullptr;  // [units] selection arrival counters
   float* logits = nullptr;       // [units][G][slots]
@@ -118,6 +120,8 @@ cudaError_t launch_score(const SelArgs& a, cudaStream_t s, bool pdl);
 cudaError_t launch_sort(const SelArgs& a, cudaStream_t s, bool pdl);
 cudaError_t launch_sample(const SelArgs& a, cudaStream_t s, bool pdl);
 cudaError_t launch_select(const SelArgs& a, cudaStream_t s, bool pdl);
+cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl);
+int sample_blocks(int slots);
 cudaError_t launch_stage1b(const SelArgs& a, cudaStream_t s);
 // fused S1-S7 (select_fused.cu)
 cudaError_t launch_select_fused(const __nv_bfloat16* q, tactic_index_s* x, double p, cudaStream_t s, bool pdl);

@@ -215,11 +215,21 @@ __global__ void __launch_bounds__(256) score_kernel(const __nv_bfloat16* __restr
   pdl_launch_dependents();
 }
 
+// sampled slot -> 1-based rank in the partially sorted token list (O6/O7)
+__device__ __forceinline__ int slot_rank(int slot, const SampleConsts& sc) {
+  if (sc.fallback) return slot + 1;
+  const int W1 = 2 * sc.w + 1;
+  if (slot < sc.N) return slot + 1;
+  if (slot < sc.N + W1) return sc.x1 - sc.w + (slot - sc.N);
+  return sc.x2 - sc.w + (slot - sc.N - W1);
+}
+
 // ------------------------------------------------------------------ S2 + S3 (bucket ranking)
 __global__ void __launch_bounds__(RANK_THREADS) rank_kernel(const double* __restrict__ crit,
                                                             const int* __restrict__ offsets, int C, int G,
                                                             int* __restrict__ order, int* __restrict__ ends,
-                                                            int* __restrict__ rowstart) {
+                                                            int* __restrict__ rowstart, SampleConsts sc,
+                                                            int* __restrict__ rowmap) {
   extern __shared__ uint8_t sm[];
   double* key = (double*)sm;                       // [C]
   int* size = (int*)(key + C);                     // [C]
@@ -232,16 +242,16 @@ __global__ void __launch_bounds__(RANK_THREADS) rank_kernel(const double* __rest
   int* bcur = btp + NBUCKET;                       // [NBUCKET]
   __shared__ double redd[32];
   __shared__ int redi[32];
-  pdl_wait();
   const int g = blockIdx.x, u = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
   const double* cr = crit + ((size_t)u * G + g) * C;
   const int* off = offsets + (size_t)u * (C + 1);
+  for (int j = tid; j < C; j += nt) size[j] = off[j + 1] - off[j];  // static: before the wait
+  pdl_wait();
   double mn = INFINITY, mx = -INFINITY;
   for (int j = tid; j < C; j += nt) {
     double x = cr[j];
     if (x == 0.0) x = 0.0;  // -0 == +0
     key[j] = x;
-    size[j] = off[j + 1] - off[j];
     mn = fmin(mn, x);
     mx = fmax(mx, x);
   }
@@ -280,6 +290,8 @@ __global__ void __launch_bounds__(RANK_THREADS) rank_kernel(const double* __rest
   int* ord = order + ((size_t)u * G + g) * C;
   int* en = ends + ((size_t)u * G + g) * C;
   int* rs = rowstart + ((size_t)u * G + g) * C;
+  int* e_s = bcur + NBUCKET;   // [C] end ranks by rank position
+  int* r_s = e_s + C;          // [C] first layout row by rank position
   for (int j = tid; j < C; j += nt) {
     const int b = bkt[j];
     const double kj = key[j];
@@ -296,90 +308,366 @@ __global__ void __launch_bounds__(RANK_THREADS) rank_kernel(const double* __rest
     ord[r] = j;
     en[r] = s + size[j];
     rs[r] = off[j];
+    e_s[r] = s + size[j];
+    r_s[r] = off[j];
+  }
+  __syncthreads();
+  // S3: layout row of every sampled slot.  Slot ranks increase with the slot, so a thread
+  // binary-searches once per contiguous run of its slots and then walks forward.
+  int* rm = rowmap + ((size_t)u * G + g) * sc.slots;
+  const int per = (sc.slots + nt - 1) / nt;
+  int r = 0, prev_rank = -1;
+  for (int slot = tid * per; slot < (tid + 1) * per && slot < sc.slots; ++slot) {
+    const int rank = slot_rank(slot, sc);
+    if (rank != prev_rank + 1 || prev_rank < 0) {
+      int lo = 0, hi = C - 1;  // smallest r with e_s[r] >= rank
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (e_s[mid] >= rank) hi = mid; else lo = mid + 1;
+      }
+      r = lo;
+    } else {
+      while (e_s[r] < rank) ++r;
+    }
+    prev_rank = rank;
+    rm[slot] = r_s[r] + (rank - 1 - (r ? e_s[r - 1] : 0));
   }
   pdl_launch_dependents();
 }
 
 // ------------------------------------------------------------------ S4 (sampled logits)
-__device__ __forceinline__ int slot_rank(int slot, const SampleConsts& sc) {
-  if (sc.fallback) return slot + 1;
-  const int W1 = 2 * sc.w + 1;
-  if (slot < sc.N) return slot + 1;
-  if (slot < sc.N + W1) return sc.x1 - sc.w + (slot - sc.N);
-  return sc.x2 - sc.w + (slot - sc.N - W1);
-}
 
-// block = 4 warps x 16 slots; lanes 0..15 resolve a slot's layout row, then the warp
-// loads its 16 rows (16 lanes x 16 B per row, 8 independent 16-byte loads per lane).
-__global__ void __launch_bounds__(128) sample_kernel(const __nv_bfloat16* __restrict__ q,
-                                                     const __nv_bfloat16* __restrict__ Kp,
-                                                     const int* __restrict__ ends,
-                                                     const int* __restrict__ rowstart, int n, int C, int G,
-                                                     SampleConsts sc, float* __restrict__ logits) {
-  extern __shared__ int s_ends[];
-  pdl_wait();
+// One CTA = SB consecutive slots of one head: slot rows come from the rank kernel's row
+// map; every warp finds the contiguous runs among its 32 rows (ballot of run breaks) and
+// the first lane of each run bulk-copies it (1-D TMA) into shared memory; logits are
+// then computed on the tensor cores (mma.sync m16n8k16, q in the n=8 dimension, only
+// column 0 live).  The CTA also emits a summary for the fit: its local max logit and the
+// sums of exp(l - m_local) over its exact-head, window-1 and window-2 slots.
+constexpr int SB = 128;
+
+__global__ void __launch_bounds__(SB) sample_kernel(const __nv_bfloat16* __restrict__ q,
+                                                    const __nv_bfloat16* __restrict__ Kp,
+                                                    const int* __restrict__ rowmap, int n, int G, SampleConsts sc,
+                                                    float* __restrict__ logits, double* __restrict__ summ, int nb) {
+  __shared__ __align__(128) uint8_t rows_s[SB * 256];
+  __shared__ float lg_s[SB];
+  __shared__ uint64_t bar;
+  __shared__ double redd[SB / 32][3];
+  __shared__ float redf[SB / 32];
   const int g = blockIdx.y, u = blockIdx.z;
   const size_t ug = (size_t)u * G + g;
-  const int* en = ends + ug * C;
-  for (int i = threadIdx.x; i < C; i += blockDim.x) s_ends[i] = en[i];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int half = lane >> 4, l16 = lane & 15;
-  float qf[8];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    mbar_init(&bar, SB);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  const int slot = blockIdx.x * SB + tid;
+  const bool valid = slot < sc.slots;
+  const int row = valid ? rowmap[ug * sc.slots + slot] : -1;
   {
-    const uint4 raw = *reinterpret_cast<const uint4*>(q + ug * 128 + l16 * 8);
-    const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+    const int prev = __shfl_up_sync(0xffffffffu, row, 1);
+    const bool start = row >= 0 && (lane == 0 || prev != row - 1);
+    const unsigned brk = __ballot_sync(0xffffffffu, start || row < 0);
+    if (start) {
+      const unsigned later = brk & ~((2u << lane) - 1u);
+      const int len = (later ? __ffs(later) - 1 : 32) - lane;
+      mbar_arrive_expect_tx(&bar, (uint32_t)len * 256u);
+      bulk_g2s(rows_s + tid * 256, Kp + ((size_t)u * n + row) * 128, (uint32_t)len * 256u, &bar);
+    } else {
+      mbar_arrive(&bar);
+    }
+  }
+  // B fragment (k = dim, n = head column): only column 0 (lanes 0..3) carries q
+  uint32_t qb[8][2];
+  {
+    const uint32_t* q32 = reinterpret_cast<const uint32_t*>(q + ug * 128);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float2 f = __bfloat1622float2(q2[i]);
-      qf[2 * i] = f.x;
-      qf[2 * i + 1] = f.y;
+    for (int ks = 0; ks < 8; ++ks) {
+      qb[ks][0] = lane < 4 ? q32[(ks * 16 + 2 * lane) >> 1] : 0u;
+      qb[ks][1] = lane < 4 ? q32[(ks * 16 + 8 + 2 * lane) >> 1] : 0u;
+    }
+  }
+  mbar_wait(&bar, 0);
+  const uint32_t sbase = smem_u32(rows_s);
+#pragma unroll
+  for (int gi = 0; gi < 2; ++gi) {
+    const int i = (lane & 7) + ((lane >> 3) & 1) * 8;  // row of the 16-row group (ldmatrix)
+    const int li = warp * 32 + gi * 16 + i;
+    const int grow = __shfl_sync(0xffffffffu, row, gi * 16 + i);
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      uint32_t af[4];
+      ldsm_x4(af[0], af[1], af[2], af[3], sbase + li * 256 + (swz_chunk(2 * ks + (lane >> 4), grow) << 4));
+      mma_bf16_16816(s, af, qb[ks][0], qb[ks][1]);
+    }
+    if ((lane & 3) == 0) {
+      lg_s[warp * 32 + gi * 16 + (lane >> 2)] = s[0] * 0.08838834764831845f;
+      lg_s[warp * 32 + gi * 16 + (lane >> 2) + 8] = s[2] * 0.08838834764831845f;
     }
   }
   __syncthreads();
-  const int base_slot = blockIdx.x * 64 + warp * 16;
-  // lanes 0..15: slot -> rank -> (r, row)
-  int myrow = -1;
-  if (lane < 16 && base_slot + lane < sc.slots) {
-    const int rank = slot_rank(base_slot + lane, sc);
-    int lo = 0, hi = C - 1;  // smallest r with ends[r] >= rank
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (s_ends[mid] >= rank) hi = mid; else lo = mid + 1;
+  const float lg = lg_s[tid];
+  if (valid) logits[ug * sc.slots + slot] = lg;
+  float mx = valid ? lg : -INFINITY;
+  mx = warp_max(mx);
+  if (lane == 0) redf[warp] = mx;
+  __syncthreads();
+  float mb = redf[0];
+#pragma unroll
+  for (int w = 1; w < SB / 32; ++w) mb = fmaxf(mb, redf[w]);
+  double e = valid ? exp((double)lg - (double)mb) : 0.0;
+  const int W1 = 2 * sc.w + 1;
+  double sh = 0.0, s1 = 0.0, s2 = 0.0;
+  if (sc.fallback || slot < sc.N) sh = e;
+  else if (slot < sc.N + W1) s1 = e;
+  else s2 = e;
+  sh = warp_sum_d(sh);
+  s1 = warp_sum_d(s1);
+  s2 = warp_sum_d(s2);
+  if (lane == 0) { redd[warp][0] = sh; redd[warp][1] = s1; redd[warp][2] = s2; }
+  __syncthreads();
+  if (tid == 0) {
+    double a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+    for (int w = 0; w < SB / 32; ++w) { a0 += redd[w][0]; a1 += redd[w][1]; a2 += redd[w][2]; }
+    double* o = summ + (ug * nb + blockIdx.x) * 4;
+    o[0] = (double)mb; o[1] = a0; o[2] = a1; o[3] = a2;
+  }
+  pdl_launch_dependents();
+}
+
+// ------------------------------------------------------------------ S5-S7 from the summaries
+struct FitParams {
+  const double* summ;     // [units][G][nb][4]: m_b, head sum, window-1 sum, window-2 sum
+  const float* logits;    // [units][G][slots]
+  const int* order;
+  const int* ends;
+  const int* offsets;
+  int n, C, G, units, nb;
+  SampleConsts sc;
+  double p;
+  double* fit;
+  int* J;
+  uint8_t* mask_acc;
+  uint8_t* umask;
+  int* ulist;
+  int* uprefix;
+  long long* unit_prefix;
+  unsigned int* head_cnt;
+  unsigned int* unit_cnt;
+  unsigned long long* tlog;  // nullable debug stamps
+};
+
+constexpr int FIT_THREADS = 256;
+
+// debug: %globaltimer stamp i of the fit kernel's CTA (g, u == 0) / of the last CTAs
+#define FIT_STAMP(i)                                                     \
+  if (P.tlog && tid == 0 && (u == 0 || (i) >= 8)) {                      \
+    unsigned long long t_;                                               \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));               \
+    P.tlog[256 + ((i) >= 8 ? 64 + (i) : g * 8 + (i))] = t_;              \
+    if ((i) < 8) P.tlog[256 + 96 + g * 8 + (i)] = clock64();             \
+  }
+
+__global__ void __launch_bounds__(FIT_THREADS) fit_kernel(const FitParams P) {
+  __shared__ double redd[32];
+  __shared__ float redf[32];
+  __shared__ int redi[32];
+  __shared__ long long sh_k;
+  __shared__ double s_pref[FIT_THREADS];
+  __shared__ bool s_last;
+  __shared__ int s_totc, s_tott;
+  extern __shared__ __align__(16) uint8_t fsm[];
+  const int g = blockIdx.x, u = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
+  const int C = P.C, n = P.n, nb = P.nb;
+  const SampleConsts sc = P.sc;
+  const size_t ug = (size_t)u * P.G + g;
+  // everything this CTA reads is staged in smem up front (one round trip): the static
+  // cluster offsets before the dependency wait, the previous kernels' outputs after it
+  double* sm = (double*)fsm;                 // [nb][4]
+  int* s_off = (int*)(sm + (size_t)nb * 4);  // [C+1]
+  int* s_end = s_off + C + 1;                // [C]
+  int* s_ord = s_end + C;                    // [C]
+  FIT_STAMP(0);
+  for (int i = tid; i <= C; i += nt) s_off[i] = P.offsets[(size_t)u * (C + 1) + i];
+  pdl_wait();
+  FIT_STAMP(1);
+  for (int i = tid; i < nb * 4; i += nt) sm[i] = P.summ[ug * nb * 4 + i];
+  for (int i = tid; i < C; i += nt) {
+    s_end[i] = P.ends[ug * C + i];
+    s_ord[i] = P.order[ug * C + i];
+  }
+  __syncthreads();
+  FIT_STAMP(2);
+  // common shift m = max of the block maxima (reading 13)
+  float mloc = -INFINITY;
+  for (int b = tid; b < nb; b += nt) mloc = fmaxf(mloc, (float)sm[b * 4]);
+  const double m = (double)block_reduce<float, RED_MAX>(mloc, redf);
+  double eh = 0.0, e1 = 0.0, e2 = 0.0;
+  for (int b = tid; b < nb; b += nt) {
+    const double f = exp(sm[b * 4] - m);
+    eh += sm[b * 4 + 1] * f;
+    e1 += sm[b * 4 + 2] * f;
+    e2 += sm[b * 4 + 3] * f;
+  }
+  const double EN = block_reduce<double, RED_SUM>(eh, redd);
+  double a = 0.0, b = 0.0, mu1 = 0.0, mu2 = 0.0, W = EN;
+  if (!sc.fallback) {
+    const int W1 = 2 * sc.w + 1;
+    mu1 = block_reduce<double, RED_SUM>(e1, redd) / (double)W1;
+    mu2 = block_reduce<double, RED_SUM>(e2, redd) / (double)W1;
+    const double x1 = (double)sc.x1, x2 = (double)sc.x2;
+    a = (mu1 - mu2) * x1 * x2 / (x2 - x1);  // O8 / Alg. 1 l.4
+    b = mu1 - a / x1;
+    W = EN + tail_mass(a, b, sc.N, n);
+  }
+  FIT_STAMP(3);
+  long long kstar = (long long)n + 1;  // p >= 1: every rank (reading 15)
+  if (P.p < 1.0) {
+    const double target = P.p * W;
+    if (EN >= target) {
+      // exact head: the crossing block (head slots are the first nex slots, in rank order)
+      const int nex = sc.fallback ? n : sc.N;
+      const int nbh = (nex + SB - 1) / SB;
+      double bh = 0.0;
+      if (tid < nbh) bh = sm[tid * 4 + 1] * exp(sm[tid * 4] - m);
+      double run = block_exclusive_scan<double>(bh, redd, (double*)nullptr);  // nbh <= blockDim (checked on host)
+      s_pref[tid] = run + bh;
+      __syncthreads();
+      if (tid == 0) {
+        int bs = nbh - 1;
+        for (int i = 0; i < nbh; ++i)
+          if (s_pref[i] >= target) { bs = i; break; }
+        sh_k = bs;
+      }
+      __syncthreads();
+      const int bs = (int)sh_k;
+      const double before = bs ? s_pref[bs - 1] : 0.0;
+      __syncthreads();
+      // within the block: warp 0 loads its (<= SB = 128) head slots at once, 4 per lane,
+      // scans the four 32-slot chunks in parallel, then carries the chunk totals
+      if (tid < 32) {
+        const int s0 = bs * SB, s1 = min(nex, s0 + SB);
+        double w[SB / 32];
+#pragma unroll
+        for (int k = 0; k < SB / 32; ++k) {
+          const int s = s0 + k * 32 + tid;
+          w[k] = s < s1 ? exp((double)__ldcg(P.logits + ug * sc.slots + s) - m) : 0.0;
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+          for (int k = 0; k < SB / 32; ++k) {
+            const double x = __shfl_up_sync(0xffffffffu, w[k], o);
+            if (tid >= o) w[k] += x;
+          }
+        double acc = before;
+        int found = -1;
+#pragma unroll
+        for (int k = 0; k < SB / 32; ++k) {
+          const int s = s0 + k * 32 + tid;
+          const unsigned hit = __ballot_sync(0xffffffffu, s < s1 && acc + w[k] >= target);
+          if (found < 0 && hit) found = s0 + k * 32 + __ffs(hit) - 1;
+          acc += __shfl_sync(0xffffffffu, w[k], 31);
+        }
+        if (tid == 0) sh_k = (found >= 0 ? found : s1 - 1) + 1;  // rounding guard: the block's last slot
+      }
+      __syncthreads();
+      kstar = sh_k;
+    } else {
+      const double aa = a, bb = b, en_ = EN;
+      const long long NN = sc.N;
+      kstar = block_lower_bound(NN + 1, n, [&](long long k) { return en_ + tail_mass(aa, bb, NN, k) >= target; },
+                                &sh_k);
     }
-    const int sr = lo ? s_ends[lo - 1] : 0;
-    myrow = __ldg(rowstart + ug * C + lo) + (rank - 1 - sr);
   }
-  uint4 kv[8];
-  int rows[8];
-#pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    rows[it] = __shfl_sync(0xffffffffu, myrow, it * 2 + half);
-    kv[it] = rows[it] >= 0
-                 ? __ldg(reinterpret_cast<const uint4*>(Kp + ((size_t)u * n + rows[it]) * 128 +
-                                                        swz_chunk(l16, rows[it]) * 8))
-                 : make_uint4(0, 0, 0, 0);
+  // J = #{r : s_r < k*} = 1 + #{r < C-1 : e_r < k*}; mark the selected non-empty clusters
+  FIT_STAMP(4);
+  const int* en = s_end;
+  const int* ord = s_ord;
+  const int* off = s_off;
+  int cnt = 0;
+  for (int r = tid; r < C - 1; r += nt) cnt += en[r] < kstar;
+  const int J = 1 + block_reduce<int, RED_SUM>(cnt, redi);
+  uint8_t* macc = P.mask_acc + (size_t)u * C;
+  for (int r = tid; r < J; r += nt) {
+    const int cid = ord[r];
+    if (off[cid + 1] > off[cid]) macc[cid] = 1;
   }
-  float dot[8];
-#pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kv[it]);
-    float d = 0.f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float2 f = __bfloat1622float2(k2[i]);
-      d = fmaf(qf[2 * i], f.x, d);
-      d = fmaf(qf[2 * i + 1], f.y, d);
+  if (tid == 0) {
+    P.J[ug] = J;
+    double* f = P.fit + ug * 6;
+    f[0] = a; f[1] = b; f[2] = m; f[3] = W; f[4] = mu1; f[5] = mu2;
+  }
+  FIT_STAMP(5);
+
+  // ---- S7: the last head of the unit compacts the union (cluster-id order)
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&P.head_cnt[u], 1u);
+    s_last = (prev == (unsigned)P.G - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  FIT_STAMP(8);
+  {
+    const int per = (C + nt - 1) / nt;
+    const int b0 = tid * per;
+    int lc = 0, lt = 0;
+    for (int j = b0; j < b0 + per && j < C; ++j)
+      if (__ldcg(macc + j)) { ++lc; lt += off[j + 1] - off[j]; }
+    int cbase = block_exclusive_scan<int>(lc, redi, &s_totc);
+    int tbase = block_exclusive_scan<int>(lt, redi, &s_tott);
+    int* ul = P.ulist + (size_t)u * C;
+    int* up = P.uprefix + (size_t)u * (C + 1);
+    uint8_t* um = P.umask + (size_t)u * C;
+    for (int j = b0; j < b0 + per && j < C; ++j) {
+      const uint8_t mk = __ldcg(macc + j);
+      um[j] = mk;
+      macc[j] = 0;  // reset the accumulator for the next call
+      if (mk) {
+        ul[cbase] = off[j];
+        up[cbase] = tbase;
+        ++cbase;
+        tbase += off[j + 1] - off[j];
+      }
     }
-    dot[it] = d;
+    const int ucount = s_totc, tot = s_tott;
+    for (int k = ucount + tid; k <= C; k += nt) {
+      up[k] = tot;
+      if (k < C) ul[k] = 0;
+    }
   }
-#pragma unroll
-  for (int it = 0; it < 8; ++it)
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) dot[it] += __shfl_xor_sync(0xffffffffu, dot[it], o);
-  if (l16 == 0) {
-#pragma unroll
-    for (int it = 0; it < 8; ++it)
-      if (rows[it] >= 0) logits[ug * sc.slots + base_slot + it * 2 + half] = dot[it] * 0.08838834764831845f;
+  if (tid == 0) P.head_cnt[u] = 0;
+  FIT_STAMP(9);
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(P.unit_cnt, 1u);
+    s_last = (prev == (unsigned)P.units - 1);
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    FIT_STAMP(10);
+    const int units = P.units;
+    const int per = (units + nt - 1) / nt;
+    const int b0 = tid * per;
+    long long loc = 0;
+    for (int v = b0; v < b0 + per && v < units; ++v) loc += __ldcg(P.uprefix + (size_t)v * (C + 1) + C);
+    long long run = block_exclusive_scan<long long>(loc, (long long*)redd, (long long*)nullptr);
+    for (int v = b0; v < b0 + per && v < units; ++v) {
+      P.unit_prefix[v] = run;
+      run += __ldcg(P.uprefix + (size_t)v * (C + 1) + C);
+    }
+    if (b0 < units && b0 + per >= units) P.unit_prefix[units] = run;
+    if (tid == 0) *P.unit_cnt = 0u;
+    FIT_STAMP(11);
   }
   pdl_launch_dependents();
 }
@@ -669,7 +957,7 @@ cudaError_t launch_score(const SelArgs& a, cudaStream_t s, bool pdl) {
 }
 
 static cudaError_t ensure_smem(const void* fn, size_t smem, size_t* done) {
-  if (smem > 48 * 1024 && smem > *done) {
+  if (smem > 40 * 1024 && smem > *done) {  // static smem counts against the 48 KB default too
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     *done = smem;
@@ -679,22 +967,59 @@ static cudaError_t ensure_smem(const void* fn, size_t smem, size_t* done) {
 
 cudaError_t launch_sort(const SelArgs& a, cudaStream_t s, bool pdl) {
   tactic_index_s* x = a.idx;
-  const size_t smem = (size_t)x->C * (8 + 4 * 3) + (size_t)NBUCKET * 4 * 5;
+  const size_t smem = (size_t)x->C * (8 + 4 * 5) + (size_t)NBUCKET * 4 * 5;
   static size_t done = 0;
   cudaError_t e = ensure_smem((const void*)rank_kernel, smem, &done);
   if (e != cudaSuccess) return e;
   cudaLaunchAttribute attr[1];
   auto cfg = make_cfg(dim3(x->G, x->units), dim3(RANK_THREADS), smem, s, pdl, attr);
   return cudaLaunchKernelEx(&cfg, rank_kernel, (const double*)x->crit, (const int*)x->offsets, x->C, x->G,
-                            x->order, x->ends, x->rowstart);
+                            x->order, x->ends, x->rowstart, x->sc, x->rowmap);
 }
+
+int sample_blocks(int slots) { return (slots + SB - 1) / SB; }
 
 cudaError_t launch_sample(const SelArgs& a, cudaStream_t s, bool pdl) {
   tactic_index_s* x = a.idx;
+  const int nb = sample_blocks(x->sc.slots);
   cudaLaunchAttribute attr[1];
-  auto cfg = make_cfg(dim3((x->sc.slots + 63) / 64, x->G, x->units), dim3(128), (size_t)x->C * 4, s, pdl, attr);
-  return cudaLaunchKernelEx(&cfg, sample_kernel, a.q, (const __nv_bfloat16*)x->Kp, (const int*)x->ends,
-                            (const int*)x->rowstart, x->n, x->C, x->G, x->sc, x->logits);
+  auto cfg = make_cfg(dim3(nb, x->G, x->units), dim3(SB), 0, s, pdl, attr);
+  return cudaLaunchKernelEx(&cfg, sample_kernel, a.q, (const __nv_bfloat16*)x->Kp, (const int*)x->rowmap, x->n,
+                            x->G, x->sc, x->logits, x->summ, nb);
+}
+
+cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
+  tactic_index_s* x = a.idx;
+  FitParams P = {};
+  P.summ = x->summ;
+  P.logits = x->logits;
+  P.order = x->order;
+  P.ends = x->ends;
+  P.offsets = x->offsets;
+  P.n = x->n;
+  P.C = x->C;
+  P.G = x->G;
+  P.units = x->units;
+  P.nb = sample_blocks(x->sc.slots);
+  P.sc = x->sc;
+  P.p = a.p;
+  P.fit = x->fit;
+  P.J = x->J;
+  P.mask_acc = x->mask_acc;
+  P.umask = x->umask;
+  P.ulist = x->union_list;
+  P.uprefix = x->union_prefix;
+  P.unit_prefix = x->unit_prefix;
+  P.head_cnt = x->head_cnt;
+  P.unit_cnt = x->counter;
+  P.tlog = x->tlog;
+  cudaLaunchAttribute attr[1];
+  const size_t smem = (size_t)P.nb * 32 + (size_t)(3 * x->C + 1) * 4 + 16;
+  static size_t done = 0;
+  cudaError_t e = ensure_smem((const void*)fit_kernel, smem, &done);
+  if (e != cudaSuccess) return e;
+  auto cfg = make_cfg(dim3(x->G, x->units), dim3(FIT_THREADS), smem, s, pdl, attr);
+  return cudaLaunchKernelEx(&cfg, fit_kernel, P);
 }
 
 cudaError_t launch_select(const SelArgs& a, cudaStream_t s, bool pdl) {

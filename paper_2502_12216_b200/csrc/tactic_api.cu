@@ -188,6 +188,8 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_
   x->o_stage = A.get<__nv_bfloat16>(U * G * 128);
   x->unit_cnt = A.get<int>(U);
   x->rowstart = A.get<int>(U * G * C);
+  x->rowmap = A.get<int>(U * G * (size_t)x->sc.slots);
+  x->summ = A.get<double>(U * G * (size_t)sample_blocks(x->sc.slots) * 4);
   x->mask_acc = A.get<uint8_t>(U * C);
   x->head_cnt = A.get<unsigned int>(U);
   if (A.err != cudaSuccess) {
@@ -473,14 +475,13 @@ static tactic_status_t run_selection(const void* q, tactic_index_t idx, double p
     CK(launch_select_fused((const __nv_bfloat16*)q, idx, p, s, pdl));
     return TACTIC_OK;
   }
+  CK(launch_score(sa, s, pdl));      // S1
   if (mode != 1) {
-    CK(launch_score(sa, s, pdl));
-    CK(launch_sort(sa, s, pdl));
-    CK(launch_sample(sa, s, pdl));
-  } else {
-    CK(launch_score(sa, s, pdl));
+    CK(launch_sort(sa, s, pdl));     // S2, S3 (+ sampled-slot row map)
+    CK(launch_sample(sa, s, pdl));   // S4 (+ per-block fit summaries)
   }
-  CK(launch_select(sa, s, pdl));
+  if (mode == 0) CK(launch_fit(sa, s, pdl));     // S5-S7
+  else CK(launch_select(sa, s, pdl));            // sharded stage rules
   return TACTIC_OK;
 }
 

@@ -377,5 +377,7 @@ def test_fused_matches_multikernel_path(T, monkeypatch):
         assert np.array_equal(a["order"], b["order"])
         assert np.array_equal(a["J"], b["J"])
         assert np.array_equal(a["union_mask"], b["union_mask"])
-        np.testing.assert_allclose(a["fit"], b["fit"], rtol=1e-6, atol=1e-12)
+        # fp32 tensor-core vs fp32 FMA logits, different summation trees: same decisions,
+        # fit values equal to ~1e-5 relative (b ~ 0 compared absolutely)
+        np.testing.assert_allclose(a["fit"], b["fit"], rtol=1e-4, atol=1e-7)
         assert torch.allclose(a["out"].float(), b["out"].float(), atol=1e-2)
