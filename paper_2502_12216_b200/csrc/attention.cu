@@ -87,6 +87,25 @@ __device__ __forceinline__ int warp_floor_search(const T* arr, int count, T key)
   return base + (31 - __clz(bal));
 }
 
+// Unit-aligned split (units <= CTAs / 2): every CTA works on exactly one unit, the unit's
+// tokens divided evenly among the unit's CTAs; CTAs are apportioned to units by largest
+// remainder on their token counts (selection kernel, `cta_map`) or equally (dense / p = 1).
+// No CTA straddles two units, so a unit's last piece is not delayed behind another
+// unit's piece, and the unit's partials sit in slots equal to the CTA indices.
+struct UnitSplit {
+  int u, j, n;  // unit, index of this CTA within the unit, CTAs of the unit (0: idle)
+};
+__device__ __forceinline__ UnitSplit unit_split_of(const AttnArgs& a, int cta, int P) {
+  if (a.cta_map) {
+    const int4 m = a.cta_map[cta];
+    return {m.x, m.y, m.z};
+  }
+  const int U = a.units, base = P / U, rem = P % U;
+  if (cta < rem * (base + 1)) return {cta / (base + 1), cta % (base + 1), base + 1};
+  const int c2 = cta - rem * (base + 1);
+  return {rem + c2 / base, c2 % base, base};
+}
+
 template <int G, bool DENSE>
 __global__ void __launch_bounds__(ATT_THREADS, 1)
     attention_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tmK,
@@ -130,18 +149,38 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     }
   };
   if (threadIdx.x == 0) stamp(0);
+  if (a.tlog && threadIdx.x == 0 && 2 * cta + 1 < 512) {  // per-CTA start / end (debug)
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    a.tlog[512 + 2 * cta] = t_;
+  }
   int ntile_dbg = 0;
   const long long T = DENSE ? dense_total : a.unit_prefix[a.units];
+
+  // unit-aligned split: CTA cta works on one unit only (see UnitSplit)
+  UnitSplit us_ = {0, 0, 0};
+  const bool unit_mode = a.unit_split != 0 || a.cta_map != nullptr;
+  if (unit_mode) us_ = unit_split_of(a, cta, P);
 
   if (warp == 0) {
     // ============================ producer (warp-uniform control flow) ============================
     const bool leader = lane == 0;
     long long t = range_start(cta, T, P);
-    const long long t_end = range_start(cta + 1, T, P);
+    long long t_end = range_start(cta + 1, T, P);
     int stage = 0;
     uint32_t phase = 0;
     int u = 0;
-    if (t < t_end) {
+    if (unit_mode) {
+      u = us_.u;
+      if (us_.n > 0) {
+        const long long ub = DENSE || a.cta_map == nullptr ? (long long)u * a.n : a.unit_prefix[u];
+        const long long tu = (DENSE || a.cta_map == nullptr ? (long long)a.n : a.unit_prefix[u + 1] - ub);
+        t = ub + tu * us_.j / us_.n;
+        t_end = ub + tu * (us_.j + 1) / us_.n;
+      } else {
+        t = t_end = 0;
+      }
+    } else if (t < t_end) {
       if (DENSE) {
         u = (int)(t / a.n);
       } else {  // largest u with unit_prefix[u] <= t
@@ -374,7 +413,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       }
       asm volatile("bar.sync 1, %0;" ::"n"(ATT_CWARPS * 32));
       const int u = md.unit;
-      const size_t slot = (size_t)cta + u;
+      // partial slot: the CTA index (unit-aligned split: one piece per CTA) or cta + unit
+      // (global split: a CTA may hold pieces of several units; c + u is unique)
+      const size_t slot = unit_mode ? (size_t)cta : (size_t)cta + u;
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         float mf = -INFINITY;
@@ -391,55 +432,86 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         a.part_o[(slot * G + g) * 128 + ct] = of / lf;
         if (ct == 0) a.part_lse[slot * G + g] = (mf + log2f(lf)) * 0.6931471805599453f;
       }
-      // ---- arrival: is this the unit's last piece?
-      __threadfence();
+      // ---- arrival: is this the unit's last piece?  The barrier orders every consumer
+      // thread's partial stores before thread 0's gpu-scope fence and atomic (fences are
+      // cumulative), and the merging CTA fences again before reading the others' partials.
       asm volatile("bar.sync 1, %0;" ::"n"(ATT_CWARPS * 32));
       const long long us = DENSE ? (long long)u * a.n : a.unit_prefix[u];
       const long long ue = DENSE ? us + a.n : a.unit_prefix[u + 1];
       int c0 = 0;
-      const int np = pieces_of_unit(us, ue, T, P, &c0);
+      const int np = unit_mode ? us_.n : pieces_of_unit(us, ue, T, P, &c0);
+      if (unit_mode) c0 = cta - us_.j;
       if (ct == 0) {
+        __threadfence();
         const int prev = atomicAdd(&a.unit_cnt[u], 1);
         s_merge = (prev == np - 1);
+        if (s_merge) __threadfence();
       }
       asm volatile("bar.sync 1, %0;" ::"n"(ATT_CWARPS * 32));
+      if (s_merge && a.tlog && ct == 0 && u < 8) {  // debug: merge start
+        unsigned long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+        a.tlog[964 + 2 * u] = t_;
+      }
       if (s_merge) {
         // ---- S9: merge this unit's pieces (slots c + u), LSE-weighted
-        __threadfence();
         // warp w merges heads w, w+4, ...; lanes hold 4 dims; piece weights are computed
         // 32 at a time (one per lane) and broadcast, so the o loads are independent.
-        const int c1 = cta_of(ue - 1, T, P);
-        const int span = c1 - c0 + 1;
+        const int span = unit_mode ? np : cta_of(ue - 1, T, P) - c0 + 1;
+        const int soff = unit_mode ? 0 : u;  // slot = c + soff
         for (int g = cw; g < G; g += ATT_CWARPS) {
-          float mx = -INFINITY;
-          for (int i = lane; i < span; i += 32) {
-            const int c = c0 + i;
-            if (T >= P || range_start(c, T, P) != range_start(c + 1, T, P))
-              mx = fmaxf(mx, __ldcg(a.part_lse + ((size_t)c + u) * G + g));
-          }
-          mx = warp_max(mx);
-          float sum = 0.f;
+          // chunks of 32 pieces: the lane's piece lse and the chunk's first 16 partial rows
+          // are loaded together (the row loads do not depend on the lse), the running max
+          // is rescaled online across chunks
+          float mx = -INFINITY, sum = 0.f;
           float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
           for (int i0 = 0; i0 < span; i0 += 32) {
             const int i = i0 + lane;
-            float wl = 0.f;
-            if (i < span && (T >= P || range_start(c0 + i, T, P) != range_start(c0 + i + 1, T, P)))
-              wl = __expf(__ldcg(a.part_lse + ((size_t)(c0 + i) + u) * G + g) - mx);
-            sum += wl;
+            const bool live = i < span && (unit_mode || T >= P ||
+                                           range_start(c0 + i, T, P) != range_start(c0 + i + 1, T, P));
+            const unsigned lmask = __ballot_sync(0xffffffffu, live);
             const int cnt = span - i0 < 32 ? span - i0 : 32;
-#pragma unroll 8
-            for (int j = 0; j < cnt; ++j) {
-              const float w = __shfl_sync(0xffffffffu, wl, j);
+            const float l = live ? __ldcg(a.part_lse + ((size_t)(c0 + i) + soff) * G + g) : -INFINITY;
+            float4 v[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
               const float4* src =
-                  reinterpret_cast<const float4*>(a.part_o + (((size_t)(c0 + i0 + j) + u) * G + g) * 128) + lane;
-              const float4 v = w != 0.f ? __ldcg(src) : make_float4(0.f, 0.f, 0.f, 0.f);
-              acc.x = fmaf(w, v.x, acc.x);
-              acc.y = fmaf(w, v.y, acc.y);
-              acc.z = fmaf(w, v.z, acc.z);
-              acc.w = fmaf(w, v.w, acc.w);
+                  reinterpret_cast<const float4*>(a.part_o + (((size_t)(c0 + i0 + k) + soff) * G + g) * 128) + lane;
+              v[k] = (k < cnt && ((lmask >> k) & 1u)) ? __ldcg(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            const float nm = fmaxf(mx, warp_max(l));
+            const float sc = mx == -INFINITY ? 0.f : __expf(mx - nm);
+            acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
+            sum *= sc;
+            mx = nm;
+            const float wl = live ? __expf(l - mx) : 0.f;
+            sum += warp_sum(wl);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const float w = __shfl_sync(0xffffffffu, wl, k);
+              acc.x = fmaf(w, v[k].x, acc.x);
+              acc.y = fmaf(w, v[k].y, acc.y);
+              acc.z = fmaf(w, v[k].z, acc.z);
+              acc.w = fmaf(w, v[k].w, acc.w);
+            }
+            if (cnt > 16) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                const int j = 16 + k;
+                const float4* src =
+                    reinterpret_cast<const float4*>(a.part_o + (((size_t)(c0 + i0 + j) + soff) * G + g) * 128) + lane;
+                v[k] = (j < cnt && ((lmask >> j) & 1u)) ? __ldcg(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                const float w = __shfl_sync(0xffffffffu, wl, 16 + k);
+                acc.x = fmaf(w, v[k].x, acc.x);
+                acc.y = fmaf(w, v[k].y, acc.y);
+                acc.z = fmaf(w, v[k].z, acc.z);
+                acc.w = fmaf(w, v[k].w, acc.w);
+              }
             }
           }
-          sum = warp_sum(sum);
           const float inv = 1.f / sum;
           const size_t orow = ((size_t)u * G + g) * 128 + lane * 4;
           if (a.out) {
@@ -453,6 +525,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           if (a.lse && lane == 0) a.lse[(size_t)u * G + g] = mx + logf(sum);
         }
         if (ct == 0) a.unit_cnt[u] = 0;  // self-reset for the next call
+        if (a.tlog && ct == 0 && u < 8) {
+          unsigned long long t_;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+          a.tlog[965 + 2 * u] = t_;
+        }
       }
       m0 = m1 = -INFINITY;
       l0 = l1 = 0.f;
@@ -461,6 +538,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     }
   }
   if (ct == 0) stamp(34);
+  if (a.tlog && ct == 0 && 2 * cta + 1 < 512) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    a.tlog[512 + 2 * cta + 1] = t_;
+    a.tlog[816 + cta] = (unsigned long long)ntile_dbg;
+  }
   pdl_launch_dependents();
 }
 
@@ -514,7 +597,7 @@ static cudaError_t launch_attn_t(const AttnArgs& a, const CUtensorMap* tmK, cons
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, a, tmK ? *tmK : dummy, tmV ? *tmV : dummy, dense_total);
 }
 

@@ -21,6 +21,12 @@ struct SampleConsts {
   int slots;  // logits computed per head: N + 2(2w+1), or n in fallback
 };
 SampleConsts sample_consts(int n);
+// programmatic dependent launch between the decode kernels (TACTIC_NO_PDL=1 disables)
+bool pdl_enabled();
+
+// Unit-aligned attention split applies when every unit can get >= 2 CTAs (and the
+// selection kernel can apportion them in one CTA: units <= 128).
+inline bool unit_split_ok(int units, int ctas) { return units <= 128 && 2 * units <= ctas; }
 
 // Token-range split of a global work list over P CTAs: CTA c owns [rs(c), rs(c+1)).
 __host__ __device__ inline long long range_start(int c, long long T, int P) {
@@ -49,6 +55,8 @@ struct tactic_index_s {
   int* iters_run = nullptr;      // [units]
   int* all_list = nullptr;       // [units][C]  rows of non-empty clusters (p >= 1 work list)
   int* unit_cnt = nullptr;       // [units] attention arrival counters
+  int4* cta_map = nullptr;       // [num_ctas] unit-aligned attention split (written by the fit kernel)
+  bool map_ready = false;        // the last selection wrote cta_map
   int* all_prefix = nullptr;     // [units][C+1]
   long long* all_unit_prefix = nullptr;  // [units+1]
   // decode workspace
@@ -97,6 +105,8 @@ struct AttnArgs {
   float* out_f32;                  // nullable
   float* lse;                      // nullable [units][G]
   unsigned long long* tlog;        // nullable debug timestamps (CTA 0)
+  const int4* cta_map;             // nullable [num_ctas]: (unit, index in unit, CTAs of unit) from the selection
+  int unit_split;                  // 1: equal unit-aligned split (units <= CTAs/2, equal unit sizes)
 };
 cudaError_t launch_attention_sparse(const AttnArgs& a, int G, int num_ctas, cudaStream_t s, bool pdl);
 cudaError_t launch_attention_dense(const AttnArgs& a, const CUtensorMap* tmK, const CUtensorMap* tmV, int G,

@@ -459,6 +459,8 @@ struct FitParams {
   unsigned int* head_cnt;
   unsigned int* unit_cnt;
   unsigned long long* tlog;  // nullable debug stamps
+  int4* cta_map;             // nullable [num_ctas] unit-aligned attention split (units <= CTAs/2)
+  int num_ctas;
 };
 
 constexpr int FIT_THREADS = 256;
@@ -670,6 +672,353 @@ __global__ void __launch_bounds__(FIT_THREADS) fit_kernel(const FitParams P) {
     FIT_STAMP(11);
   }
   pdl_launch_dependents();
+}
+
+// ------------------------------------------------------------------ S5-S7, one CTA per unit
+// One warp per query head does the whole fit with warp-level reductions (no block
+// barriers on the per-head critical path); the G heads run concurrently and OR their
+// selections into a shared-memory mask that the CTA compacts into the work list.
+
+// H(k) - H(j) for 0 <= j <= k: exact sums below 20, otherwise one log and the
+// asymptotic series of both ends (harmonic() above, written as a difference)
+__device__ double harmonic_diff(long long k, long long j) {
+  if (k <= j) return 0.0;
+  if (j < 20) return harmonic(k) - harmonic(j);
+  const double xk = (double)k, xj = (double)j;
+  auto tail = [](double x) {
+    const double x2 = 1.0 / (x * x);
+    return 0.5 / x - x2 * (1.0 / 12.0 - x2 * (1.0 / 120.0 - x2 * (1.0 / 252.0 - x2 * (1.0 / 240.0 - x2 * (1.0 / 132.0)))));
+  };
+  return log1p((xk - xj) / xj) + tail(xk) - tail(xj);
+}
+
+// sum_{i=N+1}^{k} max(0, a/i + b) with one log per evaluation
+__device__ double tail_mass1(double a, double b, long long N, long long k) {
+  if (k <= N) return 0.0;
+  if (a >= 0.0 && b >= 0.0) return a * harmonic_diff(k, N) + b * (double)(k - N);
+  if (a <= 0.0 && b <= 0.0) return 0.0;
+  if (a > 0.0) {
+    const double t = a / (-b);
+    long long top = t >= 9.0e15 ? k : (long long)floor(t);
+    if (top > k) top = k;
+    while (top < k && a / (double)(top + 1) + b > 0.0) ++top;
+    while (top > N && !(a / (double)top + b > 0.0)) --top;
+    if (top <= N) return 0.0;
+    return a * harmonic_diff(top, N) + b * (double)(top - N);
+  }
+  const double t = (-a) / b;
+  long long lo = t >= 9.0e15 ? k + 1 : (long long)floor(t) + 1;
+  if (lo < N + 1) lo = N + 1;
+  while (lo > N + 1 && a / (double)(lo - 1) + b > 0.0) --lo;
+  while (lo <= k && !(a / (double)lo + b > 0.0)) ++lo;
+  if (lo > k) return 0.0;
+  return a * harmonic_diff(k, lo - 1) + b * (double)(k - lo + 1);
+}
+
+__global__ void __launch_bounds__(256) fit_unit_kernel(const FitParams P) {
+  extern __shared__ __align__(16) uint8_t fsm[];
+  __shared__ int redi[8];
+  __shared__ int s_totc, s_tott;
+  __shared__ bool s_last;
+  const int u = blockIdx.x, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int C = P.C, n = P.n, nb = P.nb, G = P.G;
+  const SampleConsts sc = P.sc;
+  double* sm = (double*)fsm;                       // [G][nb][4]
+  int* s_off = (int*)(sm + (size_t)G * nb * 4);     // [C+1]
+  int* s_end = s_off + ((C + 1 + 3) & ~3);         // [G][C] (16-byte aligned for bulk copies)
+  int* s_ord = s_end + (size_t)G * C;              // [G][C]
+  uint8_t* mask = (uint8_t*)(s_ord + (size_t)G * C);  // [C]
+  const unsigned long long stamp_on = P.tlog != nullptr && u == 0;
+  auto stamp = [&](int i) {
+    if (stamp_on && tid == 0) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      P.tlog[256 + i] = t_;
+    }
+  };
+  stamp(0);
+  for (int i = tid; i <= C; i += nt) s_off[i] = P.offsets[(size_t)u * (C + 1) + i];
+  for (int i = tid; i < C; i += nt) mask[i] = 0;
+  __shared__ uint64_t sbar;
+  const size_t ub = (size_t)u * G;
+  const bool bulk_ok = ((ub * C) % 4 == 0) && (((size_t)G * C) % 4 == 0);
+  if (tid == 0) {
+    mbar_init(&sbar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  stamp(1);
+  // stage the previous kernels' outputs with 1-D bulk copies (one round trip)
+  if (tid == 0) {
+    const uint32_t bs = (uint32_t)G * nb * 32, be = bulk_ok ? (uint32_t)G * C * 4 : 0u;
+    mbar_arrive_expect_tx(&sbar, bs + 2 * be);
+    bulk_g2s(sm, P.summ + ub * nb * 4, bs, &sbar);
+    if (bulk_ok) {
+      bulk_g2s(s_end, P.ends + ub * C, be, &sbar);
+      bulk_g2s(s_ord, P.order + ub * C, be, &sbar);
+    }
+  }
+  if (!bulk_ok)
+    for (int i = tid; i < G * C; i += nt) {
+      s_end[i] = P.ends[ub * C + i];
+      s_ord[i] = P.order[ub * C + i];
+    }
+  mbar_wait(&sbar, 0);
+  __syncthreads();
+  stamp(2);
+  for (int g = warp; g < G; g += nt / 32) {
+    const double* sg = sm + (size_t)g * nb * 4;
+    // common shift m = max of the block maxima (reading 13)
+    float mf = -INFINITY;
+    for (int b = lane; b < nb; b += 32) mf = fmaxf(mf, (float)sg[b * 4]);
+    mf = warp_max(mf);
+    const double m = (double)mf;
+    double eh = 0.0, e1 = 0.0, e2 = 0.0;
+    for (int b = lane; b < nb; b += 32) {
+      const double f = exp(sg[b * 4] - m);
+      eh += sg[b * 4 + 1] * f;
+      e1 += sg[b * 4 + 2] * f;
+      e2 += sg[b * 4 + 3] * f;
+    }
+    const double EN = warp_sum_d(eh);
+    double a = 0.0, b = 0.0, mu1 = 0.0, mu2 = 0.0, W = EN;
+    if (!sc.fallback) {
+      const int W1 = 2 * sc.w + 1;
+      mu1 = warp_sum_d(e1) / (double)W1;
+      mu2 = warp_sum_d(e2) / (double)W1;
+      const double x1 = (double)sc.x1, x2 = (double)sc.x2;
+      a = (mu1 - mu2) * x1 * x2 / (x2 - x1);  // O8 / Alg. 1 l.4
+      b = mu1 - a / x1;
+      W = EN + tail_mass1(a, b, sc.N, n);
+    }
+    long long kstar = (long long)n + 1;  // p >= 1: every rank (reading 15)
+    if (P.p < 1.0) {
+      const double target = P.p * W;
+      if (EN >= target) {
+        // crossing block of the exact head (head slots = the first nex slots)
+        const int nex = sc.fallback ? n : sc.N;
+        const int nbh = (nex + SB - 1) / SB;
+        double carry = 0.0;
+        int bs = nbh - 1;
+        double before = 0.0;
+        for (int b0 = 0; b0 < nbh; b0 += 32) {
+          const int bb = b0 + lane;
+          const double vo = bb < nbh ? sg[bb * 4 + 1] * exp(sg[bb * 4] - m) : 0.0;
+          double v = vo;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const double x = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += x;
+          }
+          const unsigned hit = __ballot_sync(0xffffffffu, bb < nbh && carry + v >= target);
+          if (hit) {
+            const int hl = __ffs(hit) - 1;
+            bs = b0 + hl;
+            before = carry + __shfl_sync(0xffffffffu, v, hl) - __shfl_sync(0xffffffffu, vo, hl);
+            break;
+          }
+          carry += __shfl_sync(0xffffffffu, v, 31);
+          before = carry;
+        }
+        // inside the block: its <= SB slots, 4 per lane, chunk scans + carries
+        const int s0 = bs * SB, s1 = min(nex, s0 + SB);
+        double w[SB / 32];
+#pragma unroll
+        for (int k = 0; k < SB / 32; ++k) {
+          const int s = s0 + k * 32 + lane;
+          w[k] = s < s1 ? exp((double)__ldcg(P.logits + (ub + g) * sc.slots + s) - m) : 0.0;
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+          for (int k = 0; k < SB / 32; ++k) {
+            const double x = __shfl_up_sync(0xffffffffu, w[k], o);
+            if (lane >= o) w[k] += x;
+          }
+        double acc = before;
+        int found = -1;
+#pragma unroll
+        for (int k = 0; k < SB / 32; ++k) {
+          const int s = s0 + k * 32 + lane;
+          const unsigned hit = __ballot_sync(0xffffffffu, s < s1 && acc + w[k] >= target);
+          if (found < 0 && hit) found = s0 + k * 32 + __ffs(hit) - 1;
+          acc += __shfl_sync(0xffffffffu, w[k], 31);
+        }
+        kstar = (found >= 0 ? found : s1 - 1) + 1;  // rounding guard: the block's last slot
+      } else {
+        // minimal k in (N, n] with EN + tail(k) >= target: 32-way warp search
+        long long lo = sc.N + 1, hi = n;
+        while (lo < hi) {
+          const long long step = (hi - lo + 32) / 32;  // ceil((hi-lo+1)/32)
+          const long long k = lo + (long long)lane * step;
+          const bool ok = k <= hi && EN + tail_mass1(a, b, sc.N, k) >= target;
+          const unsigned bal = __ballot_sync(0xffffffffu, ok);
+          const int h = bal ? __ffs(bal) - 1 : 32;
+          const long long nhi = h < 32 ? lo + (long long)h * step : hi;
+          const long long nlo = h > 0 ? lo + (long long)(h - 1) * step + 1 : lo;
+          lo = nlo;
+          hi = nhi < hi ? nhi : hi;
+          if (step == 1) { lo = hi; break; }
+        }
+        kstar = hi;
+      }
+    }
+    // J = #{r : s_r < k*} = 1 + #{r < C-1 : e_r < k*}; mark the selected non-empty clusters
+    const int* en = s_end + (size_t)g * C;
+    const int* ord = s_ord + (size_t)g * C;
+    int cnt = 0;
+    for (int r = lane; r < C - 1; r += 32) cnt += en[r] < kstar;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    const int J = 1 + cnt;
+    for (int r = lane; r < J; r += 32) {
+      const int cid = ord[r];
+      if (s_off[cid + 1] > s_off[cid]) mask[cid] = 1;
+    }
+    if (lane == 0) {
+      P.J[ub + g] = J;
+      double* f = P.fit + (ub + g) * 6;
+      f[0] = a; f[1] = b; f[2] = m; f[3] = W; f[4] = mu1; f[5] = mu2;
+    }
+  }
+  __syncthreads();
+  stamp(3);
+  // ---- S7: compact the union (cluster-id order) into the work list.  Warp w owns a
+  // contiguous cluster range; positions come from ballots and warp scans (no block scans).
+  {
+    __shared__ int w_cnt[8], w_tok[8];
+    const int nw = nt / 32;
+    const int CW = ((C + nw - 1) / nw + 31) & ~31;
+    const int jlo = warp * CW, jhi = min(C, jlo + CW);
+    int wc = 0, wt = 0;
+    for (int j0 = jlo; j0 < jhi; j0 += 32) {
+      const int j = j0 + lane;
+      const bool mk = j < jhi && mask[j];
+      int sz = mk ? s_off[j + 1] - s_off[j] : 0;
+      wc += __popc(__ballot_sync(0xffffffffu, mk));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, o);
+      wt += sz;
+    }
+    if (lane == 0) { w_cnt[warp] = wc; w_tok[warp] = wt; }
+    __syncthreads();
+    int cbase = 0, tbase = 0, ctot = 0, ttot = 0;
+    for (int w = 0; w < nw; ++w) {
+      if (w < warp) { cbase += w_cnt[w]; tbase += w_tok[w]; }
+      ctot += w_cnt[w];
+      ttot += w_tok[w];
+    }
+    int* ul = P.ulist + (size_t)u * C;
+    int* up = P.uprefix + (size_t)u * (C + 1);
+    uint8_t* um = P.umask + (size_t)u * C;
+    for (int j0 = jlo; j0 < jhi; j0 += 32) {
+      const int j = j0 + lane;
+      const bool mk = j < jhi && mask[j];
+      const int sz = mk ? s_off[j + 1] - s_off[j] : 0;
+      if (j < jhi) um[j] = mk;
+      const unsigned bal = __ballot_sync(0xffffffffu, mk);
+      int incl = sz;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+      }
+      if (mk) {
+        const int pos = cbase + __popc(bal & ((1u << lane) - 1u));
+        ul[pos] = s_off[j];
+        up[pos] = tbase + incl - sz;
+      }
+      cbase += __popc(bal);
+      tbase += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    // entries past the union: total tokens (keeps the prefix monotone for searches)
+    for (int k = ctot + tid; k <= C; k += nt) {
+      up[k] = ttot;
+      if (k < C) ul[k] = 0;
+    }
+  }
+  stamp(4);
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(P.unit_cnt, 1u);
+    s_last = (prev == (unsigned)P.units - 1);
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    if (P.tlog && tid == 0) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      P.tlog[256 + 5] = t_;
+    }
+    const int units = P.units;
+    const int per = (units + nt - 1) / nt;
+    const int b0 = tid * per;
+    long long loc = 0;
+    for (int v = b0; v < b0 + per && v < units; ++v) loc += __ldcg(P.uprefix + (size_t)v * (C + 1) + C);
+    __shared__ long long s_tot;  // block_exclusive_scan writes the total from one thread
+    long long run = block_exclusive_scan<long long>(loc, (long long*)fsm, &s_tot);
+    for (int v = b0; v < b0 + per && v < units; ++v) {
+      P.unit_prefix[v] = run;
+      run += __ldcg(P.uprefix + (size_t)v * (C + 1) + C);
+    }
+    if (tid == 0) {
+      P.unit_prefix[units] = s_tot;
+      *P.unit_cnt = 0u;
+    }
+    if (P.cta_map) {
+      // unit-aligned attention split: every unit gets 1 CTA plus its largest-remainder share
+      // of the others in proportion to its union tokens (capped at its token count)
+      __shared__ int s_n[128], s_f[128], s_cb[129];
+      __shared__ float s_fr[128];
+      __shared__ int s_R;
+      const int Pc = P.num_ctas, extra = Pc - units;
+      const double Ttot = (double)s_tot;
+      long long Tv = 0;
+      if (tid < units) {
+        Tv = __ldcg(P.uprefix + (size_t)tid * (C + 1) + C);
+        const double qv = Ttot > 0 ? (double)extra * (double)Tv / Ttot : 0.0;
+        s_f[tid] = (int)floor(qv);
+        s_fr[tid] = (float)(qv - floor(qv));
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int sf = 0;
+        for (int v = 0; v < units; ++v) sf += s_f[v];
+        s_R = extra - sf;
+      }
+      __syncthreads();
+      if (tid < units) {
+        int rank = 0;
+        for (int v = 0; v < units; ++v) rank += (s_fr[v] > s_fr[tid]) || (s_fr[v] == s_fr[tid] && v < tid);
+        const long long nv = 1 + s_f[tid] + (rank < s_R ? 1 : 0);
+        s_n[tid] = (int)(nv < Tv ? nv : (Tv > 0 ? Tv : 1));
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int acc = 0;
+        for (int v = 0; v < units; ++v) { s_cb[v] = acc; acc += s_n[v]; }
+        s_cb[units] = acc;
+      }
+      __syncthreads();
+      for (int c = tid; c < Pc; c += nt) {
+        int4 m = make_int4(0, 0, 0, 0);
+        if (c < s_cb[units]) {
+          int v = 0;
+          while (s_cb[v + 1] <= c) ++v;
+          m = make_int4(v, c - s_cb[v], s_n[v], 0);
+        }
+        P.cta_map[c] = m;
+      }
+    }
+    if (P.tlog && tid == 0) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      P.tlog[256 + 6] = t_;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ S4-S7
@@ -938,7 +1287,7 @@ static cudaLaunchConfig_t make_cfg(dim3 grid, dim3 block, size_t smem, cudaStrea
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
   return cfg;
 }
 
@@ -1013,13 +1362,17 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
   P.head_cnt = x->head_cnt;
   P.unit_cnt = x->counter;
   P.tlog = x->tlog;
+  P.num_ctas = x->num_ctas;
+  P.cta_map = unit_split_ok(x->units, x->num_ctas) ? x->cta_map : nullptr;
   cudaLaunchAttribute attr[1];
-  const size_t smem = (size_t)P.nb * 32 + (size_t)(3 * x->C + 1) * 4 + 16;
+  const size_t smem =
+      (size_t)x->G * P.nb * 32 + (size_t)(x->C + 4) * 4 + (size_t)2 * x->G * x->C * 4 + (size_t)x->C + 64;
   static size_t done = 0;
-  cudaError_t e = ensure_smem((const void*)fit_kernel, smem, &done);
+  cudaError_t e = ensure_smem((const void*)fit_unit_kernel, smem, &done);
   if (e != cudaSuccess) return e;
-  auto cfg = make_cfg(dim3(x->G, x->units), dim3(FIT_THREADS), smem, s, pdl, attr);
-  return cudaLaunchKernelEx(&cfg, fit_kernel, P);
+  const int threads = x->G * 32 > 128 ? x->G * 32 : 128;
+  auto cfg = make_cfg(dim3(x->units), dim3(threads), smem, s, pdl, attr);
+  return cudaLaunchKernelEx(&cfg, fit_unit_kernel, P);
 }
 
 cudaError_t launch_select(const SelArgs& a, cudaStream_t s, bool pdl) {

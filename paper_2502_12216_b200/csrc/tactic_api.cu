@@ -114,6 +114,14 @@ int device_sms() {
 }  // namespace
 
 namespace tactic {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TACTIC_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 SampleConsts sample_consts(int n) {
   SampleConsts s;
   const long long nn = n;
@@ -192,6 +200,7 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_
   x->summ = A.get<double>(U * G * (size_t)sample_blocks(x->sc.slots) * 4);
   x->mask_acc = A.get<uint8_t>(U * C);
   x->head_cnt = A.get<unsigned int>(U);
+  x->cta_map = A.get<int4>((size_t)x->num_ctas);
   if (A.err != cudaSuccess) {
     for (void* p : A.ptrs) cudaFree(p);
     delete x;
@@ -471,6 +480,8 @@ static tactic_status_t run_selection(const void* q, tactic_index_t idx, double p
   sa.gmass = gmass;
   sa.local_max = local_max;
   const bool pdl = true;
+  // the fit kernel (mode 0, multi-kernel path) also writes the unit-aligned attention split
+  idx->map_ready = mode == 0 && idx->fused_R == 0 && unit_split_ok(idx->units, idx->num_ctas);
   if (mode == 0 && idx->fused_R > 0) {  // one cluster-launched kernel for S1-S7
     CK(launch_select_fused((const __nv_bfloat16*)q, idx, p, s, pdl));
     return TACTIC_OK;
@@ -505,6 +516,11 @@ static tactic_status_t run_attention(const void* q, tactic_index_t idx, bool all
   aa.out_f32 = out_f32;
   aa.lse = lse;
   aa.tlog = idx->tlog;
+  // unit-aligned split: p >= 1 lists have n tokens per unit (equal split); union lists use
+  // the proportional map the fit kernel wrote
+  if (all) aa.unit_split = unit_split_ok(idx->units, idx->num_ctas) &&
+                           (idx->num_ctas + idx->units - 1) / idx->units <= idx->n;
+  else if (idx->map_ready) aa.cta_map = idx->cta_map;
   CK(launch_attention_sparse(aa, idx->G, idx->num_ctas, s, ev_mid == nullptr));  // S8 + fused S9
   if (ev_mid) CK(cudaEventRecord(ev_mid, s));
   return TACTIC_OK;
@@ -647,6 +663,7 @@ tactic_status_t tactic_dense_decode(const void* q, const void* K, const void* V,
   aa.unit_cnt = unit_cnt;
   aa.out = (__nv_bfloat16*)out;
   aa.lse = lse;
+  aa.unit_split = unit_split_ok((int)units, P) && (P + (int)units - 1) / (int)units <= r.n;
   CK(launch_attention_dense(aa, &mk, &mv, r.G, P, s, true));  // S10 + fused merge
   return TACTIC_OK;
 }

@@ -43,16 +43,11 @@ for it in range(4):
         continue
     print(f"--- iteration {it}")
     if R == 0:
-        fs = full[256:256 + 32].reshape(4, 8)
-        last = full[256 + 64 + 8:256 + 64 + 12]
-        t0 = fs[:, 0][fs[:, 0] > 0].min()
-        names = ["start", "pdl_wait", "staged", "fit", "k*", "J+mark"]
-        cl = full[256 + 96:256 + 128].reshape(4, 8)
-        for h in range(4):
-            print(f"  fit u0 g{h}: " + "  ".join(f"{nm} {(fs[h, i] - t0) / 1e3:6.2f}" for i, nm in enumerate(names)))
-            print(f"     SM clock over the CTA: {(cl[h, 5] - cl[h, 0]) / max(fs[h, 5] - fs[h, 0], 1) * 1e3:.0f} MHz")
-        print("  last head compaction: start %.2f end %.2f; last unit prefix: start %.2f end %.2f" %
-              tuple((x - t0) / 1e3 if x > 0 else float("nan") for x in last))
+        fs = full[256:256 + 7]
+        t0 = fs[0]
+        names = ["start", "pdl_wait", "staged", "heads fitted", "compacted", "last-unit start", "last-unit end"]
+        print("  fit CTA u0: " + "  ".join(f"{nm} {(fs[i] - t0) / 1e3:6.2f}" for i, nm in enumerate(names)
+                                             if fs[i] > 0))
     else:
         t = full.reshape(-1, 16, 8)[:, :R, :]
         t0 = t[:, :, 0].min()
@@ -70,3 +65,15 @@ for it in range(4):
         print(f"  attention CTA0: starts {(b0 - t0) / 1e3:.2f} us after selection start; ends +{(at[34] - b0) / 1e3:.2f}")
         print("   tiles issued at", np.round(iss, 2).tolist())
         print("   tiles consumed at", np.round(con, 2).tolist())
+        ce = full[512:512 + 296].reshape(-1, 2)
+        ce = ce[(ce[:, 0] > 0) & (ce[:, 1] > 0)]
+        if len(ce):
+            st, en = (ce[:, 0] - b0) / 1e3, (ce[:, 1] - b0) / 1e3
+            print(f"   all CTAs: start min {st.min():.2f} max {st.max():.2f}; end min {en.min():.2f} "
+                  f"median {np.median(en):.2f} max {en.max():.2f}; slowest CTA {int(np.argmax(en))}")
+            nt_ = full[816:816 + 148]
+            order = np.argsort(-en)[:8]
+            print("   slowest CTAs (cta, end us, tiles):", [(int(c), round(float(en[c]), 2), int(nt_[c])) for c in order])
+            print("   tiles per CTA: min %d median %d max %d" % (nt_.min(), np.median(nt_), nt_.max()))
+            mg = full[964:964 + 16].reshape(8, 2)
+            print("   merges (start, end) us:", [(round((s - b0) / 1e3, 2), round((e - b0) / 1e3, 2)) for s, e in mg if s > 0])
