@@ -3,9 +3,12 @@
 //
 // One kernel serves the sparse path (the GQA union of selected clusters) and
 // the dense baseline (all n tokens of the caller's K/V, Eq. 1-2).
-// Work balancing follows the paper's sub-request idea: the selected tokens of
-// all units form one global list that is cut into equal contiguous ranges, one per CTA,
-// so head-level imbalance becomes plain sequence imbalance.
+// Work balancing follows the paper's sub-request idea: units (KV heads) get CTAs
+// in proportion to their selected tokens and each unit's list is cut into equal
+// contiguous ranges, one per CTA (unit-aligned split, see UnitSplit), so head-level
+// imbalance becomes plain sequence imbalance.  With more units than CTAs/2 the lists of
+// all units form one global list cut into equal ranges instead (a CTA may then hold
+// pieces of two units).
 //
 // Per CTA: 1 producer warp streams 64-token stages of K and V into shared memory
 //   sparse: cp.async.bulk (1-D TMA, UBLKCP) of contiguous cluster runs from the
@@ -19,7 +22,8 @@
 //   the G<=8 query heads sit in the n=8 dimension), online softmax in the exp2 domain,
 //   P^T transposed in registers with movmatrix, O^T(128 x 8) += V^T P^T.
 // A piece (the part of one unit inside a CTA's range) ends with a cross-warp LSE
-// combine and one partial (o, lse) per head written to slot blockIdx.x + unit; a per-unit
+// combine and one partial (o, lse) per head written to slot blockIdx.x (unit-aligned) or
+// blockIdx.x + unit (global split); a per-unit
 // arrival counter elects the last CTA of the unit, which merges its pieces (S9).
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -87,23 +91,60 @@ __device__ __forceinline__ int warp_floor_search(const T* arr, int count, T key)
   return base + (31 - __clz(bal));
 }
 
-// Unit-aligned split (units <= CTAs / 2): every CTA works on exactly one unit, the unit's
-// tokens divided evenly among the unit's CTAs; CTAs are apportioned to units by largest
-// remainder on their token counts (selection kernel, `cta_map`) or equally (dense / p = 1).
-// No CTA straddles two units, so a unit's last piece is not delayed behind another
-// unit's piece, and the unit's partials sit in slots equal to the CTA indices.
+// Unit-aligned split (units <= CTAs / 2): every CTA works on exactly one unit.  Unit v
+// (T_v work-list tokens, S_v = tokens of the units before it, T = all tokens) owns CTAs
+// [cb_v, cb_{v+1}) with cb_v = v + floor((P - U) S_v / T): one CTA each plus a share of
+// the rest proportional to its tokens; CTA j of the unit's n_v owns tokens
+// [T_v j / n_v, T_v (j+1) / n_v) (possibly empty when T_v < n_v).  Every warp computes it
+// from the per-unit totals (seg_prefix[v][C]) with two shuffle scans, so the selection
+// needs no cross-unit step.  No CTA straddles two units, so a unit's last piece is not
+// delayed behind another unit's piece, and the unit's partials sit in slots cb_v + j.
 struct UnitSplit {
-  int u, j, n;  // unit, index of this CTA within the unit, CTAs of the unit (0: idle)
+  int u, j, n;       // unit, index of this CTA within the unit, CTAs of the unit
+  int lo, hi;        // token range within the unit's work list
 };
+template <bool DENSE>
 __device__ __forceinline__ UnitSplit unit_split_of(const AttnArgs& a, int cta, int P) {
-  if (a.cta_map) {
-    const int4 m = a.cta_map[cta];
-    return {m.x, m.y, m.z};
+  const int U = a.units, lane = threadIdx.x & 31;
+  auto tok = [&](int v) -> long long {
+    if (v >= U) return 0;
+    return DENSE ? (long long)a.n : (long long)__ldcg(a.seg_prefix + (size_t)v * (a.C + 1) + a.C);
+  };
+  long long T = 0;
+  for (int v0 = 0; v0 < U; v0 += 32) T += tok(v0 + lane);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) T += __shfl_xor_sync(0xffffffffu, T, o);
+  const bool uniform = T <= 0;  // degenerate: equal split by unit count
+  const long long Tt = uniform ? U : T;
+  const long long extra = P - U;
+  long long S = 0;
+  UnitSplit r = {0, 0, 1, 0, 0};
+  for (int v0 = 0; v0 < U; v0 += 32) {
+    const int v = v0 + lane;
+    const long long tv = uniform ? (v < U ? 1 : 0) : tok(v);
+    long long incl = tv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    const long long Sv = S + incl - tv;
+    const long long cb = v + extra * Sv / Tt, cbn = v + 1 + extra * (Sv + tv) / Tt;
+    const unsigned hit = __ballot_sync(0xffffffffu, v < U && cb <= cta && cta < cbn);
+    if (hit) {
+      const int l = __ffs(hit) - 1;
+      const int cbl = (int)__shfl_sync(0xffffffffu, cb, l);
+      r.u = v0 + l;
+      r.j = cta - cbl;
+      r.n = (int)__shfl_sync(0xffffffffu, cbn, l) - cbl;
+      const long long Tu = uniform ? 0 : __shfl_sync(0xffffffffu, tv, l);
+      r.lo = (int)(Tu * r.j / r.n);
+      r.hi = (int)(Tu * (r.j + 1) / r.n);
+      break;
+    }
+    S += __shfl_sync(0xffffffffu, incl, 31);
   }
-  const int U = a.units, base = P / U, rem = P % U;
-  if (cta < rem * (base + 1)) return {cta / (base + 1), cta % (base + 1), base + 1};
-  const int c2 = cta - rem * (base + 1);
-  return {rem + c2 / base, c2 % base, base};
+  return r;
 }
 
 template <int G, bool DENSE>
@@ -120,6 +161,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   __shared__ int s_merge;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) tl_mark(a.tlog, 4, 0, blockIdx.x == 0);
   // zero the stage buffers once: never-written slots must hold finite values (0 * NaN)
   for (int i = threadIdx.x; i < ATT_STAGES * ATT_STAGE_BYTES / 16; i += ATT_THREADS)
     reinterpret_cast<uint4*>(stages)[i] = make_uint4(0, 0, 0, 0);
@@ -149,50 +191,60 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     }
   };
   if (threadIdx.x == 0) stamp(0);
+  if (threadIdx.x == 0) tl_mark(a.tlog, 4, 1, blockIdx.x == 0);
   if (a.tlog && threadIdx.x == 0 && 2 * cta + 1 < 512) {  // per-CTA start / end (debug)
     unsigned long long t_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
     a.tlog[512 + 2 * cta] = t_;
   }
   int ntile_dbg = 0;
-  const long long T = DENSE ? dense_total : a.unit_prefix[a.units];
-
-  // unit-aligned split: CTA cta works on one unit only (see UnitSplit)
-  UnitSplit us_ = {0, 0, 0};
-  const bool unit_mode = a.unit_split != 0 || a.cta_map != nullptr;
-  if (unit_mode) us_ = unit_split_of(a, cta, P);
+  // unit-aligned split: CTA cta works on one unit only (see UnitSplit); otherwise the
+  // global token range split (needs unit_prefix)
+  const bool unit_mode = a.unit_split != 0;
+  UnitSplit us_ = {0, 0, 1, 0, 0};
+  if (unit_mode) us_ = unit_split_of<DENSE>(a, cta, P);
+  const long long T = unit_mode ? 0 : (DENSE ? dense_total : a.unit_prefix[a.units]);
 
   if (warp == 0) {
     // ============================ producer (warp-uniform control flow) ============================
     const bool leader = lane == 0;
-    long long t = range_start(cta, T, P);
-    long long t_end = range_start(cta + 1, T, P);
+    long long t = unit_mode ? 0 : range_start(cta, T, P);
+    const long long t_end = unit_mode ? 0 : range_start(cta + 1, T, P);
     int stage = 0;
     uint32_t phase = 0;
-    int u = 0;
-    if (unit_mode) {
-      u = us_.u;
-      if (us_.n > 0) {
-        const long long ub = DENSE || a.cta_map == nullptr ? (long long)u * a.n : a.unit_prefix[u];
-        const long long tu = (DENSE || a.cta_map == nullptr ? (long long)a.n : a.unit_prefix[u + 1] - ub);
-        t = ub + tu * us_.j / us_.n;
-        t_end = ub + tu * (us_.j + 1) / us_.n;
-      } else {
-        t = t_end = 0;
-      }
-    } else if (t < t_end) {
+    int u = us_.u;
+    if (!unit_mode && t < t_end) {
       if (DENSE) {
         u = (int)(t / a.n);
       } else {  // largest u with unit_prefix[u] <= t
         u = warp_floor_search<long long>(a.unit_prefix, a.units, t);
       }
     }
-    while (t < t_end) {
-      const long long ubase = DENSE ? (long long)u * a.n : a.unit_prefix[u];
-      const long long uend = DENSE ? ubase + a.n : a.unit_prefix[u + 1];
-      const long long pend = uend < t_end ? uend : t_end;
-      int lt = (int)(t - ubase);
-      const int le = (int)(pend - ubase);
+    bool more = unit_mode || t < t_end;
+    while (more) {
+      long long pend = 0;
+      int lt, le;
+      if (unit_mode) {
+        lt = us_.lo;
+        le = us_.hi;
+      } else {
+        const long long ubase = DENSE ? (long long)u * a.n : a.unit_prefix[u];
+        const long long uend = DENSE ? ubase + a.n : a.unit_prefix[u + 1];
+        pend = uend < t_end ? uend : t_end;
+        lt = (int)(t - ubase);
+        le = (int)(pend - ubase);
+      }
+      if (lt >= le) {  // empty piece (unit mode, T_v < n_v): a partial with no tokens
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (leader) {
+          meta[stage].mask = 0;
+          meta[stage].unit = u;
+          meta[stage].flags = FLAG_FIRST | FLAG_LAST;
+          mbar_arrive(&full[stage]);
+        }
+        if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
+        break;
+      }
       // sparse: run table window of 32 segments (lane i holds segment k0 + i)
       const int* seg_row = a.seg_row + (size_t)u * a.C;
       const int* seg_pref = a.seg_prefix + (size_t)u * (a.C + 1);
@@ -280,8 +332,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         ++ntile_dbg;
         if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
       }
+      if (unit_mode) break;
       t = pend;
       ++u;
+      more = t < t_end;
     }
     // end marker
     mbar_wait(&empty[stage], phase ^ 1);
@@ -429,18 +483,21 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           lf += sww[8 * 128 + 8 + g] * e;
           of += sww[g * 128 + ct] * e;
         }
-        a.part_o[(slot * G + g) * 128 + ct] = of / lf;
-        if (ct == 0) a.part_lse[slot * G + g] = (mf + log2f(lf)) * 0.6931471805599453f;
+        const bool none = mf == -INFINITY;  // empty piece: zero weight in the merge
+        a.part_o[(slot * G + g) * 128 + ct] = none ? 0.f : of / lf;
+        if (ct == 0) a.part_lse[slot * G + g] = none ? -INFINITY : (mf + log2f(lf)) * 0.6931471805599453f;
       }
       // ---- arrival: is this the unit's last piece?  The barrier orders every consumer
       // thread's partial stores before thread 0's gpu-scope fence and atomic (fences are
       // cumulative), and the merging CTA fences again before reading the others' partials.
       asm volatile("bar.sync 1, %0;" ::"n"(ATT_CWARPS * 32));
-      const long long us = DENSE ? (long long)u * a.n : a.unit_prefix[u];
-      const long long ue = DENSE ? us + a.n : a.unit_prefix[u + 1];
-      int c0 = 0;
-      const int np = unit_mode ? us_.n : pieces_of_unit(us, ue, T, P, &c0);
-      if (unit_mode) c0 = cta - us_.j;
+      long long ue = 0;
+      int c0 = cta - us_.j, np = us_.n;
+      if (!unit_mode) {
+        const long long us = DENSE ? (long long)u * a.n : a.unit_prefix[u];
+        ue = DENSE ? us + a.n : a.unit_prefix[u + 1];
+        np = pieces_of_unit(us, ue, T, P, &c0);
+      }
       if (ct == 0) {
         __threadfence();
         const int prev = atomicAdd(&a.unit_cnt[u], 1);
@@ -484,7 +541,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
             sum *= sc;
             mx = nm;
-            const float wl = live ? __expf(l - mx) : 0.f;
+            const float wl = (live && l > -INFINITY) ? __expf(l - mx) : 0.f;
             sum += warp_sum(wl);
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
@@ -544,6 +601,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     a.tlog[512 + 2 * cta + 1] = t_;
     a.tlog[816 + cta] = (unsigned long long)ntile_dbg;
   }
+  if (ct == 0) tl_mark(a.tlog, 4, 2, cta == 0);
   pdl_launch_dependents();
 }
 

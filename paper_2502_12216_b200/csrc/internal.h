@@ -24,9 +24,30 @@ SampleConsts sample_consts(int n);
 // programmatic dependent launch between the decode kernels (TACTIC_NO_PDL=1 disables)
 bool pdl_enabled();
 
-// Unit-aligned attention split applies when every unit can get >= 2 CTAs (and the
-// selection kernel can apportion them in one CTA: units <= 128).
-inline bool unit_split_ok(int units, int ctas) { return units <= 128 && 2 * units <= ctas; }
+// Unit-aligned attention split applies when every unit can get >= 2 CTAs; otherwise the
+// attention kernel cuts the global token list (and the fit kernel computes unit_prefix).
+inline bool unit_split_ok(int units, int ctas) { return 2 * units <= ctas; }
+
+// debug timestamps (TACTIC_TLOG=1): per-kernel-specific slots below 1536, then a
+// timeline of the decode kernels at TL_BASE + 4k: first CTA start, first CTA past
+// griddepcontrol.wait, last CTA end (atomicMax); k = 0 score, 1 rank, 2 sample, 3 fit,
+// 4 attention
+constexpr int TL_BASE = 1536;
+inline size_t tlog_entries(int units) { return (size_t)(units * 128 > 2048 ? units * 128 : 2048); }
+#ifdef __CUDACC__
+// what: 0 start, 1 past the wait (first CTA only), 2 end (every CTA; the max survives).
+// Called by one thread per CTA.
+__device__ __forceinline__ void tl_mark(unsigned long long* tl, int k, int what, bool first_cta) {
+  if (!tl) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (what < 2) {
+    if (first_cta) tl[TL_BASE + 4 * k + what] = t;
+  } else {
+    atomicMax(&tl[TL_BASE + 4 * k + 2], t);
+  }
+}
+#endif
 
 // Token-range split of a global work list over P CTAs: CTA c owns [rs(c), rs(c+1)).
 __host__ __device__ inline long long range_start(int c, long long T, int P) {
@@ -55,8 +76,6 @@ struct tactic_index_s {
   int* iters_run = nullptr;      // [units]
   int* all_list = nullptr;       // [units][C]  rows of non-empty clusters (p >= 1 work list)
   int* unit_cnt = nullptr;       // [units] attention arrival counters
-  int4* cta_map = nullptr;       // [num_ctas] unit-aligned attention split (written by the fit kernel)
-  bool map_ready = false;        // the last selection wrote cta_map
   int* all_prefix = nullptr;     // [units][C+1]
   long long* all_unit_prefix = nullptr;  // [units+1]
   // decode workspace
@@ -105,8 +124,7 @@ struct AttnArgs {
   float* out_f32;                  // nullable
   float* lse;                      // nullable [units][G]
   unsigned long long* tlog;        // nullable debug timestamps (CTA 0)
-  const int4* cta_map;             // nullable [num_ctas]: (unit, index in unit, CTAs of unit) from the selection
-  int unit_split;                  // 1: equal unit-aligned split (units <= CTAs/2, equal unit sizes)
+  int unit_split;                  // 1: unit-aligned split from seg_prefix totals (units <= CTAs/2)
 };
 cudaError_t launch_attention_sparse(const AttnArgs& a, int G, int num_ctas, cudaStream_t s, bool pdl);
 cudaError_t launch_attention_dense(const AttnArgs& a, const CUtensorMap* tmK, const CUtensorMap* tmV, int G,
@@ -127,7 +145,8 @@ struct SelArgs {
   double* local_max;               // stage 1
 };
 cudaError_t launch_score(const SelArgs& a, cudaStream_t s, bool pdl);
-cudaError_t launch_sort(const SelArgs& a, cudaStream_t s, bool pdl);
+// S1 + S2 + S3 (rank_cluster.cu): crit, order, ends, sampled-slot row map
+cudaError_t launch_score_rank(const __nv_bfloat16* q, tactic_index_s* x, cudaStream_t s, bool pdl);
 cudaError_t launch_sample(const SelArgs& a, cudaStream_t s, bool pdl);
 cudaError_t launch_select(const SelArgs& a, cudaStream_t s, bool pdl);
 cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl);

@@ -1,0 +1,321 @@
+// rank_cluster.cu -- S1 + S2 + S3 in one cluster-launched kernel (§4.3
+// P:366-376, App. B Alg. 1 l.1-4; readings 8-11 of DESIGN.md).
+//
+// One thread-block cluster of R CTAs per (head g, unit u); CTA c owns the M clusters
+// [cM, cM + M), one per thread (M = 128 for C <= 1024, else 256; R = ceil(C / M)):
+//   S1  crit_j = q_g . c_j in float64 (bf16 x fp32 products are exact in fp64; only the
+//       summation order differs from the oracle).  The CTA's centroid slice is index data,
+//       so it is bulk-copied (1-D TMA) into shared memory before the grid-dependency wait.
+//       A warp scores 32 centroids with a shuffle butterfly reduce-scatter.
+//   S2  local bitonic sort of the M keys (register shuffles for partners < 32 apart,
+//       double-buffered shared memory above).  Key = order-preserving bits of -crit with
+//       the low 12 bits replaced by the cluster id, so one 64-bit compare orders by
+//       (-crit, id) (reading 24: crits closer than 2^-40 relative rank by id).  The
+//       exclusive prefix of the sorted sizes is scanned, and the sorted run (keys, size
+//       prefix) is pushed into every CTA of the cluster (DSMEM stores), one cluster barrier.
+//       The global rank of a cluster is its local position plus its lower bound in the
+//       other R-1 runs; its end rank e_r is its own inclusive prefix plus the other runs'
+//       prefixes at those bounds -- no scatter and no second barrier.
+//   S3  every cluster writes order[r], ends[r] and the row-map entries of the sampled
+//       slots inside its token interval (e_r - size, e_r] (head ranks 1..N, windows
+//       x1 +- w, x2 +- w); a warp writes one interval at a time with coalesced stores.
+// Work per SM is what bounds this stage (it is latency and issue bound, not memory
+// bound): the cluster spreads one head's sort over R SMs instead of one.
+#include <cuda_bf16.h>
+#include <limits.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace tactic {
+
+struct SRParams {
+  const __nv_bfloat16* q;   // [units][G][128]
+  const float* cent;        // [units][C][128]
+  const int* offsets;       // [units][C+1]
+  int C, G, n;
+  SampleConsts sc;
+  double* crit;             // [units][G][C]
+  int* order;               // [units][G][C]
+  int* ends;                // [units][G][C]
+  int* rowmap;              // [units][G][slots]
+  unsigned long long* tlog;
+};
+
+__device__ __forceinline__ unsigned long long crit_key(double crit, int id) {
+  if (crit == 0.0) crit = 0.0;  // -0 == +0
+  const unsigned long long b = (unsigned long long)__double_as_longlong(-crit);
+  const unsigned long long k = (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // ascending = descending crit
+  return (k & ~0xFFFull) | (unsigned long long)id;
+}
+
+// one entry of a pushed run: sorted key and exclusive size prefix (entry M: ~0, total)
+struct __align__(16) RunEnt {
+  unsigned long long key;
+  unsigned long long pre;
+};
+
+template <int M, int R>
+constexpr size_t sr_smem() {
+  return (size_t)M * 512 + (size_t)R * (M + 1) * sizeof(RunEnt) + 2 * (size_t)M * 8 + 2 * (size_t)M * 4 + 64;
+}
+
+template <int M, int R>
+__global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
+  constexpr int NW = M / 32;
+  const int c = blockIdx.x, g = blockIdx.y, u = blockIdx.z;  // the cluster spans grid x (R CTAs)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int C = P.C;
+  extern __shared__ __align__(128) uint8_t sm[];
+  float* s_cent = (float*)sm;                                // [M][128]
+  RunEnt* runs = (RunEnt*)(s_cent + M * 128);                 // [R][M+1]
+  unsigned long long* bk = (unsigned long long*)(runs + R * (M + 1));  // [2][M]
+  int* s_size = (int*)(bk + 2 * M);                           // [M]
+  int* s_row = s_size + M;                                    // [M]
+  __shared__ uint64_t bar, rbar;
+  __shared__ int red[NW];
+  const bool tl_first = c == 0 && g == 0 && u == 0;
+  if (tid == 0) tl_mark(P.tlog, 1, 0, tl_first);
+  auto pstamp = [&](int i) {  // debug phase stamps of CTA (0, 0, 0) at tlog[1600 + i]
+    if (P.tlog && tl_first && tid == 0) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      P.tlog[1600 + i] = t_;
+    }
+  };
+
+  // ---- prologue on index data (before the dependency wait)
+  const int j = c * M + tid;
+  const bool valid = j < C;
+  const int nval = C - c * M < M ? (C - c * M > 0 ? C - c * M : 0) : M;  // clusters of this CTA
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&rbar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  cluster_arrive_relaxed();  // every CTA has started (and initialised rbar) before any st.async
+  if (tid == 0) {
+    const uint32_t bytes = (uint32_t)nval * 512u;
+    mbar_arrive_expect_tx(&bar, bytes);
+    const uint8_t* src = (const uint8_t*)(P.cent + ((size_t)u * C + (size_t)c * M) * 128);
+    for (uint32_t o = 0; o < bytes; o += 16384u) {
+      const uint32_t b = bytes - o < 16384u ? bytes - o : 16384u;
+      bulk_g2s((uint8_t*)s_cent + o, src + o, b, &bar);
+    }
+    mbar_arrive_expect_tx(&rbar, (uint32_t)(R * (M + 1) * sizeof(RunEnt)));
+  }
+  {
+    const int* off = P.offsets + (size_t)u * (C + 1);
+    const int o0 = valid ? off[j] : 0, o1 = valid ? off[j + 1] : 0;
+    s_size[tid] = o1 - o0;
+    s_row[tid] = o0;
+  }
+  pdl_wait();
+  if (tid == 0) tl_mark(P.tlog, 1, 1, tl_first);
+
+  // ---- S1: crit of the warp's 32 centroids (lane L ends up with centroid 32 w + L)
+  double qd[4];
+  {
+    const uint2 raw = *reinterpret_cast<const uint2*>(P.q + ((size_t)u * P.G + g) * 128 + lane * 4);
+    const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+    const float2 a = __bfloat1622float2(q2[0]), b = __bfloat1622float2(q2[1]);
+    qd[0] = a.x; qd[1] = a.y; qd[2] = b.x; qd[3] = b.y;
+  }
+  mbar_wait(&bar, 0);
+  pstamp(0);
+  double v[32];
+#pragma unroll
+  for (int jj = 0; jj < 32; ++jj) {
+    const int lc = warp * 32 + jj;
+    const float4 cv = lc < nval ? reinterpret_cast<const float4*>(s_cent + lc * 128)[lane]
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+    double s = qd[0] * (double)cv.x;
+    s = fma(qd[1], (double)cv.y, s);
+    s = fma(qd[2], (double)cv.z, s);
+    s = fma(qd[3], (double)cv.w, s);
+    v[jj] = s;
+  }
+#pragma unroll
+  for (int o = 16, half = 16; o >= 1; o >>= 1, half >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double send = upper ? v[i] : v[i + half];
+      const double keep = upper ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  const double crit = v[0];
+  pstamp(1);
+
+  // ---- S2: local bitonic sort (ascending packed keys = descending crit, then id)
+  unsigned long long x = valid ? crit_key(crit, j) : ~0ull;
+  int buf = 0;
+#pragma unroll
+  for (int k = 2; k <= M; k <<= 1) {
+#pragma unroll
+    for (int d = k >> 1; d > 0; d >>= 1) {
+      unsigned long long o;
+      if (d < 32) {
+        o = __shfl_xor_sync(0xffffffffu, x, d);
+      } else {
+        bk[buf * M + tid] = x;
+        __syncthreads();
+        o = bk[buf * M + (tid ^ d)];
+        buf ^= 1;
+      }
+      const bool take_min = ((tid & d) == 0) == ((tid & k) == 0);
+      x = take_min ? (o < x ? o : x) : (o > x ? o : x);
+    }
+  }
+  pstamp(2);
+  // exclusive prefix of the sorted sizes
+  const bool real = x != ~0ull;
+  const int id = real ? (int)(x & 0xFFFull) : 0;
+  const int size = real ? s_size[id - c * M] : 0;
+  int incl = size;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) red[warp] = incl;
+  __syncthreads();
+  int wbase = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const int t = red[w];
+    wbase += w < warp ? t : 0;
+    tot += t;
+  }
+  const int pre = wbase + incl - size;  // exclusive
+  // push the sorted run into every CTA of the cluster (st.async, completes on their rbar)
+  cluster_wait();
+#pragma unroll
+  for (int cc = 0; cc < R; ++cc) {
+    const uint32_t rb = dsmem_addr(&rbar, (uint32_t)cc);
+    st_async_v2u64(dsmem_addr(runs + c * (M + 1) + tid, (uint32_t)cc), x, (unsigned long long)pre, rb);
+    if (tid == M - 1) st_async_v2u64(dsmem_addr(runs + c * (M + 1) + M, (uint32_t)cc), ~0ull, (unsigned long long)tot, rb);
+  }
+  const size_t ug = (size_t)u * P.G + g;
+  if (valid) P.crit[ug * C + j] = crit;
+  pstamp(3);
+  mbar_wait(&rbar, 0);
+  pstamp(4);
+
+  // ---- global rank and end rank: lower bounds in all R runs (own run: the own position)
+  int r = 0, end = size;
+  {
+    int base[R];
+#pragma unroll
+    for (int cc = 0; cc < R; ++cc) base[cc] = 0;
+#pragma unroll
+    for (int len = M; len > 1;) {
+      const int half = len >> 1;
+#pragma unroll
+      for (int cc = 0; cc < R; ++cc)
+        base[cc] = runs[cc * (M + 1) + base[cc] + half - 1].key < x ? base[cc] + half : base[cc];
+      len -= half;
+    }
+#pragma unroll
+    for (int cc = 0; cc < R; ++cc) {
+      const int lb = base[cc] + (runs[cc * (M + 1) + base[cc]].key < x ? 1 : 0);
+      r += lb;
+      end += (int)runs[cc * (M + 1) + lb].pre;
+    }
+  }
+  pstamp(5);
+  if (real) {
+    P.order[ug * C + r] = id;
+    P.ends[ug * C + r] = end;
+  }
+
+  // ---- S3: row-map entries of the sampled slots inside (end - size, end]
+  {
+    const SampleConsts sc = P.sc;
+    int* rm = P.rowmap + ug * sc.slots;
+    const int t_lo = end - size + 1, t_hi = end;  // 1-based token ranks of this cluster
+    const int row0 = real ? s_row[id - c * M] : 0;
+    const int W1 = 2 * sc.w + 1;
+    const int nseg = sc.fallback ? 1 : 3;
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+      int seg_lo, seg_hi, slot_base;
+      if (sc.fallback) { seg_lo = 1; seg_hi = P.n; slot_base = 0; }
+      else if (sgi == 0) { seg_lo = 1; seg_hi = sc.N; slot_base = 0; }
+      else if (sgi == 1) { seg_lo = sc.x1 - sc.w; seg_hi = sc.x1 + sc.w; slot_base = sc.N; }
+      else { seg_lo = sc.x2 - sc.w; seg_hi = sc.x2 + sc.w; slot_base = sc.N + W1; }
+      const int a = t_lo > seg_lo ? t_lo : seg_lo, b = t_hi < seg_hi ? t_hi : seg_hi;
+      const bool has = real && size > 0 && a <= b;
+      unsigned bal = __ballot_sync(0xffffffffu, has);
+      const int my_slot = slot_base + (a - seg_lo), my_cnt = b - a + 1, my_row = row0 + (a - t_lo);
+      while (bal) {
+        const int l = __ffs(bal) - 1;
+        bal &= bal - 1;
+        const int s0 = __shfl_sync(0xffffffffu, my_slot, l);
+        const int cnt = __shfl_sync(0xffffffffu, my_cnt, l);
+        const int rw = __shfl_sync(0xffffffffu, my_row, l);
+        for (int i = lane; i < cnt; i += 32) rm[s0 + i] = rw + i;
+      }
+    }
+  }
+  pstamp(6);
+  if (tid == 0) tl_mark(P.tlog, 1, 2, tl_first);
+  pdl_launch_dependents();
+}
+
+template <int M, int R>
+static cudaError_t launch_sr(const SRParams& P, int units, cudaStream_t s, bool pdl) {
+  constexpr size_t smem = sr_smem<M, R>();
+  static bool done = false;
+  if (!done) {
+    cudaError_t e = cudaFuncSetAttribute(score_rank_kernel<M, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (R > 8) {
+      e = cudaFuncSetAttribute(score_rank_kernel<M, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    done = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(R, P.G, units);
+  cfg.blockDim = dim3(M);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = R;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, score_rank_kernel<M, R>, P);
+}
+
+cudaError_t launch_score_rank(const __nv_bfloat16* q, tactic_index_s* x, cudaStream_t s, bool pdl) {
+  SRParams P = {};
+  P.q = q;
+  P.cent = x->cent;
+  P.offsets = x->offsets;
+  P.C = x->C;
+  P.G = x->G;
+  P.n = x->n;
+  P.sc = x->sc;
+  P.crit = x->crit;
+  P.order = x->order;
+  P.ends = x->ends;
+  P.rowmap = x->rowmap;
+  P.tlog = x->tlog;
+  // M clusters per CTA, R = pow2 >= ceil(C / M) CTAs per cluster (TACTIC_MAX_CLUSTERS = 4096)
+  const int C = x->C, U = x->units;
+  if (C <= 128) return launch_sr<128, 1>(P, U, s, pdl);
+  if (C <= 256) return launch_sr<128, 2>(P, U, s, pdl);
+  if (C <= 512) return launch_sr<128, 4>(P, U, s, pdl);
+  if (C <= 1024) return launch_sr<128, 8>(P, U, s, pdl);
+  if (C <= 2048) return launch_sr<256, 8>(P, U, s, pdl);
+  return launch_sr<256, 16>(P, U, s, pdl);
+}
+
+}  // namespace tactic

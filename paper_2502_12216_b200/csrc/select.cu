@@ -5,12 +5,9 @@
 //                     summation order differs from the oracle).  A warp scores 32/G
 //                     centroids for all G heads and reduce-scatters the 32 partial sums
 //                     with a shuffle butterfly (31 exchanges instead of 5 per value).
-//  rank_kernel    S2+S3 rank of every cluster in the order (-crit, id) and the token
-//                     rank where it starts, without a comparison sort: clusters are
-//                     bucketed by a monotone map of crit (1024 buckets), bucket counts /
-//                     token sums are scanned, and only clusters sharing a bucket are
-//                     compared.  Writes order (rank -> id), end ranks e_r, first layout
-//                     row of the r-th cluster.
+//  (S1 + S2 + S3 of the normal path run in rank_cluster.cu: one cluster kernel that
+//   scores, sorts and writes order / end ranks / the sampled-slot row map; score_kernel
+//   here serves the sharded stage 2, which needs crit only)
 //  sample_kernel  S4  exact logits q.k/sqrt(d) of the sampled ranks: the first N ranks
 //                     and two windows of 2w+1 ranks around x1, x2 (Alg. 1 l.4,
 //                     readings 8-11); 16 rows in flight per warp.
@@ -34,7 +31,6 @@ namespace tactic {
 
 constexpr int SEL_THREADS = 512;
 constexpr int RANK_THREADS = 512;
-constexpr int NBUCKET = 1024;
 
 // ------------------------------------------------------------------ helpers
 __device__ double harmonic(long long k) {
@@ -168,9 +164,12 @@ __device__ long long block_lower_bound(long long lo, long long hi, Pred pred, lo
 template <int G>
 __global__ void __launch_bounds__(256) score_kernel(const __nv_bfloat16* __restrict__ q,
                                                     const float* __restrict__ cent, int C,
-                                                    double* __restrict__ crit) {
+                                                    double* __restrict__ crit, unsigned long long* tlog) {
   constexpr int CPW = 32 / G;
+  const bool tl_first = blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
+  if (threadIdx.x == 0) tl_mark(tlog, 0, 0, tl_first);
   pdl_wait();
+  if (threadIdx.x == 0) tl_mark(tlog, 0, 1, tl_first);
   const int u = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double qd[G][4];
 #pragma unroll
@@ -212,6 +211,7 @@ __global__ void __launch_bounds__(256) score_kernel(const __nv_bfloat16* __restr
   }
   const int jj = lane / G, g = lane % G;
   if (j0 + jj < C) crit[((size_t)u * G + g) * C + j0 + jj] = v[0];
+  if (threadIdx.x == 0) tl_mark(tlog, 0, 2, tl_first);
   pdl_launch_dependents();
 }
 
@@ -222,117 +222,6 @@ __device__ __forceinline__ int slot_rank(int slot, const SampleConsts& sc) {
   if (slot < sc.N) return slot + 1;
   if (slot < sc.N + W1) return sc.x1 - sc.w + (slot - sc.N);
   return sc.x2 - sc.w + (slot - sc.N - W1);
-}
-
-// ------------------------------------------------------------------ S2 + S3 (bucket ranking)
-__global__ void __launch_bounds__(RANK_THREADS) rank_kernel(const double* __restrict__ crit,
-                                                            const int* __restrict__ offsets, int C, int G,
-                                                            int* __restrict__ order, int* __restrict__ ends,
-                                                            int* __restrict__ rowstart, SampleConsts sc,
-                                                            int* __restrict__ rowmap) {
-  extern __shared__ uint8_t sm[];
-  double* key = (double*)sm;                       // [C]
-  int* size = (int*)(key + C);                     // [C]
-  int* bkt = size + C;                             // [C]
-  int* members = bkt + C;                          // [C]
-  int* bcnt = members + C;                         // [NBUCKET]
-  int* btok = bcnt + NBUCKET;                      // [NBUCKET]
-  int* bpos = btok + NBUCKET;                      // [NBUCKET] count prefix
-  int* btp = bpos + NBUCKET;                       // [NBUCKET] token prefix
-  int* bcur = btp + NBUCKET;                       // [NBUCKET]
-  __shared__ double redd[32];
-  __shared__ int redi[32];
-  const int g = blockIdx.x, u = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
-  const double* cr = crit + ((size_t)u * G + g) * C;
-  const int* off = offsets + (size_t)u * (C + 1);
-  for (int j = tid; j < C; j += nt) size[j] = off[j + 1] - off[j];  // static: before the wait
-  pdl_wait();
-  double mn = INFINITY, mx = -INFINITY;
-  for (int j = tid; j < C; j += nt) {
-    double x = cr[j];
-    if (x == 0.0) x = 0.0;  // -0 == +0
-    key[j] = x;
-    mn = fmin(mn, x);
-    mx = fmax(mx, x);
-  }
-  for (int b = tid; b < NBUCKET; b += nt) { bcnt[b] = 0; btok[b] = 0; bcur[b] = 0; }
-  mn = block_reduce<double, RED_MIN>(mn, redd);
-  mx = block_reduce<double, RED_MAX>(mx, redd);
-  // monotone bucket map: higher crit -> lower-or-equal bucket (fl(), floor and min are
-  // monotone), so a strict crit order never contradicts the bucket order.
-  const double scale = mx > mn ? (double)NBUCKET / (mx - mn) : 0.0;
-  for (int j = tid; j < C; j += nt) {
-    int b = (int)((mx - key[j]) * scale);
-    b = b < NBUCKET - 1 ? b : NBUCKET - 1;
-    bkt[j] = b;
-    atomicAdd(&bcnt[b], 1);
-    atomicAdd(&btok[b], size[j]);
-  }
-  __syncthreads();
-  {
-    constexpr int PER = NBUCKET / RANK_THREADS;
-    int lc = 0, lt = 0;
-#pragma unroll
-    for (int i = 0; i < PER; ++i) { lc += bcnt[tid * PER + i]; lt += btok[tid * PER + i]; }
-    int cb = block_exclusive_scan<int>(lc, redi, (int*)nullptr);
-    int tb = block_exclusive_scan<int>(lt, redi, (int*)nullptr);
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      bpos[tid * PER + i] = cb;
-      btp[tid * PER + i] = tb;
-      cb += bcnt[tid * PER + i];
-      tb += btok[tid * PER + i];
-    }
-  }
-  __syncthreads();
-  for (int j = tid; j < C; j += nt) members[bpos[bkt[j]] + atomicAdd(&bcur[bkt[j]], 1)] = j;
-  __syncthreads();
-  int* ord = order + ((size_t)u * G + g) * C;
-  int* en = ends + ((size_t)u * G + g) * C;
-  int* rs = rowstart + ((size_t)u * G + g) * C;
-  int* e_s = bcur + NBUCKET;   // [C] end ranks by rank position
-  int* r_s = e_s + C;          // [C] first layout row by rank position
-  for (int j = tid; j < C; j += nt) {
-    const int b = bkt[j];
-    const double kj = key[j];
-    int r = bpos[b], s = btp[b];
-    const int e = bpos[b] + bcnt[b];
-    for (int m = bpos[b]; m < e; ++m) {
-      const int i = members[m];
-      const double ki = key[i];
-      if (ki > kj || (ki == kj && i < j)) {
-        ++r;
-        s += size[i];
-      }
-    }
-    ord[r] = j;
-    en[r] = s + size[j];
-    rs[r] = off[j];
-    e_s[r] = s + size[j];
-    r_s[r] = off[j];
-  }
-  __syncthreads();
-  // S3: layout row of every sampled slot.  Slot ranks increase with the slot, so a thread
-  // binary-searches once per contiguous run of its slots and then walks forward.
-  int* rm = rowmap + ((size_t)u * G + g) * sc.slots;
-  const int per = (sc.slots + nt - 1) / nt;
-  int r = 0, prev_rank = -1;
-  for (int slot = tid * per; slot < (tid + 1) * per && slot < sc.slots; ++slot) {
-    const int rank = slot_rank(slot, sc);
-    if (rank != prev_rank + 1 || prev_rank < 0) {
-      int lo = 0, hi = C - 1;  // smallest r with e_s[r] >= rank
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (e_s[mid] >= rank) hi = mid; else lo = mid + 1;
-      }
-      r = lo;
-    } else {
-      while (e_s[r] < rank) ++r;
-    }
-    prev_rank = rank;
-    rm[slot] = r_s[r] + (rank - 1 - (r ? e_s[r - 1] : 0));
-  }
-  pdl_launch_dependents();
 }
 
 // ------------------------------------------------------------------ S4 (sampled logits)
@@ -348,7 +237,8 @@ constexpr int SB = 128;
 __global__ void __launch_bounds__(SB) sample_kernel(const __nv_bfloat16* __restrict__ q,
                                                     const __nv_bfloat16* __restrict__ Kp,
                                                     const int* __restrict__ rowmap, int n, int G, SampleConsts sc,
-                                                    float* __restrict__ logits, double* __restrict__ summ, int nb) {
+                                                    float* __restrict__ logits, double* __restrict__ summ, int nb,
+                                                    unsigned long long* tlog) {
   __shared__ __align__(128) uint8_t rows_s[SB * 256];
   __shared__ float lg_s[SB];
   __shared__ uint64_t bar;
@@ -357,12 +247,15 @@ __global__ void __launch_bounds__(SB) sample_kernel(const __nv_bfloat16* __restr
   const int g = blockIdx.y, u = blockIdx.z;
   const size_t ug = (size_t)u * G + g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool tl_first = blockIdx.x == 0 && g == 0 && u == 0;
   if (tid == 0) {
+    tl_mark(tlog, 2, 0, tl_first);
     mbar_init(&bar, SB);
     fence_barrier_init();
   }
   __syncthreads();
   pdl_wait();
+  if (tid == 0) tl_mark(tlog, 2, 1, tl_first);
   const int slot = blockIdx.x * SB + tid;
   const bool valid = slot < sc.slots;
   const int row = valid ? rowmap[ug * sc.slots + slot] : -1;
@@ -435,6 +328,7 @@ __global__ void __launch_bounds__(SB) sample_kernel(const __nv_bfloat16* __restr
     for (int w = 0; w < SB / 32; ++w) { a0 += redd[w][0]; a1 += redd[w][1]; a2 += redd[w][2]; }
     double* o = summ + (ug * nb + blockIdx.x) * 4;
     o[0] = (double)mb; o[1] = a0; o[2] = a1; o[3] = a2;
+    tl_mark(tlog, 2, 2, tl_first);
   }
   pdl_launch_dependents();
 }
@@ -459,8 +353,7 @@ struct FitParams {
   unsigned int* head_cnt;
   unsigned int* unit_cnt;
   unsigned long long* tlog;  // nullable debug stamps
-  int4* cta_map;             // nullable [num_ctas] unit-aligned attention split (units <= CTAs/2)
-  int num_ctas;
+  int need_unit_prefix;      // global attention split (units > CTAs/2): compute unit_prefix
 };
 
 constexpr int FIT_THREADS = 256;
@@ -715,11 +608,67 @@ __device__ double tail_mass1(double a, double b, long long N, long long k) {
   return a * harmonic_diff(k, lo - 1) + b * (double)(k - lo + 1);
 }
 
-__global__ void __launch_bounds__(256) fit_unit_kernel(const FitParams P) {
+// The positive terms of a/i + b over i in (N, n] form one interval [lo, hi] (a/i + b is
+// monotone in i), found once per head; tail(k) = tail_mass1(a, b, N, k) for every k <= n
+// then costs one harmonic_diff.
+struct TailFn {
+  double a, b;
+  long long lo, hi;  // empty when lo > hi
+  __device__ double operator()(long long k) const {
+    const long long kk = k < hi ? k : hi;
+    if (kk < lo) return 0.0;
+    return a * harmonic_diff(kk, lo - 1) + b * (double)(kk - lo + 1);
+  }
+};
+__device__ TailFn make_tail(double a, double b, long long N, long long n) {
+  TailFn f = {a, b, N + 1, n};
+  if (a >= 0.0 && b >= 0.0) return f;
+  if (a <= 0.0 && b <= 0.0) { f.lo = n + 1; return f; }
+  if (a > 0.0) {  // decreasing: positive for i <= top
+    const double t = a / (-b);
+    long long top = t >= 9.0e15 ? n : (long long)floor(t);
+    if (top > n) top = n;
+    while (top < n && a / (double)(top + 1) + b > 0.0) ++top;
+    while (top > N && !(a / (double)top + b > 0.0)) --top;
+    f.hi = top;  // top <= N: empty
+    return f;
+  }
+  const double t = (-a) / b;  // increasing: positive for i >= lo
+  long long lo = t >= 9.0e15 ? n + 1 : (long long)floor(t) + 1;
+  if (lo < N + 1) lo = N + 1;
+  while (lo > N + 1 && a / (double)(lo - 1) + b > 0.0) --lo;
+  while (lo <= n && !(a / (double)lo + b > 0.0)) ++lo;
+  f.lo = lo;
+  return f;
+}
+
+// Warp-cooperative count of entries < key in a non-decreasing int array (all lanes call):
+// 32 probes per round, 2 rounds for 1024 entries.
+__device__ __forceinline__ int warp_count_less(const int* arr, int len, long long key) {
+  const int lane = threadIdx.x & 31;
+  int lo = 0, hi = len;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const int step = (hi - lo + 31) >> 5;
+    const int idx = lo + lane * step;
+    const unsigned bal = __ballot_sync(0xffffffffu, idx < hi && (long long)arr[idx] < key);
+    const int c = __popc(bal);
+    const int nlo = c > 0 ? lo + (c - 1) * step + 1 : lo;
+    const int nhi = lo + c * step < hi ? lo + c * step : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  const int idx = lo + lane;
+  return lo + __popc(__ballot_sync(0xffffffffu, idx < hi && (long long)arr[idx] < key));
+}
+
+constexpr int FITU_THREADS = 512;
+
+__global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams P) {
   extern __shared__ __align__(16) uint8_t fsm[];
   __shared__ int redi[8];
   __shared__ int s_totc, s_tott;
   __shared__ bool s_last;
+  __shared__ int s_J[64];
   const int u = blockIdx.x, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int C = P.C, n = P.n, nb = P.nb, G = P.G;
   const SampleConsts sc = P.sc;
@@ -737,6 +686,7 @@ __global__ void __launch_bounds__(256) fit_unit_kernel(const FitParams P) {
     }
   };
   stamp(0);
+  if (tid == 0) tl_mark(P.tlog, 3, 0, u == 0);
   for (int i = tid; i <= C; i += nt) s_off[i] = P.offsets[(size_t)u * (C + 1) + i];
   for (int i = tid; i < C; i += nt) mask[i] = 0;
   __shared__ uint64_t sbar;
@@ -749,6 +699,7 @@ __global__ void __launch_bounds__(256) fit_unit_kernel(const FitParams P) {
   __syncthreads();
   pdl_wait();
   stamp(1);
+  if (tid == 0) tl_mark(P.tlog, 3, 1, u == 0);
   // stage the previous kernels' outputs with 1-D bulk copies (one round trip)
   if (tid == 0) {
     const uint32_t bs = (uint32_t)G * nb * 32, be = bulk_ok ? (uint32_t)G * C * 4 : 0u;
@@ -783,6 +734,7 @@ __global__ void __launch_bounds__(256) fit_unit_kernel(const FitParams P) {
     }
     const double EN = warp_sum_d(eh);
     double a = 0.0, b = 0.0, mu1 = 0.0, mu2 = 0.0, W = EN;
+    TailFn tail = {0.0, 0.0, 1, 0};
     if (!sc.fallback) {
       const int W1 = 2 * sc.w + 1;
       mu1 = warp_sum_d(e1) / (double)W1;
@@ -790,7 +742,8 @@ __global__ void __launch_bounds__(256) fit_unit_kernel(const FitParams P) {
       const double x1 = (double)sc.x1, x2 = (double)sc.x2;
       a = (mu1 - mu2) * x1 * x2 / (x2 - x1);  // O8 / Alg. 1 l.4
       b = mu1 - a / x1;
-      W = EN + tail_mass1(a, b, sc.N, n);
+      tail = make_tail(a, b, sc.N, n);
+      W = EN + tail(n);
     }
     long long kstar = (long long)n + 1;  // p >= 1: every rank (reading 15)
     if (P.p < 1.0) {
@@ -852,7 +805,7 @@ __global__ void __launch_bounds__(256) fit_unit_kernel(const FitParams P) {
         while (lo < hi) {
           const long long step = (hi - lo + 32) / 32;  // ceil((hi-lo+1)/32)
           const long long k = lo + (long long)lane * step;
-          const bool ok = k <= hi && EN + tail_mass1(a, b, sc.N, k) >= target;
+          const bool ok = k <= hi && EN + tail(k) >= target;
           const unsigned bal = __ballot_sync(0xffffffffu, ok);
           const int h = bal ? __ffs(bal) - 1 : 32;
           const long long nhi = h < 32 ? lo + (long long)h * step : hi;
@@ -865,78 +818,77 @@ __global__ void __launch_bounds__(256) fit_unit_kernel(const FitParams P) {
       }
     }
     // J = #{r : s_r < k*} = 1 + #{r < C-1 : e_r < k*}; mark the selected non-empty clusters
-    const int* en = s_end + (size_t)g * C;
-    const int* ord = s_ord + (size_t)g * C;
-    int cnt = 0;
-    for (int r = lane; r < C - 1; r += 32) cnt += en[r] < kstar;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    const int J = 1 + cnt;
-    for (int r = lane; r < J; r += 32) {
-      const int cid = ord[r];
-      if (s_off[cid + 1] > s_off[cid]) mask[cid] = 1;
-    }
+    // (the ends are non-decreasing in rank: a 32-way search)
+    const int J = 1 + warp_count_less(s_end + (size_t)g * C, C - 1, kstar);
     if (lane == 0) {
+      s_J[g] = J;
       P.J[ub + g] = J;
       double* f = P.fit + (ub + g) * 6;
       f[0] = a; f[1] = b; f[2] = m; f[3] = W; f[4] = mu1; f[5] = mu2;
     }
   }
   __syncthreads();
+  // mark the selected non-empty clusters of every head (all threads)
+  for (int g = 0; g < G; ++g) {
+    const int* ord = s_ord + (size_t)g * C;
+    for (int r = tid; r < s_J[g]; r += nt) {
+      const int cid = ord[r];
+      if (s_off[cid + 1] > s_off[cid]) mask[cid] = 1;
+    }
+  }
+  __syncthreads();
   stamp(3);
-  // ---- S7: compact the union (cluster-id order) into the work list.  Warp w owns a
-  // contiguous cluster range; positions come from ballots and warp scans (no block scans).
+  // ---- S7: compact the union (cluster-id order) into the work list.  Thread t owns a
+  // contiguous cluster chunk; one packed (tokens << 20 | clusters) block scan places it.
   {
-    __shared__ int w_cnt[8], w_tok[8];
-    const int nw = nt / 32;
-    const int CW = ((C + nw - 1) / nw + 31) & ~31;
-    const int jlo = warp * CW, jhi = min(C, jlo + CW);
-    int wc = 0, wt = 0;
-    for (int j0 = jlo; j0 < jhi; j0 += 32) {
-      const int j = j0 + lane;
-      const bool mk = j < jhi && mask[j];
-      int sz = mk ? s_off[j + 1] - s_off[j] : 0;
-      wc += __popc(__ballot_sync(0xffffffffu, mk));
+    __shared__ unsigned long long w_sum[32];
+    const int nw = nt >> 5;
+    const int per = (C + nt - 1) / nt;
+    const int j0 = tid * per, j1 = min(C, j0 + per);
+    unsigned long long loc = 0;
+    for (int j = j0; j < j1; ++j)
+      if (mask[j]) loc += ((unsigned long long)(s_off[j + 1] - s_off[j]) << 20) | 1ull;
+    unsigned long long incl = loc;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, o);
-      wt += sz;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
     }
-    if (lane == 0) { w_cnt[warp] = wc; w_tok[warp] = wt; }
+    if (lane == 31) w_sum[warp] = incl;
     __syncthreads();
-    int cbase = 0, tbase = 0, ctot = 0, ttot = 0;
+    unsigned long long base = incl - loc, tot = 0;
     for (int w = 0; w < nw; ++w) {
-      if (w < warp) { cbase += w_cnt[w]; tbase += w_tok[w]; }
-      ctot += w_cnt[w];
-      ttot += w_tok[w];
+      const unsigned long long v = w_sum[w];
+      if (w < warp) base += v;
+      tot += v;
     }
+    int cb = (int)(base & 0xFFFFFull), tb = (int)(base >> 20);
     int* ul = P.ulist + (size_t)u * C;
     int* up = P.uprefix + (size_t)u * (C + 1);
     uint8_t* um = P.umask + (size_t)u * C;
-    for (int j0 = jlo; j0 < jhi; j0 += 32) {
-      const int j = j0 + lane;
-      const bool mk = j < jhi && mask[j];
-      const int sz = mk ? s_off[j + 1] - s_off[j] : 0;
-      if (j < jhi) um[j] = mk;
-      const unsigned bal = __ballot_sync(0xffffffffu, mk);
-      int incl = sz;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int x = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += x;
-      }
+    for (int j = j0; j < j1; ++j) {
+      const uint8_t mk = mask[j];
+      um[j] = mk;
       if (mk) {
-        const int pos = cbase + __popc(bal & ((1u << lane) - 1u));
-        ul[pos] = s_off[j];
-        up[pos] = tbase + incl - sz;
+        ul[cb] = s_off[j];
+        up[cb] = tb;
+        ++cb;
+        tb += s_off[j + 1] - s_off[j];
       }
-      cbase += __popc(bal);
-      tbase += __shfl_sync(0xffffffffu, incl, 31);
     }
     // entries past the union: total tokens (keeps the prefix monotone for searches)
+    const int ctot = (int)(tot & 0xFFFFFull), ttot = (int)(tot >> 20);
     for (int k = ctot + tid; k <= C; k += nt) {
       up[k] = ttot;
       if (k < C) ul[k] = 0;
     }
+  }
+  // the unit-aligned attention split reads only the per-unit totals (uprefix[u][C]); the
+  // global split needs unit_prefix, computed by the last CTA to finish
+  if (!P.need_unit_prefix) {
+    stamp(4);
+    if (tid == 0) tl_mark(P.tlog, 3, 2, u == 0);
+    return;
   }
   stamp(4);
   __syncthreads();
@@ -968,57 +920,13 @@ __global__ void __launch_bounds__(256) fit_unit_kernel(const FitParams P) {
       P.unit_prefix[units] = s_tot;
       *P.unit_cnt = 0u;
     }
-    if (P.cta_map) {
-      // unit-aligned attention split: every unit gets 1 CTA plus its largest-remainder share
-      // of the others in proportion to its union tokens (capped at its token count)
-      __shared__ int s_n[128], s_f[128], s_cb[129];
-      __shared__ float s_fr[128];
-      __shared__ int s_R;
-      const int Pc = P.num_ctas, extra = Pc - units;
-      const double Ttot = (double)s_tot;
-      long long Tv = 0;
-      if (tid < units) {
-        Tv = __ldcg(P.uprefix + (size_t)tid * (C + 1) + C);
-        const double qv = Ttot > 0 ? (double)extra * (double)Tv / Ttot : 0.0;
-        s_f[tid] = (int)floor(qv);
-        s_fr[tid] = (float)(qv - floor(qv));
-      }
-      __syncthreads();
-      if (tid == 0) {
-        int sf = 0;
-        for (int v = 0; v < units; ++v) sf += s_f[v];
-        s_R = extra - sf;
-      }
-      __syncthreads();
-      if (tid < units) {
-        int rank = 0;
-        for (int v = 0; v < units; ++v) rank += (s_fr[v] > s_fr[tid]) || (s_fr[v] == s_fr[tid] && v < tid);
-        const long long nv = 1 + s_f[tid] + (rank < s_R ? 1 : 0);
-        s_n[tid] = (int)(nv < Tv ? nv : (Tv > 0 ? Tv : 1));
-      }
-      __syncthreads();
-      if (tid == 0) {
-        int acc = 0;
-        for (int v = 0; v < units; ++v) { s_cb[v] = acc; acc += s_n[v]; }
-        s_cb[units] = acc;
-      }
-      __syncthreads();
-      for (int c = tid; c < Pc; c += nt) {
-        int4 m = make_int4(0, 0, 0, 0);
-        if (c < s_cb[units]) {
-          int v = 0;
-          while (s_cb[v + 1] <= c) ++v;
-          m = make_int4(v, c - s_cb[v], s_n[v], 0);
-        }
-        P.cta_map[c] = m;
-      }
-    }
     if (P.tlog && tid == 0) {
       unsigned long long t_;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
       P.tlog[256 + 6] = t_;
     }
   }
+  if (tid == 0) tl_mark(P.tlog, 3, 2, u == 0);
 }
 
 // ------------------------------------------------------------------ S4-S7
@@ -1297,10 +1205,10 @@ cudaError_t launch_score(const SelArgs& a, cudaStream_t s, bool pdl) {
   const int per_block = 8 * (32 / x->G);
   auto cfg = make_cfg(dim3((x->C + per_block - 1) / per_block, x->units), dim3(256), 0, s, pdl, attr);
   switch (x->G) {
-    case 1: return cudaLaunchKernelEx(&cfg, score_kernel<1>, a.q, (const float*)x->cent, x->C, x->crit);
-    case 2: return cudaLaunchKernelEx(&cfg, score_kernel<2>, a.q, (const float*)x->cent, x->C, x->crit);
-    case 4: return cudaLaunchKernelEx(&cfg, score_kernel<4>, a.q, (const float*)x->cent, x->C, x->crit);
-    case 8: return cudaLaunchKernelEx(&cfg, score_kernel<8>, a.q, (const float*)x->cent, x->C, x->crit);
+    case 1: return cudaLaunchKernelEx(&cfg, score_kernel<1>, a.q, (const float*)x->cent, x->C, x->crit, x->tlog);
+    case 2: return cudaLaunchKernelEx(&cfg, score_kernel<2>, a.q, (const float*)x->cent, x->C, x->crit, x->tlog);
+    case 4: return cudaLaunchKernelEx(&cfg, score_kernel<4>, a.q, (const float*)x->cent, x->C, x->crit, x->tlog);
+    case 8: return cudaLaunchKernelEx(&cfg, score_kernel<8>, a.q, (const float*)x->cent, x->C, x->crit, x->tlog);
   }
   return cudaErrorInvalidValue;
 }
@@ -1314,18 +1222,6 @@ static cudaError_t ensure_smem(const void* fn, size_t smem, size_t* done) {
   return cudaSuccess;
 }
 
-cudaError_t launch_sort(const SelArgs& a, cudaStream_t s, bool pdl) {
-  tactic_index_s* x = a.idx;
-  const size_t smem = (size_t)x->C * (8 + 4 * 5) + (size_t)NBUCKET * 4 * 5;
-  static size_t done = 0;
-  cudaError_t e = ensure_smem((const void*)rank_kernel, smem, &done);
-  if (e != cudaSuccess) return e;
-  cudaLaunchAttribute attr[1];
-  auto cfg = make_cfg(dim3(x->G, x->units), dim3(RANK_THREADS), smem, s, pdl, attr);
-  return cudaLaunchKernelEx(&cfg, rank_kernel, (const double*)x->crit, (const int*)x->offsets, x->C, x->G,
-                            x->order, x->ends, x->rowstart, x->sc, x->rowmap);
-}
-
 int sample_blocks(int slots) { return (slots + SB - 1) / SB; }
 
 cudaError_t launch_sample(const SelArgs& a, cudaStream_t s, bool pdl) {
@@ -1334,7 +1230,7 @@ cudaError_t launch_sample(const SelArgs& a, cudaStream_t s, bool pdl) {
   cudaLaunchAttribute attr[1];
   auto cfg = make_cfg(dim3(nb, x->G, x->units), dim3(SB), 0, s, pdl, attr);
   return cudaLaunchKernelEx(&cfg, sample_kernel, a.q, (const __nv_bfloat16*)x->Kp, (const int*)x->rowmap, x->n,
-                            x->G, x->sc, x->logits, x->summ, nb);
+                            x->G, x->sc, x->logits, x->summ, nb, x->tlog);
 }
 
 cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
@@ -1362,16 +1258,14 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
   P.head_cnt = x->head_cnt;
   P.unit_cnt = x->counter;
   P.tlog = x->tlog;
-  P.num_ctas = x->num_ctas;
-  P.cta_map = unit_split_ok(x->units, x->num_ctas) ? x->cta_map : nullptr;
+  P.need_unit_prefix = !unit_split_ok(x->units, x->num_ctas);
   cudaLaunchAttribute attr[1];
   const size_t smem =
       (size_t)x->G * P.nb * 32 + (size_t)(x->C + 4) * 4 + (size_t)2 * x->G * x->C * 4 + (size_t)x->C + 64;
   static size_t done = 0;
   cudaError_t e = ensure_smem((const void*)fit_unit_kernel, smem, &done);
   if (e != cudaSuccess) return e;
-  const int threads = x->G * 32 > 128 ? x->G * 32 : 128;
-  auto cfg = make_cfg(dim3(x->units), dim3(threads), smem, s, pdl, attr);
+  auto cfg = make_cfg(dim3(x->units), dim3(FITU_THREADS), smem, s, pdl, attr);
   return cudaLaunchKernelEx(&cfg, fit_unit_kernel, P);
 }
 

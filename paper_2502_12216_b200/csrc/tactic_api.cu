@@ -200,7 +200,6 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_
   x->summ = A.get<double>(U * G * (size_t)sample_blocks(x->sc.slots) * 4);
   x->mask_acc = A.get<uint8_t>(U * C);
   x->head_cnt = A.get<unsigned int>(U);
-  x->cta_map = A.get<int4>((size_t)x->num_ctas);
   if (A.err != cudaSuccess) {
     for (void* p : A.ptrs) cudaFree(p);
     delete x;
@@ -212,8 +211,8 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_
     const char* sel = getenv("TACTIC_SELECT");
     x->fused_R = (sel && strcmp(sel, "fused") == 0) ? choose_fused_R(x) : 0;
     const char* tl = getenv("TACTIC_TLOG");
-    if (tl && tl[0] == '1' && cudaMalloc((void**)&x->tlog, U * 16 * 8 * 8) == cudaSuccess) {
-      cudaMemset(x->tlog, 0, U * 16 * 8 * 8);
+    if (tl && tl[0] == '1' && cudaMalloc((void**)&x->tlog, tlog_entries(U) * 8) == cudaSuccess) {
+      cudaMemset(x->tlog, 0, tlog_entries(U) * 8);
       std::lock_guard<std::mutex> lk(g_mu);
       A.ptrs.push_back(x->tlog);
     }
@@ -415,7 +414,7 @@ void tactic_index_destroy(tactic_index_t idx) {
 tactic_status_t tactic_index_debug_timing(tactic_index_t idx, uint64_t* host, int32_t count) {
   if (!idx || !host) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
   if (!idx->tlog) return fail(TACTIC_ERR_UNSUPPORTED, "index created without TACTIC_TLOG=1");
-  const size_t n = (size_t)idx->units * 16 * 8;
+  const size_t n = tlog_entries(idx->units);
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(host, idx->tlog, (count < (int32_t)n ? (size_t)count : n) * 8, cudaMemcpyDeviceToHost));
   return TACTIC_OK;
@@ -480,16 +479,15 @@ static tactic_status_t run_selection(const void* q, tactic_index_t idx, double p
   sa.gmass = gmass;
   sa.local_max = local_max;
   const bool pdl = true;
-  // the fit kernel (mode 0, multi-kernel path) also writes the unit-aligned attention split
-  idx->map_ready = mode == 0 && idx->fused_R == 0 && unit_split_ok(idx->units, idx->num_ctas);
   if (mode == 0 && idx->fused_R > 0) {  // one cluster-launched kernel for S1-S7
     CK(launch_select_fused((const __nv_bfloat16*)q, idx, p, s, pdl));
     return TACTIC_OK;
   }
-  CK(launch_score(sa, s, pdl));      // S1
   if (mode != 1) {
-    CK(launch_sort(sa, s, pdl));     // S2, S3 (+ sampled-slot row map)
-    CK(launch_sample(sa, s, pdl));   // S4 (+ per-block fit summaries)
+    CK(launch_score_rank(sa.q, idx, s, pdl));  // S1, S2, S3 (+ sampled-slot row map)
+    CK(launch_sample(sa, s, pdl));             // S4 (+ per-block fit summaries)
+  } else {
+    CK(launch_score(sa, s, pdl));              // S1 only (sharded stage 2)
   }
   if (mode == 0) CK(launch_fit(sa, s, pdl));     // S5-S7
   else CK(launch_select(sa, s, pdl));            // sharded stage rules
@@ -516,11 +514,7 @@ static tactic_status_t run_attention(const void* q, tactic_index_t idx, bool all
   aa.out_f32 = out_f32;
   aa.lse = lse;
   aa.tlog = idx->tlog;
-  // unit-aligned split: p >= 1 lists have n tokens per unit (equal split); union lists use
-  // the proportional map the fit kernel wrote
-  if (all) aa.unit_split = unit_split_ok(idx->units, idx->num_ctas) &&
-                           (idx->num_ctas + idx->units - 1) / idx->units <= idx->n;
-  else if (idx->map_ready) aa.cta_map = idx->cta_map;
+  aa.unit_split = unit_split_ok(idx->units, idx->num_ctas);  // else the global split (unit_prefix)
   CK(launch_attention_sparse(aa, idx->G, idx->num_ctas, s, ev_mid == nullptr));  // S8 + fused S9
   if (ev_mid) CK(cudaEventRecord(ev_mid, s));
   return TACTIC_OK;
@@ -663,7 +657,7 @@ tactic_status_t tactic_dense_decode(const void* q, const void* K, const void* V,
   aa.unit_cnt = unit_cnt;
   aa.out = (__nv_bfloat16*)out;
   aa.lse = lse;
-  aa.unit_split = unit_split_ok((int)units, P) && (P + (int)units - 1) / (int)units <= r.n;
+  aa.unit_split = unit_split_ok((int)units, P);
   CK(launch_attention_dense(aa, &mk, &mv, r.G, P, s, true));  // S10 + fused merge
   return TACTIC_OK;
 }

@@ -179,8 +179,9 @@ class Index:
         return {f: getattr(i, f) for f, _ in IndexInfo._fields_}
 
     def debug_timing(self) -> np.ndarray:
-        """Phase timestamps (ns) of the fused selection kernel: [units][16 ranks][8 phases]."""
-        buf = np.zeros((self.units, 16, 8), dtype=np.uint64)
+        """Debug %globaltimer stamps (ns), flat: kernel-specific slots below 1536, the decode
+        timeline at 1536 + 4k (TACTIC_TLOG=1 indexes only; see csrc/internal.h)."""
+        buf = np.zeros(max(self.units * 128, 2048), dtype=np.uint64)
         _check(lib().tactic_index_debug_timing(self.handle, buf.ctypes.data, buf.size))
         return buf
 

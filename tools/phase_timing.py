@@ -10,6 +10,7 @@ import sys
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--select", default="multi")
+ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between calls")
 args = ap.parse_args()
 os.environ["TACTIC_TLOG"] = "1"
 os.environ["TACTIC_SELECT"] = args.select
@@ -33,15 +34,33 @@ R = idx.info()["select_cluster_size"]
 print("select cluster size R =", R)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 out = torch.empty_like(qd)
-for it in range(4):
-    flush.fill_(1)
-    torch.cuda.synchronize()
+T.decode(qd, idx, 0.9, out=out)
+torch.cuda.synchronize()
+graph = torch.cuda.CUDAGraph()  # replayed like bench.py (no host launch gaps)
+with torch.cuda.graph(graph):
     T.decode(qd, idx, 0.9, out=out)
+for it in range(4):
+    if not args.no_flush:
+        flush.fill_(1)
+    torch.cuda.synchronize()
+    graph.replay()
     torch.cuda.synchronize()
     full = idx.debug_timing().astype(np.int64).reshape(-1)
     if it < 2:
         continue
     print(f"--- iteration {it}")
+    tl = full[1536:1536 + 20].reshape(5, 4)
+    if (tl[:, 0] > 0).any():
+        z = tl[:, 0][tl[:, 0] > 0].min()
+        print("  timeline (us from first start: first-CTA start / past wait / last CTA end):")
+        for k, nm in enumerate(["score", "score+rank", "sample", "fit", "attention"]):
+            if tl[k, 0] > 0:
+                print(f"    {nm:9s} {(tl[k, 0] - z) / 1e3:7.2f} {(tl[k, 1] - z) / 1e3:7.2f} {(tl[k, 2] - z) / 1e3:7.2f}")
+        rk = full[1600:1607]
+        if rk[0] > 0:
+            names = ["centroids in", "scored", "sorted", "pushed", "runs in", "ranked", "rowmap"]
+            print("  rank CTA(0,0) phases (us after its wait): " +
+                  "  ".join(f"{nm} {(rk[i] - tl[1, 1]) / 1e3:.2f}" for i, nm in enumerate(names)))
     if R == 0:
         fs = full[256:256 + 7]
         t0 = fs[0]

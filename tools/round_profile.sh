@@ -1,0 +1,14 @@
+#!/bin/bash
+# One gpurun call: bench line, ncu launch list of the bench command, ncu --set full of the decode kernels.
+#   gpurun --timeout 2400 -- 'bash tools/round_profile.sh r01'
+R=${1:-r01}
+mkdir -p gpurun_out
+timeout 900 python bench.py > gpurun_out/bench_$R.json 2> gpurun_out/bench_$R.err
+tail -1 gpurun_out/bench_$R.json
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
+  --log-file gpurun_out/launches_$R.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/launches_$R.log 2>&1
+echo "launch list rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on \
+  -k regex:"attention_kernel|score_kernel|rank_kernel|sample_kernel|fit_unit_kernel" -s 5 -c 6 \
+  -o gpurun_out/full_$R -f python tools/profile_decode.py > gpurun_out/full_$R.log 2>&1
+echo "full capture rc=$?"
