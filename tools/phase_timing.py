@@ -67,6 +67,11 @@ for it in range(4):
         names = ["start", "pdl_wait", "staged", "heads fitted", "compacted", "last-unit start", "last-unit end"]
         print("  fit CTA u0: " + "  ".join(f"{nm} {(fs[i] - t0) / 1e3:6.2f}" for i, nm in enumerate(names)
                                              if fs[i] > 0))
+        hs = full[1700:1705]
+        if hs[0] > 0:
+            names = ["sums", "W", "k*", "J", "all heads"]
+            print("  fit warp 0 (us after staged): " + "  ".join(f"{nm} {(hs[i] - fs[2]) / 1e3:.2f}"
+                                                               for i, nm in enumerate(names)))
     else:
         t = full.reshape(-1, 16, 8)[:, :R, :]
         t0 = t[:, :, 0].min()

@@ -1,10 +1,10 @@
 """Short C2 driver for `ncu --set full` captures (one GPU, no CUDA graph).
 
     ncu --set full --clock-control none --import-source on \
-        -k regex:"attention_kernel|score_kernel|rank_kernel|sample_kernel|fit_unit_kernel" \
-        -s 5 -c 6 -o gpurun_out/full_r01 python tools/profile_decode.py
+        -k regex:"attention_kernel|score_rank|sample_kernel|fit_unit_kernel" \
+        -s 4 -c 5 -o gpurun_out/full_r01 python tools/profile_decode.py
 
-Launch order: decode #1 (5 launches, skipped by -s 5), decode #2 (score, rank, sample,
+Launch order: decode #1 (4 launches, skipped by -s 4), decode #2 (score_rank, sample,
 fit, sparse attention), dense decode (1 launch).  L2 is flushed before every call.
 """
 import os

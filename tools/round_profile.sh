@@ -9,6 +9,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --
   --log-file gpurun_out/launches_$R.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/launches_$R.log 2>&1
 echo "launch list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"attention_kernel|score_kernel|rank_kernel|sample_kernel|fit_unit_kernel" -s 5 -c 6 \
+  -k regex:"attention_kernel|score_rank|sample_kernel|fit_unit_kernel" -s 4 -c 5 \
   -o gpurun_out/full_$R -f python tools/profile_decode.py > gpurun_out/full_$R.log 2>&1
 echo "full capture rc=$?"
