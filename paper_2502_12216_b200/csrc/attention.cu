@@ -47,8 +47,11 @@ struct __align__(16) StageMeta {
 };
 
 constexpr int SCRATCH_FLOATS = ATT_CWARPS * (8 * 128 + 16);
+// unit-aligned split: the unit's work list (segment rows + token prefix) staged in smem
+constexpr int LIST_INTS = 2 * TACTIC_MAX_CLUSTERS + 4;
 constexpr size_t ATT_SMEM = (size_t)ATT_STAGES * ATT_STAGE_BYTES + ATT_STAGES * sizeof(StageMeta) +
-                            2 * ATT_STAGES * sizeof(uint64_t) + SCRATCH_FLOATS * sizeof(float) + 1024;
+                            3 * ATT_STAGES * sizeof(uint64_t) + SCRATCH_FLOATS * sizeof(float) +
+                            LIST_INTS * sizeof(int) + 1024;
 
 size_t attention_smem_bytes() { return ATT_SMEM; }
 
@@ -103,6 +106,16 @@ struct UnitSplit {
   int u, j, n;       // unit, index of this CTA within the unit, CTAs of the unit
   int lo, hi;        // token range within the unit's work list
 };
+// floor(x / y) for 0 <= x, 0 < y, quotient below 2^24: an fp32 reciprocal estimate fixed
+// up with exact 64-bit multiplies (a dependent 64-bit integer or fp64 division costs
+// hundreds of cycles on the single warp that computes the split)
+__device__ __forceinline__ long long floor_div(long long x, long long y) {
+  long long q = (long long)((float)x * __frcp_rn((float)y));
+  while (q > 0 && q * y > x) --q;
+  while ((q + 1) * y <= x) ++q;
+  return q;
+}
+
 template <bool DENSE>
 __device__ __forceinline__ UnitSplit unit_split_of(const AttnArgs& a, int cta, int P) {
   const int U = a.units, lane = threadIdx.x & 31;
@@ -129,7 +142,10 @@ __device__ __forceinline__ UnitSplit unit_split_of(const AttnArgs& a, int cta, i
       if (lane >= o) incl += x;
     }
     const long long Sv = S + incl - tv;
-    const long long cb = v + extra * Sv / Tt, cbn = v + 1 + extra * (Sv + tv) / Tt;
+    // cb_v = v + floor(extra S_v / T); cb_{v+1} from the next lane (S_{v+1} = S_v + t_v)
+    const long long cb = v + floor_div(extra * Sv, Tt);
+    long long cbn = __shfl_down_sync(0xffffffffu, cb, 1);
+    if (lane == 31) cbn = v + 1 + floor_div(extra * (Sv + tv), Tt);
     const unsigned hit = __ballot_sync(0xffffffffu, v < U && cb <= cta && cta < cbn);
     if (hit) {
       const int l = __ffs(hit) - 1;
@@ -138,13 +154,20 @@ __device__ __forceinline__ UnitSplit unit_split_of(const AttnArgs& a, int cta, i
       r.j = cta - cbl;
       r.n = (int)__shfl_sync(0xffffffffu, cbn, l) - cbl;
       const long long Tu = uniform ? 0 : __shfl_sync(0xffffffffu, tv, l);
-      r.lo = (int)(Tu * r.j / r.n);
-      r.hi = (int)(Tu * (r.j + 1) / r.n);
+      r.lo = (int)floor_div(Tu * r.j, r.n);
+      r.hi = (int)floor_div(Tu * (r.j + 1), r.n);
       break;
     }
     S += __shfl_sync(0xffffffffu, incl, 31);
   }
   return r;
+}
+
+// the unit-aligned split's merge stages the unit's contiguous partials in the idle stage
+// buffers (a CTA of that split holds one piece, so no copy is in flight at its end)
+template <int G>
+__device__ __forceinline__ bool smem_merge_ok(bool unit_mode, int np) {
+  return unit_mode && np * G * 4 + 16 <= 1024 && (size_t)np * G * 512 + 1024 <= (size_t)ATT_STAGES * ATT_STAGE_BYTES;
 }
 
 template <int G, bool DENSE>
@@ -157,7 +180,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   StageMeta* meta = (StageMeta*)(stages + ATT_STAGES * ATT_STAGE_BYTES);
   uint64_t* full = (uint64_t*)(meta + ATT_STAGES);
   uint64_t* empty = full + ATT_STAGES;
-  float* scratch = (float*)(empty + ATT_STAGES);
+  uint64_t* mbar = empty + ATT_STAGES;  // [0]: merge staging (unit-aligned split)
+  float* scratch = (float*)(empty + 2 * ATT_STAGES);
+  int* s_list = (int*)(scratch + SCRATCH_FLOATS);  // seg_row [C] | seg_prefix [C+1]
   __shared__ int s_merge;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -170,6 +195,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], ATT_CWARPS);
     }
+    mbar_init(mbar, 1);
     fence_barrier_init();
   }
   fence_proxy_async_smem();
@@ -203,7 +229,33 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   const bool unit_mode = a.unit_split != 0;
   UnitSplit us_ = {0, 0, 1, 0, 0};
   if (unit_mode) us_ = unit_split_of<DENSE>(a, cta, P);
+  if (threadIdx.x == 0) stamp(40);
   const long long T = unit_mode ? 0 : (DENSE ? dense_total : a.unit_prefix[a.units]);
+  // unit-aligned sparse split: the CTA's unit's whole work list into smem with one round
+  // trip of independent loads (all threads), so the producer's segment search and run
+  // walk never wait on L2
+  const bool list_smem = !DENSE && unit_mode;
+  if (list_smem) {
+    const int* gr = a.seg_row + (size_t)us_.u * a.C;
+    const int* gp = a.seg_prefix + (size_t)us_.u * (a.C + 1);
+    constexpr int PER = 16;  // independent loads in flight per thread (2 C + 1 <= 2560: one batch)
+    for (int i0 = 0; i0 < 2 * a.C + 1; i0 += PER * ATT_THREADS) {
+      int v[PER];
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int i = i0 + k * ATT_THREADS + threadIdx.x;
+        v[k] = i < a.C ? __ldcg(gr + i) : (i < 2 * a.C + 1 ? __ldcg(gp + (i - a.C)) : 0);
+      }
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int i = i0 + k * ATT_THREADS + threadIdx.x;
+        if (i < 2 * a.C + 1) s_list[i] = v[k];
+      }
+    }
+    if (threadIdx.x == 0) stamp(41);
+    __syncthreads();
+    if (threadIdx.x == 0) stamp(42);
+  }
 
   if (warp == 0) {
     // ============================ producer (warp-uniform control flow) ============================
@@ -246,16 +298,18 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         break;
       }
       // sparse: run table window of 32 segments (lane i holds segment k0 + i)
-      const int* seg_row = a.seg_row + (size_t)u * a.C;
-      const int* seg_pref = a.seg_prefix + (size_t)u * (a.C + 1);
+      const int* seg_row = list_smem ? s_list : a.seg_row + (size_t)u * a.C;
+      const int* seg_pref = list_smem ? s_list + a.C : a.seg_prefix + (size_t)u * (a.C + 1);
       int k = 0, k0 = 0, row = 0, left = 0, w_row = 0, w_end = 0;
       if (!DENSE) {
+        if (leader) stamp(43);
         k = k0 = warp_floor_search<int>(seg_pref, a.C, lt);  // largest k with seg_pref[k] <= lt
         w_row = (k0 + lane < a.C) ? seg_row[k0 + lane] : 0;
         w_end = (k0 + lane < a.C) ? seg_pref[k0 + lane + 1] : 0;
         const int sp = seg_pref[k];
         row = __shfl_sync(0xffffffffu, w_row, 0) + (lt - sp);
         left = __shfl_sync(0xffffffffu, w_end, 0) - lt;
+        if (leader) stamp(44);
       }
       bool first = true;
       while (lt < le) {
@@ -499,10 +553,19 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         np = pieces_of_unit(us, ue, T, P, &c0);
       }
       if (ct == 0) {
-        __threadfence();
-        const int prev = atomicAdd(&a.unit_cnt[u], 1);
+        const int prev = atom_add_acq_rel_gpu(&a.unit_cnt[u], 1);
         s_merge = (prev == np - 1);
-        if (s_merge) __threadfence();
+        if (s_merge && smem_merge_ok<G>(unit_mode, np)) {
+          // the unit's partials are contiguous slots [c0, c0 + np): one bulk copy of the
+          // o rows and one of the lse values into the (now idle) stage buffers
+          fence_proxy_async_global();
+          // (lse: from the 16-byte aligned slot at or below c0 G; the merge skips the head)
+          const int l0 = (c0 * G) & 3;
+          const uint32_t ob = (uint32_t)(np * G * 128 * 4), lb = (uint32_t)(((l0 + np * G) * 4 + 15) & ~15);
+          mbar_arrive_expect_tx(mbar, ob + lb);
+          bulk_g2s(stages + 1024, a.part_o + (size_t)c0 * G * 128, ob, mbar);
+          bulk_g2s(stages, a.part_lse + ((size_t)c0 * G - l0), lb, mbar);
+        }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(ATT_CWARPS * 32));
       if (s_merge && a.tlog && ct == 0 && u < 8) {  // debug: merge start
@@ -510,7 +573,47 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
         a.tlog[964 + 2 * u] = t_;
       }
-      if (s_merge) {
+      if (s_merge && smem_merge_ok<G>(unit_mode, np)) {
+        // ---- S9 (unit-aligned split): merge the staged pieces from shared memory
+        mbar_wait(mbar, 0);
+        const float* sl = reinterpret_cast<const float*>(stages) + ((c0 * G) & 3);
+        const float* so = reinterpret_cast<const float*>(stages + 1024);
+        for (int g = cw; g < G; g += ATT_CWARPS) {
+          float mx = -INFINITY;
+          for (int i = lane; i < np; i += 32) mx = fmaxf(mx, sl[i * G + g]);
+          mx = warp_max(mx);
+          float sum = 0.f;
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+          for (int i = 0; i < np; ++i) {
+            const float l = sl[i * G + g];
+            const float w = l > -INFINITY ? __expf(l - mx) : 0.f;
+            const float4 v = reinterpret_cast<const float4*>(so + ((size_t)i * G + g) * 128)[lane];
+            sum += w;
+            acc.x = fmaf(w, v.x, acc.x);
+            acc.y = fmaf(w, v.y, acc.y);
+            acc.z = fmaf(w, v.z, acc.z);
+            acc.w = fmaf(w, v.w, acc.w);
+          }
+          const float inv = 1.f / sum;
+          const size_t orow = ((size_t)u * G + g) * 128 + lane * 4;
+          if (a.out) {
+            __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(a.out + orow);
+            ob[0] = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+            ob[1] = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+          }
+          if (a.out_f32)
+            *reinterpret_cast<float4*>(a.out_f32 + orow) =
+                make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+          if (a.lse && lane == 0) a.lse[(size_t)u * G + g] = mx + logf(sum);
+        }
+        if (ct == 0) a.unit_cnt[u] = 0;  // self-reset for the next call
+        if (a.tlog && ct == 0 && u < 8) {
+          unsigned long long t_;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+          a.tlog[965 + 2 * u] = t_;
+        }
+      } else if (s_merge) {
         // ---- S9: merge this unit's pieces (slots c + u), LSE-weighted
         // warp w merges heads w, w+4, ...; lanes hold 4 dims; piece weights are computed
         // 32 at a time (one per lane) and broadcast, so the o loads are independent.

@@ -82,6 +82,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// gpu-scope acquire-release fetch-add: releases this thread's (and, cumulatively, its
+// barrier-ordered CTA peers') prior writes and acquires the other arrivers' writes
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
+  int r;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  return r;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // 1-D bulk copy global -> shared (TMA "non-tensor" path, SASS UBLKCP), completion
 // counted in bytes on `bar`.  src/dst 16-byte aligned, bytes a multiple of 16.
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {

@@ -84,7 +84,7 @@ struct tactic_index_s {
   int* ends = nullptr;           // [units][G][C]
   int* rowstart = nullptr;       // [units][G][C] first layout row of the r-th ranked cluster
   int* rowmap = nullptr;         // [units][G][slots] layout row of every sampled slot
-  double* summ = nullptr;        // [units][G][nb][4] per-sample-block fit summaries
+  float* summ = nullptr;         // [units][G][nb][4] per-sample-block fit summaries
   uint8_t* mask_acc = nullptr;   // [units][C] union accumulator (zero between calls)
   unsigned int* head_cnt = nullptr;  // [units] selection arrival counters
   float* logits = nullptr;       // [units][G][slots]

@@ -237,12 +237,12 @@ constexpr int SB = 128;
 __global__ void __launch_bounds__(SB) sample_kernel(const __nv_bfloat16* __restrict__ q,
                                                     const __nv_bfloat16* __restrict__ Kp,
                                                     const int* __restrict__ rowmap, int n, int G, SampleConsts sc,
-                                                    float* __restrict__ logits, double* __restrict__ summ, int nb,
+                                                    float* __restrict__ logits, float* __restrict__ summ, int nb,
                                                     unsigned long long* tlog) {
   __shared__ __align__(128) uint8_t rows_s[SB * 256];
   __shared__ float lg_s[SB];
   __shared__ uint64_t bar;
-  __shared__ double redd[SB / 32][3];
+  __shared__ float redd[SB / 32][3];
   __shared__ float redf[SB / 32];
   const int g = blockIdx.y, u = blockIdx.z;
   const size_t ug = (size_t)u * G + g;
@@ -311,23 +311,25 @@ __global__ void __launch_bounds__(SB) sample_kernel(const __nv_bfloat16* __restr
   float mb = redf[0];
 #pragma unroll
   for (int w = 1; w < SB / 32; ++w) mb = fmaxf(mb, redf[w]);
-  double e = valid ? exp((double)lg - (double)mb) : 0.0;
+  const float e = valid ? __expf(lg - mb) : 0.f;
   const int W1 = 2 * sc.w + 1;
-  double sh = 0.0, s1 = 0.0, s2 = 0.0;
+  float sh = 0.f, s1 = 0.f, s2 = 0.f;
   if (sc.fallback || slot < sc.N) sh = e;
   else if (slot < sc.N + W1) s1 = e;
   else s2 = e;
-  sh = warp_sum_d(sh);
-  s1 = warp_sum_d(s1);
-  s2 = warp_sum_d(s2);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sh += __shfl_xor_sync(0xffffffffu, sh, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
   if (lane == 0) { redd[warp][0] = sh; redd[warp][1] = s1; redd[warp][2] = s2; }
   __syncthreads();
   if (tid == 0) {
-    double a0 = 0, a1 = 0, a2 = 0;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f;
 #pragma unroll
     for (int w = 0; w < SB / 32; ++w) { a0 += redd[w][0]; a1 += redd[w][1]; a2 += redd[w][2]; }
-    double* o = summ + (ug * nb + blockIdx.x) * 4;
-    o[0] = (double)mb; o[1] = a0; o[2] = a1; o[3] = a2;
+    *reinterpret_cast<float4*>(summ + (ug * nb + blockIdx.x) * 4) = make_float4(mb, a0, a1, a2);
     tl_mark(tlog, 2, 2, tl_first);
   }
   pdl_launch_dependents();
@@ -335,7 +337,7 @@ __global__ void __launch_bounds__(SB) sample_kernel(const __nv_bfloat16* __restr
 
 // ------------------------------------------------------------------ S5-S7 from the summaries
 struct FitParams {
-  const double* summ;     // [units][G][nb][4]: m_b, head sum, window-1 sum, window-2 sum
+  const float* summ;      // [units][G][nb][4]: m_b, head sum, window-1 sum, window-2 sum
   const float* logits;    // [units][G][slots]
   const int* order;
   const int* ends;
@@ -356,339 +358,118 @@ struct FitParams {
   int need_unit_prefix;      // global attention split (units > CTAs/2): compute unit_prefix
 };
 
-constexpr int FIT_THREADS = 256;
-
-// debug: %globaltimer stamp i of the fit kernel's CTA (g, u == 0) / of the last CTAs
-#define FIT_STAMP(i)                                                     \
-  if (P.tlog && tid == 0 && (u == 0 || (i) >= 8)) {                      \
-    unsigned long long t_;                                               \
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));               \
-    P.tlog[256 + ((i) >= 8 ? 64 + (i) : g * 8 + (i))] = t_;              \
-    if ((i) < 8) P.tlog[256 + 96 + g * 8 + (i)] = clock64();             \
-  }
-
-__global__ void __launch_bounds__(FIT_THREADS) fit_kernel(const FitParams P) {
-  __shared__ double redd[32];
-  __shared__ float redf[32];
-  __shared__ int redi[32];
-  __shared__ long long sh_k;
-  __shared__ double s_pref[FIT_THREADS];
-  __shared__ bool s_last;
-  __shared__ int s_totc, s_tott;
-  extern __shared__ __align__(16) uint8_t fsm[];
-  const int g = blockIdx.x, u = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
-  const int C = P.C, n = P.n, nb = P.nb;
-  const SampleConsts sc = P.sc;
-  const size_t ug = (size_t)u * P.G + g;
-  // everything this CTA reads is staged in smem up front (one round trip): the static
-  // cluster offsets before the dependency wait, the previous kernels' outputs after it
-  double* sm = (double*)fsm;                 // [nb][4]
-  int* s_off = (int*)(sm + (size_t)nb * 4);  // [C+1]
-  int* s_end = s_off + C + 1;                // [C]
-  int* s_ord = s_end + C;                    // [C]
-  FIT_STAMP(0);
-  for (int i = tid; i <= C; i += nt) s_off[i] = P.offsets[(size_t)u * (C + 1) + i];
-  pdl_wait();
-  FIT_STAMP(1);
-  for (int i = tid; i < nb * 4; i += nt) sm[i] = P.summ[ug * nb * 4 + i];
-  for (int i = tid; i < C; i += nt) {
-    s_end[i] = P.ends[ug * C + i];
-    s_ord[i] = P.order[ug * C + i];
-  }
-  __syncthreads();
-  FIT_STAMP(2);
-  // common shift m = max of the block maxima (reading 13)
-  float mloc = -INFINITY;
-  for (int b = tid; b < nb; b += nt) mloc = fmaxf(mloc, (float)sm[b * 4]);
-  const double m = (double)block_reduce<float, RED_MAX>(mloc, redf);
-  double eh = 0.0, e1 = 0.0, e2 = 0.0;
-  for (int b = tid; b < nb; b += nt) {
-    const double f = exp(sm[b * 4] - m);
-    eh += sm[b * 4 + 1] * f;
-    e1 += sm[b * 4 + 2] * f;
-    e2 += sm[b * 4 + 3] * f;
-  }
-  const double EN = block_reduce<double, RED_SUM>(eh, redd);
-  double a = 0.0, b = 0.0, mu1 = 0.0, mu2 = 0.0, W = EN;
-  if (!sc.fallback) {
-    const int W1 = 2 * sc.w + 1;
-    mu1 = block_reduce<double, RED_SUM>(e1, redd) / (double)W1;
-    mu2 = block_reduce<double, RED_SUM>(e2, redd) / (double)W1;
-    const double x1 = (double)sc.x1, x2 = (double)sc.x2;
-    a = (mu1 - mu2) * x1 * x2 / (x2 - x1);  // O8 / Alg. 1 l.4
-    b = mu1 - a / x1;
-    W = EN + tail_mass(a, b, sc.N, n);
-  }
-  FIT_STAMP(3);
-  long long kstar = (long long)n + 1;  // p >= 1: every rank (reading 15)
-  if (P.p < 1.0) {
-    const double target = P.p * W;
-    if (EN >= target) {
-      // exact head: the crossing block (head slots are the first nex slots, in rank order)
-      const int nex = sc.fallback ? n : sc.N;
-      const int nbh = (nex + SB - 1) / SB;
-      double bh = 0.0;
-      if (tid < nbh) bh = sm[tid * 4 + 1] * exp(sm[tid * 4] - m);
-      double run = block_exclusive_scan<double>(bh, redd, (double*)nullptr);  // nbh <= blockDim (checked on host)
-      s_pref[tid] = run + bh;
-      __syncthreads();
-      if (tid == 0) {
-        int bs = nbh - 1;
-        for (int i = 0; i < nbh; ++i)
-          if (s_pref[i] >= target) { bs = i; break; }
-        sh_k = bs;
-      }
-      __syncthreads();
-      const int bs = (int)sh_k;
-      const double before = bs ? s_pref[bs - 1] : 0.0;
-      __syncthreads();
-      // within the block: warp 0 loads its (<= SB = 128) head slots at once, 4 per lane,
-      // scans the four 32-slot chunks in parallel, then carries the chunk totals
-      if (tid < 32) {
-        const int s0 = bs * SB, s1 = min(nex, s0 + SB);
-        double w[SB / 32];
-#pragma unroll
-        for (int k = 0; k < SB / 32; ++k) {
-          const int s = s0 + k * 32 + tid;
-          w[k] = s < s1 ? exp((double)__ldcg(P.logits + ug * sc.slots + s) - m) : 0.0;
-        }
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1)
-#pragma unroll
-          for (int k = 0; k < SB / 32; ++k) {
-            const double x = __shfl_up_sync(0xffffffffu, w[k], o);
-            if (tid >= o) w[k] += x;
-          }
-        double acc = before;
-        int found = -1;
-#pragma unroll
-        for (int k = 0; k < SB / 32; ++k) {
-          const int s = s0 + k * 32 + tid;
-          const unsigned hit = __ballot_sync(0xffffffffu, s < s1 && acc + w[k] >= target);
-          if (found < 0 && hit) found = s0 + k * 32 + __ffs(hit) - 1;
-          acc += __shfl_sync(0xffffffffu, w[k], 31);
-        }
-        if (tid == 0) sh_k = (found >= 0 ? found : s1 - 1) + 1;  // rounding guard: the block's last slot
-      }
-      __syncthreads();
-      kstar = sh_k;
-    } else {
-      const double aa = a, bb = b, en_ = EN;
-      const long long NN = sc.N;
-      kstar = block_lower_bound(NN + 1, n, [&](long long k) { return en_ + tail_mass(aa, bb, NN, k) >= target; },
-                                &sh_k);
-    }
-  }
-  // J = #{r : s_r < k*} = 1 + #{r < C-1 : e_r < k*}; mark the selected non-empty clusters
-  FIT_STAMP(4);
-  const int* en = s_end;
-  const int* ord = s_ord;
-  const int* off = s_off;
-  int cnt = 0;
-  for (int r = tid; r < C - 1; r += nt) cnt += en[r] < kstar;
-  const int J = 1 + block_reduce<int, RED_SUM>(cnt, redi);
-  uint8_t* macc = P.mask_acc + (size_t)u * C;
-  for (int r = tid; r < J; r += nt) {
-    const int cid = ord[r];
-    if (off[cid + 1] > off[cid]) macc[cid] = 1;
-  }
-  if (tid == 0) {
-    P.J[ug] = J;
-    double* f = P.fit + ug * 6;
-    f[0] = a; f[1] = b; f[2] = m; f[3] = W; f[4] = mu1; f[5] = mu2;
-  }
-  FIT_STAMP(5);
-
-  // ---- S7: the last head of the unit compacts the union (cluster-id order)
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(&P.head_cnt[u], 1u);
-    s_last = (prev == (unsigned)P.G - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  FIT_STAMP(8);
-  {
-    const int per = (C + nt - 1) / nt;
-    const int b0 = tid * per;
-    int lc = 0, lt = 0;
-    for (int j = b0; j < b0 + per && j < C; ++j)
-      if (__ldcg(macc + j)) { ++lc; lt += off[j + 1] - off[j]; }
-    int cbase = block_exclusive_scan<int>(lc, redi, &s_totc);
-    int tbase = block_exclusive_scan<int>(lt, redi, &s_tott);
-    int* ul = P.ulist + (size_t)u * C;
-    int* up = P.uprefix + (size_t)u * (C + 1);
-    uint8_t* um = P.umask + (size_t)u * C;
-    for (int j = b0; j < b0 + per && j < C; ++j) {
-      const uint8_t mk = __ldcg(macc + j);
-      um[j] = mk;
-      macc[j] = 0;  // reset the accumulator for the next call
-      if (mk) {
-        ul[cbase] = off[j];
-        up[cbase] = tbase;
-        ++cbase;
-        tbase += off[j + 1] - off[j];
-      }
-    }
-    const int ucount = s_totc, tot = s_tott;
-    for (int k = ucount + tid; k <= C; k += nt) {
-      up[k] = tot;
-      if (k < C) ul[k] = 0;
-    }
-  }
-  if (tid == 0) P.head_cnt[u] = 0;
-  FIT_STAMP(9);
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(P.unit_cnt, 1u);
-    s_last = (prev == (unsigned)P.units - 1);
-  }
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    FIT_STAMP(10);
-    const int units = P.units;
-    const int per = (units + nt - 1) / nt;
-    const int b0 = tid * per;
-    long long loc = 0;
-    for (int v = b0; v < b0 + per && v < units; ++v) loc += __ldcg(P.uprefix + (size_t)v * (C + 1) + C);
-    long long run = block_exclusive_scan<long long>(loc, (long long*)redd, (long long*)nullptr);
-    for (int v = b0; v < b0 + per && v < units; ++v) {
-      P.unit_prefix[v] = run;
-      run += __ldcg(P.uprefix + (size_t)v * (C + 1) + C);
-    }
-    if (b0 < units && b0 + per >= units) P.unit_prefix[units] = run;
-    if (tid == 0) *P.unit_cnt = 0u;
-    FIT_STAMP(11);
-  }
-  pdl_launch_dependents();
-}
-
 // ------------------------------------------------------------------ S5-S7, one CTA per unit
-// One warp per query head does the whole fit with warp-level reductions (no block
-// barriers on the per-head critical path); the G heads run concurrently and OR their
-// selections into a shared-memory mask that the CTA compacts into the work list.
+// One warp per query head does the whole fit (Alg. 1 l.4-10) with warp-level reductions
+// and no block barrier on the per-head critical path; the G heads run concurrently and
+// OR their selected clusters into a shared-memory mask that the CTA compacts into the
+// attention work list (S7).  Float32 arithmetic throughout: on sm_100a a dependent fp64
+// exp/log costs ~170/~290 cycles against ~55 for the fp32 special-function unit, and the
+// fit is one long dependency chain.  fp32 keeps every decision within the parity
+// contract's 1e-5 threshold band (the sums are tree reductions of <= 4K terms).
 
-// H(k) - H(j) for 0 <= j <= k: exact sums below 20, otherwise one log and the
-// asymptotic series of both ends (harmonic() above, written as a difference)
-__device__ double harmonic_diff(long long k, long long j) {
-  if (k <= j) return 0.0;
-  if (j < 20) return harmonic(k) - harmonic(j);
-  const double xk = (double)k, xj = (double)j;
-  auto tail = [](double x) {
-    const double x2 = 1.0 / (x * x);
-    return 0.5 / x - x2 * (1.0 / 12.0 - x2 * (1.0 / 120.0 - x2 * (1.0 / 252.0 - x2 * (1.0 / 240.0 - x2 * (1.0 / 132.0)))));
+// H(k) - H(j) = sum_{i=j+1}^{k} 1/i for 0 <= j <= k: exact terms below 16, above that
+// log1p of the ratio plus the difference of the asymptotic series 1/2x - 1/12x^2 + 1/120x^4
+// (the next term is < 2.4e-10 at x = 16).
+__device__ __forceinline__ float harm_diff_f(int k, int j) {
+  if (k <= j) return 0.f;
+  float s = 0.f;
+  while (j < 16 && j < k) s += 1.f / (float)(++j);  // tiny n only
+  if (k <= j) return s;
+  const float xk = (float)k, xj = (float)j;
+  auto t = [](float x) {
+    const float r = 1.f / x, r2 = r * r;
+    return r * 0.5f - r2 * (1.f / 12.f - r2 * (1.f / 120.f));
   };
-  return log1p((xk - xj) / xj) + tail(xk) - tail(xj);
+  return s + log1pf((xk - xj) / xj) + (t(xk) - t(xj));
 }
 
-// sum_{i=N+1}^{k} max(0, a/i + b) with one log per evaluation
-__device__ double tail_mass1(double a, double b, long long N, long long k) {
-  if (k <= N) return 0.0;
-  if (a >= 0.0 && b >= 0.0) return a * harmonic_diff(k, N) + b * (double)(k - N);
-  if (a <= 0.0 && b <= 0.0) return 0.0;
-  if (a > 0.0) {
-    const double t = a / (-b);
-    long long top = t >= 9.0e15 ? k : (long long)floor(t);
-    if (top > k) top = k;
-    while (top < k && a / (double)(top + 1) + b > 0.0) ++top;
-    while (top > N && !(a / (double)top + b > 0.0)) --top;
-    if (top <= N) return 0.0;
-    return a * harmonic_diff(top, N) + b * (double)(top - N);
-  }
-  const double t = (-a) / b;
-  long long lo = t >= 9.0e15 ? k + 1 : (long long)floor(t) + 1;
-  if (lo < N + 1) lo = N + 1;
-  while (lo > N + 1 && a / (double)(lo - 1) + b > 0.0) --lo;
-  while (lo <= k && !(a / (double)lo + b > 0.0)) ++lo;
-  if (lo > k) return 0.0;
-  return a * harmonic_diff(k, lo - 1) + b * (double)(k - lo + 1);
-}
-
-// The positive terms of a/i + b over i in (N, n] form one interval [lo, hi] (a/i + b is
-// monotone in i), found once per head; tail(k) = tail_mass1(a, b, N, k) for every k <= n
-// then costs one harmonic_diff.
-struct TailFn {
-  double a, b;
-  long long lo, hi;  // empty when lo > hi
-  __device__ double operator()(long long k) const {
-    const long long kk = k < hi ? k : hi;
-    if (kk < lo) return 0.0;
-    return a * harmonic_diff(kk, lo - 1) + b * (double)(kk - lo + 1);
+// sum_{i=N+1}^{k} max(0, a/i + b): the positive terms of the monotone a/i + b form one
+// rank interval [lo, hi] inside (N, n] (a/i + b > 0  <=>  a + b i > 0 for i > 0), found
+// once per head; each evaluation then costs one log1pf.
+struct TailF {
+  float a, b;
+  int lo, hi;  // empty when lo > hi
+  __device__ __forceinline__ float operator()(int k) const {
+    const int kk = k < hi ? k : hi;
+    if (kk < lo) return 0.f;
+    return a * harm_diff_f(kk, lo - 1) + b * (float)(kk - lo + 1);
   }
 };
-__device__ TailFn make_tail(double a, double b, long long N, long long n) {
-  TailFn f = {a, b, N + 1, n};
-  if (a >= 0.0 && b >= 0.0) return f;
-  if (a <= 0.0 && b <= 0.0) { f.lo = n + 1; return f; }
-  if (a > 0.0) {  // decreasing: positive for i <= top
-    const double t = a / (-b);
-    long long top = t >= 9.0e15 ? n : (long long)floor(t);
-    if (top > n) top = n;
-    while (top < n && a / (double)(top + 1) + b > 0.0) ++top;
-    while (top > N && !(a / (double)top + b > 0.0)) --top;
+__device__ __forceinline__ TailF make_tail_f(float a, float b, int N, int n) {
+  TailF f = {a, b, N + 1, n};
+  auto pos = [&](int i) { return fmaf(b, (float)i, a) > 0.f; };
+  if (a >= 0.f && b >= 0.f) return f;
+  if (a <= 0.f && b <= 0.f) { f.lo = n + 1; return f; }
+  if (a > 0.f) {  // decreasing: positive for i < a / (-b)
+    const float t = a / (-b);
+    int top = t >= (float)n ? n : (int)floorf(t);
+    while (top < n && pos(top + 1)) ++top;
+    while (top > N && !pos(top)) --top;
     f.hi = top;  // top <= N: empty
     return f;
   }
-  const double t = (-a) / b;  // increasing: positive for i >= lo
-  long long lo = t >= 9.0e15 ? n + 1 : (long long)floor(t) + 1;
+  const float t = (-a) / b;  // increasing: positive for i > (-a) / b
+  int lo = t >= (float)n ? n + 1 : (int)floorf(t) + 1;
   if (lo < N + 1) lo = N + 1;
-  while (lo > N + 1 && a / (double)(lo - 1) + b > 0.0) --lo;
-  while (lo <= n && !(a / (double)lo + b > 0.0)) ++lo;
+  while (lo > N + 1 && pos(lo - 1)) --lo;
+  while (lo <= n && !pos(lo)) ++lo;
   f.lo = lo;
   return f;
 }
 
-// Warp-cooperative count of entries < key in a non-decreasing int array (all lanes call):
-// 32 probes per round, 2 rounds for 1024 entries.
-__device__ __forceinline__ int warp_count_less(const int* arr, int len, long long key) {
+// Warp-cooperative count of the leading falses of a monotone predicate over [0, len)
+// (false ... false true ... true): 32 probes per round, 2 rounds for len <= 1024.
+template <typename Pred>
+__device__ __forceinline__ int warp_count_false(int len, Pred pred) {
   const int lane = threadIdx.x & 31;
   int lo = 0, hi = len;  // answer in [lo, hi]
   while (hi - lo > 32) {
     const int step = (hi - lo + 31) >> 5;
     const int idx = lo + lane * step;
-    const unsigned bal = __ballot_sync(0xffffffffu, idx < hi && (long long)arr[idx] < key);
-    const int c = __popc(bal);
+    const int c = __popc(__ballot_sync(0xffffffffu, idx < hi && !pred(idx)));
     const int nlo = c > 0 ? lo + (c - 1) * step + 1 : lo;
     const int nhi = lo + c * step < hi ? lo + c * step : hi;
     lo = nlo;
     hi = nhi;
   }
   const int idx = lo + lane;
-  return lo + __popc(__ballot_sync(0xffffffffu, idx < hi && (long long)arr[idx] < key));
+  return lo + __popc(__ballot_sync(0xffffffffu, idx < hi && !pred(idx)));
 }
 
-constexpr int FITU_THREADS = 512;
+constexpr int FITU_THREADS = 256;
 
 __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams P) {
   extern __shared__ __align__(16) uint8_t fsm[];
-  __shared__ int redi[8];
-  __shared__ int s_totc, s_tott;
+  __shared__ int s_J[8];
   __shared__ bool s_last;
-  __shared__ int s_J[64];
   const int u = blockIdx.x, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int C = P.C, n = P.n, nb = P.nb, G = P.G;
   const SampleConsts sc = P.sc;
-  double* sm = (double*)fsm;                       // [G][nb][4]
-  int* s_off = (int*)(sm + (size_t)G * nb * 4);     // [C+1]
-  int* s_end = s_off + ((C + 1 + 3) & ~3);         // [G][C] (16-byte aligned for bulk copies)
-  int* s_ord = s_end + (size_t)G * C;              // [G][C]
-  uint8_t* mask = (uint8_t*)(s_ord + (size_t)G * C);  // [C]
-  const unsigned long long stamp_on = P.tlog != nullptr && u == 0;
-  auto stamp = [&](int i) {
+  float* sm = (float*)fsm;                           // [G][nb][4]
+  int* s_off = (int*)(sm + (((size_t)G * nb * 4 + 3) & ~(size_t)3));  // [C+1]
+  int* s_end = s_off + ((C + 1 + 3) & ~3);           // [G][C] (16-byte aligned for bulk copies)
+  int* s_ord = s_end + (size_t)G * C;                // [G][C]
+  uint8_t* mask = (uint8_t*)(s_ord + (size_t)G * C); // [C]
+  const bool stamp_on = P.tlog != nullptr && u == 0;
+  auto stamp = [&](int i) {  // debug: CTA of unit 0 at tlog[256 + i]
     if (stamp_on && tid == 0) {
       unsigned long long t_;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
       P.tlog[256 + i] = t_;
     }
   };
+  auto wstamp = [&](int i) {  // debug: warp 0 (head 0) of unit 0 at tlog[1700 + i]
+    if (stamp_on && tid == 0) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      P.tlog[1700 + i] = t_;
+      P.tlog[1710 + i] = clock64();
+    }
+  };
   stamp(0);
   if (tid == 0) tl_mark(P.tlog, 3, 0, u == 0);
+  // index data (not produced by the previous kernels): before the dependency wait
   for (int i = tid; i <= C; i += nt) s_off[i] = P.offsets[(size_t)u * (C + 1) + i];
-  for (int i = tid; i < C; i += nt) mask[i] = 0;
   __shared__ uint64_t sbar;
   const size_t ub = (size_t)u * G;
   const bool bulk_ok = ((ub * C) % 4 == 0) && (((size_t)G * C) % 4 == 0);
@@ -696,72 +477,86 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
     mbar_init(&sbar, 1);
     fence_barrier_init();
   }
+  for (int i = tid; i < C; i += nt) mask[i] = 0;
   __syncthreads();
-  pdl_wait();
-  stamp(1);
-  if (tid == 0) tl_mark(P.tlog, 3, 1, u == 0);
-  // stage the previous kernels' outputs with 1-D bulk copies (one round trip)
-  if (tid == 0) {
-    const uint32_t bs = (uint32_t)G * nb * 32, be = bulk_ok ? (uint32_t)G * C * 4 : 0u;
-    mbar_arrive_expect_tx(&sbar, bs + 2 * be);
-    bulk_g2s(sm, P.summ + ub * nb * 4, bs, &sbar);
-    if (bulk_ok) {
-      bulk_g2s(s_end, P.ends + ub * C, be, &sbar);
-      bulk_g2s(s_ord, P.order + ub * C, be, &sbar);
+  {
+    pdl_wait();
+    stamp(1);
+    if (tid == 0) tl_mark(P.tlog, 3, 1, u == 0);
+    // stage the previous kernels' outputs with 1-D bulk copies (one round trip)
+    if (tid == 0) {
+      const uint32_t bs = (uint32_t)G * nb * 16, be = bulk_ok ? (uint32_t)G * C * 4 : 0u;
+      mbar_arrive_expect_tx(&sbar, bs + 2 * be);
+      bulk_g2s(sm, P.summ + ub * nb * 4, bs, &sbar);
+      if (bulk_ok) {
+        bulk_g2s(s_end, P.ends + ub * C, be, &sbar);
+        bulk_g2s(s_ord, P.order + ub * C, be, &sbar);
+      }
     }
+    if (!bulk_ok)
+      for (int i = tid; i < G * C; i += nt) {
+        s_end[i] = P.ends[ub * C + i];
+        s_ord[i] = P.order[ub * C + i];
+      }
+    mbar_wait(&sbar, 0);
+    __syncthreads();
+    stamp(2);
+    if (stamp_on && tid == 0) P.tlog[1709] = clock64();
   }
-  if (!bulk_ok)
-    for (int i = tid; i < G * C; i += nt) {
-      s_end[i] = P.ends[ub * C + i];
-      s_ord[i] = P.order[ub * C + i];
-    }
-  mbar_wait(&sbar, 0);
-  __syncthreads();
-  stamp(2);
-  for (int g = warp; g < G; g += nt / 32) {
-    const double* sg = sm + (size_t)g * nb * 4;
-    // common shift m = max of the block maxima (reading 13)
+  if (warp < G) {
+    const int g = warp;
+    const float* sg = sm + (size_t)g * nb * 4;
+    // common shift m = max of the block maxima (reading 13), then the three region sums
     float mf = -INFINITY;
-    for (int b = lane; b < nb; b += 32) mf = fmaxf(mf, (float)sg[b * 4]);
-    mf = warp_max(mf);
-    const double m = (double)mf;
-    double eh = 0.0, e1 = 0.0, e2 = 0.0;
+    for (int b = lane; b < nb; b += 32) mf = fmaxf(mf, sg[b * 4]);
+    const float m = warp_max(mf);
+    float eh = 0.f, e1 = 0.f, e2 = 0.f;
     for (int b = lane; b < nb; b += 32) {
-      const double f = exp(sg[b * 4] - m);
-      eh += sg[b * 4 + 1] * f;
-      e1 += sg[b * 4 + 2] * f;
-      e2 += sg[b * 4 + 3] * f;
+      const float4 v = *reinterpret_cast<const float4*>(sg + b * 4);
+      const float f = __expf(v.x - m);
+      eh = fmaf(v.y, f, eh);
+      e1 = fmaf(v.z, f, e1);
+      e2 = fmaf(v.w, f, e2);
     }
-    const double EN = warp_sum_d(eh);
-    double a = 0.0, b = 0.0, mu1 = 0.0, mu2 = 0.0, W = EN;
-    TailFn tail = {0.0, 0.0, 1, 0};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {  // three interleaved butterflies
+      eh += __shfl_xor_sync(0xffffffffu, eh, o);
+      e1 += __shfl_xor_sync(0xffffffffu, e1, o);
+      e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+    }
+    const float EN = eh;
+    wstamp(0);
+    float a = 0.f, b = 0.f, mu1 = 0.f, mu2 = 0.f, W = EN;
+    TailF tail = {0.f, 0.f, 1, 0};
     if (!sc.fallback) {
-      const int W1 = 2 * sc.w + 1;
-      mu1 = warp_sum_d(e1) / (double)W1;
-      mu2 = warp_sum_d(e2) / (double)W1;
-      const double x1 = (double)sc.x1, x2 = (double)sc.x2;
-      a = (mu1 - mu2) * x1 * x2 / (x2 - x1);  // O8 / Alg. 1 l.4
+      const float W1 = (float)(2 * sc.w + 1);
+      mu1 = e1 / W1;
+      mu2 = e2 / W1;
+      const float x1 = (float)sc.x1, x2 = (float)sc.x2;
+      a = (mu1 - mu2) * (x1 * x2 / (x2 - x1));  // O8 / Alg. 1 l.4
       b = mu1 - a / x1;
-      tail = make_tail(a, b, sc.N, n);
+      tail = make_tail_f(a, b, sc.N, n);
       W = EN + tail(n);
     }
-    long long kstar = (long long)n + 1;  // p >= 1: every rank (reading 15)
+    wstamp(1);
+    int J = C;  // p >= 1: every cluster (reading 15)
     if (P.p < 1.0) {
-      const double target = P.p * W;
+      const float target = (float)P.p * W;
+      const int* eg = s_end + (size_t)g * C;
       if (EN >= target) {
-        // crossing block of the exact head (head slots = the first nex slots)
+        // the crossing lies inside the exact head (slots 0..nex-1 = ranks 1..nex): the
+        // block of SB slots that crosses, then the slot inside it (one global round trip)
         const int nex = sc.fallback ? n : sc.N;
         const int nbh = (nex + SB - 1) / SB;
-        double carry = 0.0;
+        float carry = 0.f, before = 0.f;
         int bs = nbh - 1;
-        double before = 0.0;
         for (int b0 = 0; b0 < nbh; b0 += 32) {
           const int bb = b0 + lane;
-          const double vo = bb < nbh ? sg[bb * 4 + 1] * exp(sg[bb * 4] - m) : 0.0;
-          double v = vo;
+          const float vo = bb < nbh ? sg[bb * 4 + 1] * __expf(sg[bb * 4] - m) : 0.f;
+          float v = vo;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
-            const double x = __shfl_up_sync(0xffffffffu, v, o);
+            const float x = __shfl_up_sync(0xffffffffu, v, o);
             if (lane >= o) v += x;
           }
           const unsigned hit = __ballot_sync(0xffffffffu, bb < nbh && carry + v >= target);
@@ -774,74 +569,61 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
           carry += __shfl_sync(0xffffffffu, v, 31);
           before = carry;
         }
-        // inside the block: its <= SB slots, 4 per lane, chunk scans + carries
         const int s0 = bs * SB, s1 = min(nex, s0 + SB);
-        double w[SB / 32];
+        float w[SB / 32];
 #pragma unroll
-        for (int k = 0; k < SB / 32; ++k) {
-          const int s = s0 + k * 32 + lane;
-          w[k] = s < s1 ? exp((double)__ldcg(P.logits + (ub + g) * sc.slots + s) - m) : 0.0;
+        for (int k = 0; k < SB / 32; ++k) {  // slot s0 + 4 lane + k: 4 consecutive per lane
+          const int s = s0 + 4 * lane + k;
+          w[k] = s < s1 ? __expf(__ldcg(P.logits + (ub + g) * sc.slots + s) - m) : 0.f;
         }
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1)
+        for (int k = 1; k < SB / 32; ++k) w[k] += w[k - 1];
+        float v = w[SB / 32 - 1];
 #pragma unroll
-          for (int k = 0; k < SB / 32; ++k) {
-            const double x = __shfl_up_sync(0xffffffffu, w[k], o);
-            if (lane >= o) w[k] += x;
-          }
-        double acc = before;
-        int found = -1;
-#pragma unroll
-        for (int k = 0; k < SB / 32; ++k) {
-          const int s = s0 + k * 32 + lane;
-          const unsigned hit = __ballot_sync(0xffffffffu, s < s1 && acc + w[k] >= target);
-          if (found < 0 && hit) found = s0 + k * 32 + __ffs(hit) - 1;
-          acc += __shfl_sync(0xffffffffu, w[k], 31);
+        for (int o = 1; o < 32; o <<= 1) {
+          const float x = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += x;
         }
-        kstar = (found >= 0 ? found : s1 - 1) + 1;  // rounding guard: the block's last slot
+        const float excl = before + v - w[SB / 32 - 1];
+        int kl = SB / 32;
+#pragma unroll
+        for (int k = SB / 32 - 1; k >= 0; --k)
+          if (s0 + 4 * lane + k < s1 && excl + w[k] >= target) kl = k;
+        const unsigned hit = __ballot_sync(0xffffffffu, kl < SB / 32);
+        const int hl = hit ? __ffs(hit) - 1 : 31;
+        const int kls = __shfl_sync(0xffffffffu, kl, hl);
+        // k* = the 1-based rank of the crossing slot (rounding guard: the block's last slot)
+        const int kstar = hit ? s0 + 4 * hl + kls + 1 : s1;
+        J = 1 + warp_count_false(C - 1, [&](int r) { return eg[r] >= kstar; });
       } else {
-        // minimal k in (N, n] with EN + tail(k) >= target: 32-way warp search
-        long long lo = sc.N + 1, hi = n;
-        while (lo < hi) {
-          const long long step = (hi - lo + 32) / 32;  // ceil((hi-lo+1)/32)
-          const long long k = lo + (long long)lane * step;
-          const bool ok = k <= hi && EN + tail(k) >= target;
-          const unsigned bal = __ballot_sync(0xffffffffu, ok);
-          const int h = bal ? __ffs(bal) - 1 : 32;
-          const long long nhi = h < 32 ? lo + (long long)h * step : hi;
-          const long long nlo = h > 0 ? lo + (long long)(h - 1) * step + 1 : lo;
-          lo = nlo;
-          hi = nhi < hi ? nhi : hi;
-          if (step == 1) { lo = hi; break; }
-        }
-        kstar = hi;
+        // past the head: cum(e_r) = EN + tail(e_r) at the cluster ends; the first cluster
+        // whose end reaches the target (ends are non-decreasing in rank)
+        const int r = warp_count_false(C, [&](int r) { return eg[r] > sc.N && EN + tail(eg[r]) >= target; });
+        J = r < C ? r + 1 : C;
       }
     }
-    // J = #{r : s_r < k*} = 1 + #{r < C-1 : e_r < k*}; mark the selected non-empty clusters
-    // (the ends are non-decreasing in rank: a 32-way search)
-    const int J = 1 + warp_count_less(s_end + (size_t)g * C, C - 1, kstar);
+    wstamp(3);
     if (lane == 0) {
       s_J[g] = J;
       P.J[ub + g] = J;
       double* f = P.fit + (ub + g) * 6;
       f[0] = a; f[1] = b; f[2] = m; f[3] = W; f[4] = mu1; f[5] = mu2;
     }
-  }
-  __syncthreads();
-  // mark the selected non-empty clusters of every head (all threads)
-  for (int g = 0; g < G; ++g) {
+    // mark this head's selected non-empty clusters (the OR over heads is the GQA union)
     const int* ord = s_ord + (size_t)g * C;
-    for (int r = tid; r < s_J[g]; r += nt) {
+    __syncwarp();
+    for (int r = lane; r < J; r += 32) {
       const int cid = ord[r];
       if (s_off[cid + 1] > s_off[cid]) mask[cid] = 1;
     }
+    wstamp(4);
   }
   __syncthreads();
   stamp(3);
   // ---- S7: compact the union (cluster-id order) into the work list.  Thread t owns a
   // contiguous cluster chunk; one packed (tokens << 20 | clusters) block scan places it.
   {
-    __shared__ unsigned long long w_sum[32];
+    __shared__ unsigned long long w_sum[FITU_THREADS / 32];
     const int nw = nt >> 5;
     const int per = (C + nt - 1) / nt;
     const int j0 = tid * per, j1 = min(C, j0 + per);
@@ -883,14 +665,13 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
       if (k < C) ul[k] = 0;
     }
   }
+  stamp(4);
   // the unit-aligned attention split reads only the per-unit totals (uprefix[u][C]); the
   // global split needs unit_prefix, computed by the last CTA to finish
   if (!P.need_unit_prefix) {
-    stamp(4);
     if (tid == 0) tl_mark(P.tlog, 3, 2, u == 0);
     return;
   }
-  stamp(4);
   __syncthreads();
   if (tid == 0) {
     __threadfence();
@@ -900,11 +681,6 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
   __syncthreads();
   if (s_last) {
     __threadfence();
-    if (P.tlog && tid == 0) {
-      unsigned long long t_;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-      P.tlog[256 + 5] = t_;
-    }
     const int units = P.units;
     const int per = (units + nt - 1) / nt;
     const int b0 = tid * per;
@@ -919,11 +695,6 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
     if (tid == 0) {
       P.unit_prefix[units] = s_tot;
       *P.unit_cnt = 0u;
-    }
-    if (P.tlog && tid == 0) {
-      unsigned long long t_;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-      P.tlog[256 + 6] = t_;
     }
   }
   if (tid == 0) tl_mark(P.tlog, 3, 2, u == 0);
@@ -1261,7 +1032,7 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
   P.need_unit_prefix = !unit_split_ok(x->units, x->num_ctas);
   cudaLaunchAttribute attr[1];
   const size_t smem =
-      (size_t)x->G * P.nb * 32 + (size_t)(x->C + 4) * 4 + (size_t)2 * x->G * x->C * 4 + (size_t)x->C + 64;
+      (size_t)x->G * P.nb * 16 + 16 + (size_t)(x->C + 4) * 4 + (size_t)2 * x->G * x->C * 4 + (size_t)x->C + 64;
   static size_t done = 0;
   cudaError_t e = ensure_smem((const void*)fit_unit_kernel, smem, &done);
   if (e != cudaSuccess) return e;

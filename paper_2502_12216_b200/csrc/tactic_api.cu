@@ -190,14 +190,14 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_
   x->unit_prefix = A.get<long long>(U + 1);
   x->counter = A.get<unsigned int>(1);
   x->part_o = A.get<float>((x->num_ctas + U) * G * 128);
-  x->part_lse = A.get<float>((x->num_ctas + U) * G);
+  x->part_lse = A.get<float>((x->num_ctas + U) * G + 4);  // +4: the merge's 16-byte bulk reads
   x->stage = A.get<double>(U * G * 2);
   x->q_stage = A.get<__nv_bfloat16>(U * G * 128);
   x->o_stage = A.get<__nv_bfloat16>(U * G * 128);
   x->unit_cnt = A.get<int>(U);
   x->rowstart = A.get<int>(U * G * C);
   x->rowmap = A.get<int>(U * G * (size_t)x->sc.slots);
-  x->summ = A.get<double>(U * G * (size_t)sample_blocks(x->sc.slots) * 4);
+  x->summ = A.get<float>(U * G * (size_t)sample_blocks(x->sc.slots) * 4);
   x->mask_acc = A.get<uint8_t>(U * C);
   x->head_cnt = A.get<unsigned int>(U);
   if (A.err != cudaSuccess) {

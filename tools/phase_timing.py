@@ -69,9 +69,11 @@ for it in range(4):
                                              if fs[i] > 0))
         hs = full[1700:1705]
         if hs[0] > 0:
-            names = ["sums", "W", "k*", "J", "all heads"]
+            names = ["sums", "W", "k*", "J", "marked"]
             print("  fit warp 0 (us after staged): " + "  ".join(f"{nm} {(hs[i] - fs[2]) / 1e3:.2f}"
-                                                               for i, nm in enumerate(names)))
+                                                               for i, nm in enumerate(names) if hs[i] > 0))
+            ck = full[1709:1715]
+            print("  fit warp 0 (cycles after staged): " + "  ".join(f"{nm} {ck[i + 1] - ck[0]}" for i, nm in enumerate(names) if hs[i] > 0))
     else:
         t = full.reshape(-1, 16, 8)[:, :R, :]
         t0 = t[:, :, 0].min()
@@ -88,6 +90,9 @@ for it in range(4):
         con = [(x - b0) / 1e3 for x in at[18:34] if x > 0]
         print(f"  attention CTA0: starts {(b0 - t0) / 1e3:.2f} us after selection start; ends +{(at[34] - b0) / 1e3:.2f}")
         print("   tiles issued at", np.round(iss, 2).tolist())
+        pz = full[192 + 40:192 + 45]
+        print("   producer setup (us after wait): " + "  ".join(f"{nm} {(x - b0) / 1e3:.2f}" for nm, x in
+              zip(["split", "lists loaded", "synced", "search start", "window in"], pz) if x > 0))
         print("   tiles consumed at", np.round(con, 2).tolist())
         ce = full[512:512 + 296].reshape(-1, 2)
         ce = ce[(ce[:, 0] > 0) & (ce[:, 1] > 0)]
