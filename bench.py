@@ -12,9 +12,12 @@ timed separately ("build").  N>1 (torchrun): each rank runs its own batch-1 C2 l
 (batch x KV-head sharding, no collective on the data path), scaling "weak"; the
 reported time is the max over ranks divided by N (job-level us per layer-step).
 
-L2: a 256 MiB buffer is written before every timed step (the 40 MB sparse working set
-would otherwise stay in the 126 MB L2); each step is bracketed by CUDA events on the
-launching stream.  --impl reference times the float64 CPU oracle (the reference arm of
+Layers: the timed steps cycle over LAYERS = 8 distinct synthetic layers (seeds 8 rank + l),
+one index each, as a model's decode does (>= 8 distinct layer caches); the
+selected fraction varies from layer to layer, so the mean is over layers.
+L2: a 256 MiB buffer is written before every timed step as well (the sparse working set
+would otherwise partly stay in the 126 MB L2); each step is bracketed by CUDA events on
+the launching stream.  --impl reference times the float64 CPU oracle (the reference arm of
 this tier) on the same workload.
 """
 from __future__ import annotations
@@ -35,6 +38,7 @@ METRIC = "decode-attn µs/layer-step & HBM GB/s vs own dense decode @128K, p=0.9
 UNIT = "µs/layer-step"
 WORKLOAD = "C2"
 CFG = dict(B=1, Hkv=8, G=4, n=131072, C=1024, iters=10)
+LAYERS = 8
 PAPER_CONTEXT = ("paper (context, not target): up to 7.29x decode-attention and 1.58x end-to-end speedup vs "
                  "FlashInfer full attention on Nvidia Ada 6000, CUDA 12.4 (P:47, P:404, P:691, P:701)")
 
@@ -45,7 +49,7 @@ def _config(args, n_gpus):
             "global_batch": n_gpus, "seq_len": CFG["n"], "n_clusters": CFG["C"], "p": args.p,
             "parallelism": f"batch x KV-head sharded over {n_gpus} GPU(s), no data-path collective",
             "l2": "cold L2 before every timed step: 256 MiB buffer written, then a 256 MiB buffer read (write-back drained)",
-            "inputs": "tactic-synth-v1 (synth/), seed = rank"}
+            "inputs": f"tactic-synth-v1 (synth/), {LAYERS} layers per GPU (seeds {LAYERS} rank + l), steps cycle over them"}
 
 
 def _peaks():
@@ -205,37 +209,65 @@ def cpu_baseline(args, budget_s=12.0):
 
 
 # ------------------------------------------------------------------ GPU arm
+def _unit_bits(job):
+    from synth import bf16_bits, make_unit
+    seed, h = job
+    u = make_unit(CFG["n"], CFG["G"], seed=seed, b=0, h=h)
+    return seed, h, bf16_bits(u["K"]), bf16_bits(u["V"]), bf16_bits(u["q"])
+
+
+def make_layers(seeds, dev):
+    """The synthetic layers (one per seed) as bf16 device tensors, generated in parallel
+    on the host cores (input generation only; synth/ holds no method arithmetic)."""
+    import multiprocessing as mp
+
+    import torch
+    Hkv, G, n = CFG["Hkv"], CFG["G"], CFG["n"]
+    bf = lambda a: torch.from_numpy(a.view(np.int16)).to(dev).view(torch.bfloat16)  # noqa: E731
+    layers = {sd: {"K": torch.empty((1, Hkv, n, 128), dtype=torch.bfloat16, device=dev),
+                   "V": torch.empty((1, Hkv, n, 128), dtype=torch.bfloat16, device=dev),
+                   "q": torch.empty((1, Hkv * G, 128), dtype=torch.bfloat16, device=dev)} for sd in seeds}
+    jobs = [(sd, h) for sd in seeds for h in range(Hkv)]
+    workers = max(1, min(len(jobs), len(os.sched_getaffinity(0)) - 1, 32))
+    with mp.get_context("fork").Pool(workers) as pool:
+        for sd, h, kb, vb, qb in pool.imap_unordered(_unit_bits, jobs):
+            L = layers[sd]
+            L["K"][0, h] = bf(kb)
+            L["V"][0, h] = bf(vb)
+            L["q"][0, h * G:(h + 1) * G] = bf(qb)
+    return [layers[sd] for sd in seeds]
+
+
 def run_gpu(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2502_12216_b200 import build as B
     B.build()
     from paper_2502_12216_b200 import tactic as T
-    from synth import make_layer
-
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     T.device_check()
     G, n, C = CFG["G"], CFG["n"], CFG["C"]
-    K, V, q = make_layer(CFG["B"], CFG["Hkv"], G, n, seed=rank)
-    to = lambda a: torch.from_numpy(a).to(dev).to(torch.bfloat16)  # noqa: E731
-    Kd, Vd, qd = to(K), to(V), to(q)
-    del K, V
-    stream = torch.cuda.current_stream()
+    layers = make_layers([LAYERS * rank + l for l in range(LAYERS)], dev)
 
-    # ---- index build (tcgen05 k-means), timed separately
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    T.build_index(Kd[:, :1, :8192].contiguous(), Vd[:, :1, :8192].contiguous(), 64, 2, group_size=G)  # warm
+    # ---- index build per layer (tcgen05 k-means + relayout), timed separately
+    T.build_index(layers[0]["K"][:, :1, :8192].contiguous(), layers[0]["V"][:, :1, :8192].contiguous(), 64, 2,
+                  group_size=G)  # warm
     torch.cuda.synchronize()
-    e0.record()
-    index = T.build_index(Kd, Vd, C, CFG["iters"], group_size=G, seed=rank)
-    e1.record()
-    torch.cuda.synchronize()
-    build_ms = e0.elapsed_time(e1)
-    ex = index.export()
-    iters_run = ex["iters_run"].tolist()
-    sizes = np.stack([np.bincount(ex["assign"][u], minlength=C) for u in range(index.units)])
-    alg_tflop = 2.0 * n * C * 128 * sum(iters_run) / 1e12
+    build_ms, iters_run = [], []
+    for li, L in enumerate(layers):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        L["index"] = T.build_index(L["K"], L["V"], C, CFG["iters"], group_size=G, seed=LAYERS * rank + li)
+        e1.record()
+        torch.cuda.synchronize()
+        build_ms.append(e0.elapsed_time(e1))
+        ex = L["index"].export()
+        iters_run += ex["iters_run"].tolist()
+        L["sizes"] = np.stack([np.bincount(ex["assign"][u], minlength=C) for u in range(L["index"].units)])
+        L["out"] = torch.empty_like(L["q"])
+    units = layers[0]["index"].units
+    alg_tflop = 2.0 * n * C * 128 * sum(iters_run) / 1e12 / len(layers)   # per layer
 
     # cold L2 before every timed step: write a 256 MiB buffer (> 126 MB L2), then read a
     # second one so the dirty lines of the write are written back before the step starts
@@ -243,48 +275,43 @@ def run_gpu(args, rank, world, local_rank):
     flush_r = torch.ones(32 << 20, dtype=torch.int64, device=dev)
     flush_acc = torch.empty((), dtype=torch.int64, device=dev)
 
-    class _Flush:
-        @staticmethod
-        def fill_(v):
-            flush.fill_(v)
-            torch.sum(flush_r, dim=0, out=flush_acc)
+    def l2_flush():
+        flush.fill_(1)
+        torch.sum(flush_r, dim=0, out=flush_acc)
 
-    l2 = _Flush()
-    out = torch.empty_like(qd)
-
-    # ---- CUDA graph of one decode step
-    T.decode(qd, index, args.p, out=out)
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        T.decode(qd, index, args.p, out=out)
+    # ---- one CUDA graph per layer: one decode layer-step
+    for L in layers:
+        T.decode(L["q"], L["index"], args.p, out=L["out"])
+        torch.cuda.synchronize()
+        L["graph"] = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(L["graph"]):
+            T.decode(L["q"], L["index"], args.p, out=L["out"])
     torch.cuda.synchronize()
 
-    def timed_loop(fn, steps, flush_each=True):
+    def timed_loop(fns, steps, flush_each=True):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-        for a, b in evs:
+        for i, (a, b) in enumerate(evs):
             if flush_each:
-                l2.fill_(1)
+                l2_flush()
             a.record()
-            fn()
+            fns[i % len(fns)]()
             b.record()
         return evs
 
-    for _ in range(args.warmup):
-        l2.fill_(1)
-        g.replay()
+    replays = [L["graph"].replay for L in layers]
+    timed_loop(replays, args.warmup)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
-        evs = timed_loop(g.replay, args.steps)
+        evs = timed_loop(replays, args.steps)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         # keep the GPU busy a little longer for the clock sampler (not part of the number)
-        timed_loop(g.replay, min(args.steps, 200))
+        timed_loop(replays, min(args.steps, 200))
         torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     ms = float(np.mean(step_ms))
@@ -295,46 +322,54 @@ def run_gpu(args, rank, world, local_rank):
 
     # ---- per-stage breakdown (selection / attention / merge), events between stages
     st = []
-    for _ in range(max(20, min(args.steps, 200))):
-        l2.fill_(1)
+    for i in range(max(3 * LAYERS, min(args.steps, 200))):
+        L = layers[i % len(layers)]
+        l2_flush()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        T.decode_profiled(qd, index, args.p, ev, out=out)
+        T.decode_profiled(L["q"], L["index"], args.p, ev, out=L["out"])
         st.append(ev)
     torch.cuda.synchronize()
     sel_us = 1e3 * float(np.mean([e[0].elapsed_time(e[1]) for e in st]))
     att_us = 1e3 * float(np.mean([e[1].elapsed_time(e[2]) for e in st]))
     mrg_us = 1e3 * float(np.mean([e[2].elapsed_time(e[3]) for e in st]))
 
-    # ---- algorithmic bytes from the selection the GPU made
-    dbg = T.decode_debug(qd, index, args.p)
-    assert torch.equal(dbg["out"], out), "debug decode must reproduce the graph output"
-    bm = step_bytes(dbg, sizes, G, n, C)
+    # ---- algorithmic bytes from the selections the GPU made (mean over layers)
+    bms = []
+    for L in layers:
+        dbg = T.decode_debug(L["q"], L["index"], args.p)
+        assert torch.equal(dbg["out"], L["out"]), "debug decode must reproduce the graph output"
+        bms.append(step_bytes(dbg, L["sizes"], G, n, C))
+    bm = {k: float(np.mean([b[k] for b in bms])) for k in bms[0]}
+    bm["union_frac_per_layer"] = [round(b["union_frac"], 5) for b in bms]
 
-    # ---- dense baseline (own split-KV flash-decode over the caller's K/V)
-    dout = torch.empty_like(qd)
-    T.dense_decode(qd, Kd, Vd, out=dout)
-    gd = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(gd):
-        T.dense_decode(qd, Kd, Vd, out=dout)
-    for _ in range(3):
-        gd.replay()
+    # ---- dense baseline (own split-KV flash-decode over the caller's K/V), same layers
+    dgraphs = []
+    for L in layers:
+        L["dout"] = torch.empty_like(L["q"])
+        T.dense_decode(L["q"], L["K"], L["V"], out=L["dout"])
+        gd = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gd):
+            T.dense_decode(L["q"], L["K"], L["V"], out=L["dout"])
+        dgraphs.append(gd.replay)
+    timed_loop(dgraphs, 3 * LAYERS)
     torch.cuda.synchronize()
-    devs = timed_loop(gd.replay, max(10, min(args.steps, 100)))
+    devs = timed_loop(dgraphs, max(2 * LAYERS, min(args.steps, 100)))
     torch.cuda.synchronize()
     dense_ms = float(np.mean([a.elapsed_time(b) for a, b in devs]))
-    dense_bytes = 2 * index.units * n * 128 * 2 + 2 * index.units * G * 128 * 2
+    dense_bytes = 2 * units * n * 128 * 2 + 2 * units * G * 128 * 2
 
     # ---- e2e through the C ABI with host buffers (H2D q, D2H out inside the timed region)
-    q_host = qd.cpu().pin_memory()
-    o_host = torch.empty_like(q_host).pin_memory()
-    for _ in range(3):
-        T.decode_host(q_host, index, args.p, o_host)
+    for L in layers:
+        L["q_host"] = L["q"].cpu().pin_memory()
+        L["o_host"] = torch.empty_like(L["q_host"]).pin_memory()
+        T.decode_host(L["q_host"], L["index"], args.p, L["o_host"])
     e2e = []
-    for _ in range(max(10, min(args.steps, 200))):
-        l2.fill_(1)
+    for i in range(max(2 * LAYERS, min(args.steps, 200))):
+        L = layers[i % len(layers)]
+        l2_flush()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        T.decode_host(q_host, index, args.p, o_host)
+        T.decode_host(L["q_host"], L["index"], args.p, L["o_host"])
         b.record()
         torch.cuda.synchronize()
         e2e.append(a.elapsed_time(b))
@@ -343,6 +378,9 @@ def run_gpu(args, rank, world, local_rank):
         t = torch.tensor([e2e_ms, dense_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms, dense_ms = float(t[0]), float(t[1])
+    qd = layers[0]["q"]
+    index = layers[0]["index"]
+    build_ms = float(np.mean(build_ms))
 
     if rank != 0:
         return
@@ -363,8 +401,8 @@ def run_gpu(args, rank, world, local_rank):
         "metric": METRIC, "value": value_us, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": _config(args, world),
-        # per decode step: score, rank, sample, fit, attention (fused selection: 1 + attention)
-        "gpu_launches": (1 if args.p >= 1 else (2 if index.info()["select_cluster_size"] else 5)) * args.steps,
+        # per decode step: score+rank, sample, fit, attention (fused selection: 1 + attention)
+        "gpu_launches": (1 if args.p >= 1 else (2 if index.info()["select_cluster_size"] else 4)) * args.steps,
         "roofline": {"bound": "hbm", "kernel": "attention_kernel<4,false> (S8 sparse split-KV)",
                      "achieved": att_gbs, "peak": hbm, "unit": "GB/s", "frac": att_gbs / hbm,
                      "traffic": traffic, "peak_source": peak_src,
