@@ -48,7 +48,9 @@ struct __align__(16) StageMeta {
 
 constexpr int SCRATCH_FLOATS = ATT_CWARPS * (8 * 128 + 16);
 // unit-aligned split: the unit's work list (segment rows + token prefix) staged in smem
-constexpr int LIST_INTS = 2 * TACTIC_MAX_CLUSTERS + 4;
+// (or, when they fit, every unit's lists: one bulk copy of each array, no separate round
+// trip for the per-unit totals of the split)
+constexpr int LIST_INTS = 16400;
 constexpr size_t ATT_SMEM = (size_t)ATT_STAGES * ATT_STAGE_BYTES + ATT_STAGES * sizeof(StageMeta) +
                             3 * ATT_STAGES * sizeof(uint64_t) + SCRATCH_FLOATS * sizeof(float) +
                             LIST_INTS * sizeof(int) + 1024;
@@ -117,11 +119,11 @@ __device__ __forceinline__ long long floor_div(long long x, long long y) {
 }
 
 template <bool DENSE>
-__device__ __forceinline__ UnitSplit unit_split_of(const AttnArgs& a, int cta, int P) {
+__device__ __forceinline__ UnitSplit unit_split_of(const AttnArgs& a, int cta, int P, const int* pref) {
   const int U = a.units, lane = threadIdx.x & 31;
   auto tok = [&](int v) -> long long {
     if (v >= U) return 0;
-    return DENSE ? (long long)a.n : (long long)__ldcg(a.seg_prefix + (size_t)v * (a.C + 1) + a.C);
+    return DENSE ? (long long)a.n : (long long)pref[(size_t)v * (a.C + 1) + a.C];
   };
   long long T = 0;
   for (int v0 = 0; v0 < U; v0 += 32) T += tok(v0 + lane);
@@ -196,6 +198,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       mbar_init(&empty[i], ATT_CWARPS);
     }
     mbar_init(mbar, 1);
+    mbar_init(mbar + 1, 1);
     fence_barrier_init();
   }
   fence_proxy_async_smem();
@@ -227,15 +230,31 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   // unit-aligned split: CTA cta works on one unit only (see UnitSplit); otherwise the
   // global token range split (needs unit_prefix)
   const bool unit_mode = a.unit_split != 0;
+  // every unit's work list in smem (sparse, unit-aligned split, when it fits): rows then
+  // prefixes, two bulk copies of 16-byte multiples (the arrays carry 4 ints of padding)
+  const size_t rows_n = (size_t)a.units * a.C, pref_n = (size_t)a.units * (a.C + 1);
+  const size_t rows_pad = (rows_n + 3) & ~(size_t)3, pref_pad = (pref_n + 3) & ~(size_t)3;
+  const bool all_lists = !DENSE && unit_mode && rows_pad + pref_pad <= (size_t)LIST_INTS;
+  const int* pref_src = a.seg_prefix;
+  if (all_lists) {
+    if (threadIdx.x == 0) {
+      fence_proxy_async_global();
+      mbar_arrive_expect_tx(mbar + 1, (uint32_t)((rows_pad + pref_pad) * 4));
+      bulk_g2s(s_list, a.seg_row, (uint32_t)(rows_pad * 4), mbar + 1);
+      bulk_g2s(s_list + rows_pad, a.seg_prefix, (uint32_t)(pref_pad * 4), mbar + 1);
+    }
+    mbar_wait(mbar + 1, 0);
+    pref_src = s_list + rows_pad;
+  }
   UnitSplit us_ = {0, 0, 1, 0, 0};
-  if (unit_mode) us_ = unit_split_of<DENSE>(a, cta, P);
+  if (unit_mode) us_ = unit_split_of<DENSE>(a, cta, P, pref_src);
   if (threadIdx.x == 0) stamp(40);
   const long long T = unit_mode ? 0 : (DENSE ? dense_total : a.unit_prefix[a.units]);
   // unit-aligned sparse split: the CTA's unit's whole work list into smem with one round
   // trip of independent loads (all threads), so the producer's segment search and run
   // walk never wait on L2
   const bool list_smem = !DENSE && unit_mode;
-  if (list_smem) {
+  if (list_smem && !all_lists) {
     const int* gr = a.seg_row + (size_t)us_.u * a.C;
     const int* gp = a.seg_prefix + (size_t)us_.u * (a.C + 1);
     constexpr int PER = 16;  // independent loads in flight per thread (2 C + 1 <= 2560: one batch)
@@ -298,8 +317,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         break;
       }
       // sparse: run table window of 32 segments (lane i holds segment k0 + i)
-      const int* seg_row = list_smem ? s_list : a.seg_row + (size_t)u * a.C;
-      const int* seg_pref = list_smem ? s_list + a.C : a.seg_prefix + (size_t)u * (a.C + 1);
+      const int* seg_row = all_lists ? s_list + (size_t)u * a.C
+                           : list_smem ? s_list : a.seg_row + (size_t)u * a.C;
+      const int* seg_pref = all_lists ? s_list + rows_pad + (size_t)u * (a.C + 1)
+                            : list_smem ? s_list + a.C : a.seg_prefix + (size_t)u * (a.C + 1);
       int k = 0, k0 = 0, row = 0, left = 0, w_row = 0, w_end = 0;
       if (!DENSE) {
         if (leader) stamp(43);

@@ -89,6 +89,11 @@ __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
   asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
   return r;
 }
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int r;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+  return r;
+}
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -111,6 +116,10 @@ __device__ __forceinline__ void tma_load_4d(void* dst_smem, const void* tmap, in
       "%5}], [%6];" ::"r"(smem_u32(dst_smem)),
       "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
+}
+// 1-D bulk prefetch global -> L2 (no completion, no smem); 16-byte aligned, multiple of 16
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");

@@ -108,6 +108,7 @@ struct tactic_index_s {
 
 namespace tactic {
 
+
 // ---- attention (attention.cu)
 struct AttnArgs {
   const __nv_bfloat16* q;          // [units][G][128]

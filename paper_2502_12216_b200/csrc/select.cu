@@ -470,34 +470,42 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
   if (tid == 0) tl_mark(P.tlog, 3, 0, u == 0);
   // index data (not produced by the previous kernels): before the dependency wait
   for (int i = tid; i <= C; i += nt) s_off[i] = P.offsets[(size_t)u * (C + 1) + i];
-  __shared__ uint64_t sbar;
+  __shared__ uint64_t sbar, obar;
   const size_t ub = (size_t)u * G;
   const bool bulk_ok = ((ub * C) % 4 == 0) && (((size_t)G * C) % 4 == 0);
   if (tid == 0) {
     mbar_init(&sbar, 1);
+    mbar_init(&obar, 1);
     fence_barrier_init();
   }
   for (int i = tid; i < C; i += nt) mask[i] = 0;
+  __syncthreads();
+  // The unit's order / end ranks (score_rank) are complete before the dependency wait:
+  // this grid starts only after the sample kernel passed ITS wait on score_rank.  Stage
+  // them now; only the sample kernel's summaries remain for after the wait.
+  if (tid == 0 && bulk_ok) {
+    const uint32_t be = (uint32_t)G * C * 4;
+    mbar_arrive_expect_tx(&obar, 2 * be);
+    bulk_g2s(s_end, P.ends + ub * C, be, &obar);
+    bulk_g2s(s_ord, P.order + ub * C, be, &obar);
+  }
+  if (!bulk_ok)
+    for (int i = tid; i < G * C; i += nt) {
+      s_end[i] = P.ends[ub * C + i];
+      s_ord[i] = P.order[ub * C + i];
+    }
+  if (bulk_ok) mbar_wait(&obar, 0);
   __syncthreads();
   {
     pdl_wait();
     stamp(1);
     if (tid == 0) tl_mark(P.tlog, 3, 1, u == 0);
-    // stage the previous kernels' outputs with 1-D bulk copies (one round trip)
+    // stage the sample kernel's summaries (one round trip)
     if (tid == 0) {
-      const uint32_t bs = (uint32_t)G * nb * 16, be = bulk_ok ? (uint32_t)G * C * 4 : 0u;
-      mbar_arrive_expect_tx(&sbar, bs + 2 * be);
+      const uint32_t bs = (uint32_t)G * nb * 16;
+      mbar_arrive_expect_tx(&sbar, bs);
       bulk_g2s(sm, P.summ + ub * nb * 4, bs, &sbar);
-      if (bulk_ok) {
-        bulk_g2s(s_end, P.ends + ub * C, be, &sbar);
-        bulk_g2s(s_ord, P.order + ub * C, be, &sbar);
-      }
     }
-    if (!bulk_ok)
-      for (int i = tid; i < G * C; i += nt) {
-        s_end[i] = P.ends[ub * C + i];
-        s_ord[i] = P.order[ub * C + i];
-      }
     mbar_wait(&sbar, 0);
     __syncthreads();
     stamp(2);

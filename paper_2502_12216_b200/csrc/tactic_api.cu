@@ -185,8 +185,8 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_
   x->cumend = A.get<double>(U * G * C);
   x->J = A.get<int>(U * G);
   x->umask = A.get<uint8_t>(U * C);
-  x->union_list = A.get<int>(U * C);
-  x->union_prefix = A.get<int>(U * (C + 1));
+  x->union_list = A.get<int>(U * C + 4);          // +4: 16-byte bulk reads of the whole list
+  x->union_prefix = A.get<int>(U * (C + 1) + 4);
   x->unit_prefix = A.get<long long>(U + 1);
   x->counter = A.get<unsigned int>(1);
   x->part_o = A.get<float>((x->num_ctas + U) * G * 128);
@@ -221,6 +221,9 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_
   cudaMemset(x->unit_cnt, 0, U * sizeof(int));
   cudaMemset(x->mask_acc, 0, U * C);
   cudaMemset(x->head_cnt, 0, U * sizeof(unsigned int));
+  cudaMemset(x->order, 0, U * G * C * sizeof(int));  // valid cluster ids before the first decode
+
+  cudaMemset(x->ends, 0, U * G * C * sizeof(int));
   std::vector<long long> up(U + 1);
   for (size_t u = 0; u <= U; ++u) up[u] = (long long)u * (long long)n;
   cudaMemcpy(x->all_unit_prefix, up.data(), (U + 1) * sizeof(long long), cudaMemcpyHostToDevice);

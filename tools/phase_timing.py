@@ -61,7 +61,17 @@ for it in range(4):
             names = ["centroids in", "scored", "sorted", "pushed", "runs in", "ranked", "rowmap"]
             print("  rank CTA(0,0) phases (us after its wait): " +
                   "  ".join(f"{nm} {(rk[i] - tl[1, 1]) / 1e3:.2f}" for i, nm in enumerate(names)))
-    if R == 0:
+    if R == 0 and full[256] > 0 and full[256 + 6] == 0:
+        fs = full[256:256 + 6]
+        z = tl[:, 0][tl[:, 0] > 0].min()
+        names = ["head0 last chunk", "staged", "fitted", "marked", "unit0 compact start", "unit0 compact end"]
+        print("  sample_fit (us from first start): " + "  ".join(f"{nm} {(fs[i] - z) / 1e3:6.2f}" for i, nm in enumerate(names)
+                                                              if fs[i] > 0))
+        cs = full[264:268]
+        print("  compaction (us from first start): " + "  ".join(f"{nm} {(cs[i] - z) / 1e3:6.2f}" for i, nm in
+              enumerate(["pass1", "scan", "pass2", "fill"]) if cs[i] > 0))
+        t0 = z
+    elif R == 0:
         fs = full[256:256 + 7]
         t0 = fs[0]
         names = ["start", "pdl_wait", "staged", "heads fitted", "compacted", "last-unit start", "last-unit end"]
