@@ -382,6 +382,35 @@ def run_gpu(args, rank, world, local_rank):
     index = layers[0]["index"]
     build_ms = float(np.mean(build_ms))
 
+    # ---- target-fraction sweep (BASELINE.json configs[4], C5): same layers, graph per (p,
+    # layer), device-timed like the headline, plus the union fraction the GPU selected
+    sweep = []
+    if args.sweep and world == 1:
+        for p in (0.5, 0.8, 0.9, 0.95, 0.99, 1.0):
+            reps = []
+            for L in layers:
+                o = torch.empty_like(L["q"])
+                T.decode(L["q"], L["index"], p, out=o)
+                gp = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gp):
+                    T.decode(L["q"], L["index"], p, out=o)
+                reps.append(gp.replay)
+            timed_loop(reps, 2 * LAYERS)
+            torch.cuda.synchronize()
+            ev = timed_loop(reps, max(4 * LAYERS, min(args.steps, 96)))
+            torch.cuda.synchronize()
+            us = 1e3 * float(np.mean([a.elapsed_time(b) for a, b in ev]))
+            uf = []
+            for L in layers:
+                if p >= 1.0:
+                    uf.append(float((L["sizes"] > 0).sum() and 1.0))
+                else:
+                    dbg = T.decode_debug(L["q"], L["index"], p)
+                    uf.append(sum(int(L["sizes"][u][dbg["union_mask"][u].astype(bool)].sum())
+                                  for u in range(units)) / (units * n))
+            sweep.append({"p": p, "us_per_layer_step": us, "speedup_vs_dense": dense_ms * 1e3 / us,
+                          "union_frac": float(np.mean(uf))})
+
     if rank != 0:
         return
     peaks = _peaks()
@@ -413,6 +442,7 @@ def run_gpu(args, rank, world, local_rank):
         "dense": {"us_per_layer_step": dense_ms * 1e3, "gbs": dense_bytes / (dense_ms * 1e-3) / 1e9,
                   "frac": dense_bytes / (dense_ms * 1e-3) / 1e9 / hbm, "bytes": dense_bytes},
         "speedup_vs_dense": dense_ms / ms,
+        "p_sweep": sweep or None,
         "select_cluster_size": index.info()["select_cluster_size"],
         "build": {"ms": build_ms, "iters_run": iters_run, "alg_tflop": alg_tflop,
                   "alg_tflops": alg_tflop / (build_ms * 1e-3),
@@ -435,6 +465,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--p", type=float, default=0.9)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", type=int, default=1, help="1: add the C5 target-fraction sweep (p_sweep)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
