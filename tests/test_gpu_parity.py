@@ -381,3 +381,49 @@ def test_fused_matches_multikernel_path(T, monkeypatch):
         # fit values equal to ~1e-5 relative (b ~ 0 compared absolutely)
         np.testing.assert_allclose(a["fit"], b["fit"], rtol=1e-4, atol=1e-7)
         assert torch.allclose(a["out"].float(), b["out"].float(), atol=1e-2)
+
+
+# ----------------------------------------------------------------------------- attention work-split modes
+@pytest.mark.parametrize("B,H,n,C", [(12, 8, 2048, 32),    # 96 units > CTAs/2: global token split,
+                                     (64, 8, 1024, 16)])   # C3-like unit count (512 units)
+def test_global_split_many_units(T, B, H, n, C):
+    """More units than half the CTAs (BASELINE configs[2] shape class: batch x KV heads):
+    the fit kernel's last unit writes the token prefix over units and the attention
+    kernel cuts one global token list (a CTA may hold pieces of two units)."""
+    G = 4
+    K, V, q = _layer(B, H, G, n, 500 + B)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, B)
+    index = _import(T, K, V, cents, asg, G)
+    units = B * H
+    res = T.decode_debug(dev_bf16(q), index, 0.9)
+    got = res["out"].float().cpu().numpy()
+    for u in sorted({0, 1, units // 3, units // 2, units - 2, units - 1}):
+        b, h = divmod(u, H)
+        qo = q[b, h * G:(h + 1) * G]
+        ro = O.decode_unit(qo, idxs[u], 0.9)
+        _check_unit_selection(res, u, G, ro["heads"], 0.9, C)
+        toks = O.cluster_tokens(idxs[u], np.nonzero(res["union_mask"][u])[0])
+        o, _ = O.sparse_attention(qo, idxs[u].K, idxs[u].V, toks)
+        assert_output_close(got[b, h * G:(h + 1) * G], o, f"units={units} u={u}")
+
+
+def test_unit_split_per_unit_list_fallback(T):
+    """Unit-aligned split whose units' work lists do not all fit the attention kernel's
+    shared-memory list area (8 units x C = 2048): the CTA stages its own unit's list."""
+    G, n, C = 4, 16384, 2048
+    K, V, q = _layer(1, 8, G, n, 901)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 2, 901)
+    index = _import(T, K, V, cents, asg, G)
+    for p in (0.9, 1.0):
+        res = T.decode_debug(dev_bf16(q), index, p)
+        got = res["out"].float().cpu().numpy()
+        for u in (0, 3, 7):
+            qo = q[0, u * G:(u + 1) * G]
+            if p < 1.0:
+                ro = O.decode_unit(qo, idxs[u], p)
+                _check_unit_selection(res, u, G, ro["heads"], p, C)
+                toks = O.cluster_tokens(idxs[u], np.nonzero(res["union_mask"][u])[0])
+                o, _ = O.sparse_attention(qo, idxs[u].K, idxs[u].V, toks)
+            else:
+                o, _ = O.full_attention(qo, K[0, u], V[0, u])
+            assert_output_close(got[0, u * G:(u + 1) * G], o, f"C={C} p={p} u={u}")

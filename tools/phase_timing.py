@@ -116,3 +116,6 @@ for it in range(4):
             print("   tiles per CTA: min %d median %d max %d" % (nt_.min(), np.median(nt_), nt_.max()))
             mg = full[964:964 + 16].reshape(8, 2)
             print("   merges (start, end) us:", [(round((s - b0) / 1e3, 2), round((e - b0) / 1e3, 2)) for s, e in mg if s > 0])
+            cp = full[980:988]
+            npc = full[990:998]
+            print("   merge staged at / pieces:", [(round((c - b0) / 1e3, 2), int(k)) for c, k in zip(cp, npc) if c > 0])
