@@ -211,31 +211,83 @@ def cpu_baseline(args, budget_s=12.0):
 # ------------------------------------------------------------------ GPU arm
 def _unit_bits(job):
     from synth import bf16_bits, make_unit
-    seed, h = job
-    u = make_unit(CFG["n"], CFG["G"], seed=seed, b=0, h=h)
-    return seed, h, bf16_bits(u["K"]), bf16_bits(u["V"]), bf16_bits(u["q"])
+    seed, b, h, n, G = job
+    u = make_unit(n, G, seed=seed, b=b, h=h)
+    return seed, b, h, bf16_bits(u["K"]), bf16_bits(u["V"]), bf16_bits(u["q"])
 
 
-def make_layers(seeds, dev):
-    """The synthetic layers (one per seed) as bf16 device tensors, generated in parallel
-    on the host cores (input generation only; synth/ holds no method arithmetic)."""
+def make_layers(seeds, dev, B=1, Hkv=None, n=None):
+    """The synthetic layers (one per seed) as bf16 device tensors [B][Hkv][n][128],
+    generated in parallel on the host cores (input generation only; synth/ holds no
+    method arithmetic)."""
     import multiprocessing as mp
 
     import torch
-    Hkv, G, n = CFG["Hkv"], CFG["G"], CFG["n"]
+    Hkv = Hkv or CFG["Hkv"]
+    n = n or CFG["n"]
+    G = CFG["G"]
     bf = lambda a: torch.from_numpy(a.view(np.int16)).to(dev).view(torch.bfloat16)  # noqa: E731
-    layers = {sd: {"K": torch.empty((1, Hkv, n, 128), dtype=torch.bfloat16, device=dev),
-                   "V": torch.empty((1, Hkv, n, 128), dtype=torch.bfloat16, device=dev),
-                   "q": torch.empty((1, Hkv * G, 128), dtype=torch.bfloat16, device=dev)} for sd in seeds}
-    jobs = [(sd, h) for sd in seeds for h in range(Hkv)]
+    layers = {sd: {"K": torch.empty((B, Hkv, n, 128), dtype=torch.bfloat16, device=dev),
+                   "V": torch.empty((B, Hkv, n, 128), dtype=torch.bfloat16, device=dev),
+                   "q": torch.empty((B, Hkv * G, 128), dtype=torch.bfloat16, device=dev)} for sd in seeds}
+    jobs = [(sd, b, h, n, G) for sd in seeds for b in range(B) for h in range(Hkv)]
     workers = max(1, min(len(jobs), len(os.sched_getaffinity(0)) - 1, 32))
     with mp.get_context("fork").Pool(workers) as pool:
-        for sd, h, kb, vb, qb in pool.imap_unordered(_unit_bits, jobs):
+        for sd, b, h, kb, vb, qb in pool.imap_unordered(_unit_bits, jobs, chunksize=4):
             L = layers[sd]
-            L["K"][0, h] = bf(kb)
-            L["V"][0, h] = bf(vb)
-            L["q"][0, h * G:(h + 1) * G] = bf(qb)
+            L["K"][b, h] = bf(kb)
+            L["V"][b, h] = bf(vb)
+            L["q"][b, h * G:(h + 1) * G] = bf(qb)
     return [layers[sd] for sd in seeds]
+
+
+C3 = dict(B=64, Hkv=8, n=32768, C=256, iters=10)
+
+
+def measure_c3(T, dev, p, steps, timed_loop):
+    """BASELINE.json configs[2] on this GPU: Llama-3-8B layer, 32K context, batch 64
+    (512 units, 256 clusters each): decode layer-step vs the own dense decode (the global
+    token split of the attention kernel: more units than half the CTAs)."""
+    import torch
+    L = make_layers([9000], dev, B=C3["B"], Hkv=C3["Hkv"], n=C3["n"])[0]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    idx = T.build_index(L["K"], L["V"], C3["C"], C3["iters"], group_size=CFG["G"], seed=9000)
+    e1.record()
+    torch.cuda.synchronize()
+    build_ms = e0.elapsed_time(e1)
+    ex = idx.export()
+    units = idx.units
+    sizes = np.stack([np.bincount(ex["assign"][u], minlength=C3["C"]) for u in range(units)])
+    out = torch.empty_like(L["q"])
+    T.decode(L["q"], idx, p, out=out)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        T.decode(L["q"], idx, p, out=out)
+    dout = torch.empty_like(L["q"])
+    T.dense_decode(L["q"], L["K"], L["V"], out=dout)
+    gd = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gd):
+        T.dense_decode(L["q"], L["K"], L["V"], out=dout)
+    k = max(10, min(steps, 50))
+    timed_loop([g.replay], 3)
+    ev = timed_loop([g.replay], k)
+    torch.cuda.synchronize()
+    us = 1e3 * float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    timed_loop([gd.replay], 3)
+    ev = timed_loop([gd.replay], k)
+    torch.cuda.synchronize()
+    dus = 1e3 * float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    dbg = T.decode_debug(L["q"], idx, p)
+    uf = sum(int(sizes[u][dbg["union_mask"][u].astype(bool)].sum()) for u in range(units)) / (units * C3["n"])
+    dense_bytes = 2 * units * C3["n"] * 256
+    res = {"workload": "C3: Llama-3-8B layer, 32K context, batch 64 (512 units), 256 clusters/KV head, "
+                       f"p={p}, 1 GPU", "us_per_layer_step": us, "dense_us_per_layer_step": dus,
+           "speedup_vs_dense": dus / us, "union_frac": uf, "dense_gbs": dense_bytes / (dus * 1e-6) / 1e9,
+           "build_ms": build_ms}
+    del L, idx
+    torch.cuda.empty_cache()
+    return res
 
 
 def run_gpu(args, rank, world, local_rank):
@@ -381,6 +433,7 @@ def run_gpu(args, rank, world, local_rank):
     qd = layers[0]["q"]
     index = layers[0]["index"]
     build_ms = float(np.mean(build_ms))
+    c3 = measure_c3(T, dev, args.p, args.steps, timed_loop) if (args.c3 and world == 1) else None
 
     # ---- target-fraction sweep (BASELINE.json configs[4], C5): same layers, graph per (p,
     # layer), device-timed like the headline, plus the union fraction the GPU selected
@@ -443,6 +496,7 @@ def run_gpu(args, rank, world, local_rank):
                   "frac": dense_bytes / (dense_ms * 1e-3) / 1e9 / hbm, "bytes": dense_bytes},
         "speedup_vs_dense": dense_ms / ms,
         "p_sweep": sweep or None,
+        "c3": c3,
         "select_cluster_size": index.info()["select_cluster_size"],
         "build": {"ms": build_ms, "iters_run": iters_run, "alg_tflop": alg_tflop,
                   "alg_tflops": alg_tflop / (build_ms * 1e-3),
@@ -466,6 +520,7 @@ def main():
     ap.add_argument("--p", type=float, default=0.9)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sweep", type=int, default=1, help="1: add the C5 target-fraction sweep (p_sweep)")
+    ap.add_argument("--c3", type=int, default=1, help="1: add the C3 batch-64 32K measurement (configs[2])")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
