@@ -36,6 +36,8 @@ extern "C" {
 #define TACTIC_MAX_SEQ_LEN 1048576    /* per unit (exact-head prefix of Alg. 1 kept in smem) */
 #define TACTIC_SHARD_GRID_T 512       /* sequence-sharded mode: criticality grid points   */
 #define TACTIC_SHARD_GRID_STEP 0.0625 /* grid step in logit units (1/16), reading 23      */
+#define TACTIC_TAIL_CAPACITY 2048     /* default recent-token tail per unit (re-cluster
+                                         every 2048 generated tokens)                      */
 
 typedef enum {
   TACTIC_OK = 0,
@@ -208,6 +210,33 @@ tactic_status_t tactic_decode_stage1b(tactic_index_t idx, const double* global_m
 tactic_status_t tactic_decode_stage2(const void* q, tactic_index_t idx, float p,
                                      const double* global_max, const double* global_mass,
                                      float* o_part, float* lse_part, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Multi-step generation.  P:112 (§1): Tactic "performs full
+ * attention on newly generated tokens" and re-clusters periodically ("every ... 2048
+ * tokens").  Tokens generated after the build are appended to a per-unit dense tail
+ * that every later decode attends in full, after the selected clusters (the selection
+ * S1-S7 still ranks only the clustered tokens; with p >= 1 the decode equals full
+ * attention over the n + tail tokens).  When the tail is full the caller re-clusters:
+ * builds a new index over the clustered + tail tokens (the Python DecodeSession policy).
+ *
+ * tactic_set_tail_capacity: (re)allocates room for `capacity` tail tokens per unit;
+ *   only while the tail is empty (else INVALID_ARGUMENT).  0 frees it.  Not capturable.
+ * tactic_append: appends t >= 0 tokens per unit.  k_new, v_new device bf16 [units][t][128]
+ *   (unit u = b * Hkv + h, as for q).  Allocates the default capacity
+ *   (TACTIC_TAIL_CAPACITY) on first use; SHAPE if the tail would overflow.  Decodes
+ *   enqueued after it on the same stream see the tokens.  A CUDA graph captured before an
+ *   append keeps the tail length of its capture: re-capture after appending.
+ * tactic_index_tail: host outputs (nullable) tail length / capacity.
+ * tactic_assign_tokens: SPEC assign_token: for t new keys per unit
+ *   (device bf16 [units][t][128]) the nearest centroid by squared Euclidean distance in
+ *   float64, ties to the lowest id (readings 4, 7); device int32 [units][t].          */
+tactic_status_t tactic_set_tail_capacity(tactic_index_t idx, int32_t capacity);
+tactic_status_t tactic_append(tactic_index_t idx, const void* k_new, const void* v_new, int32_t t,
+                              void* stream);
+tactic_status_t tactic_index_tail(tactic_index_t idx, int32_t* len, int32_t* capacity);
+tactic_status_t tactic_assign_tokens(tactic_index_t idx, const void* k, int32_t t, int32_t* assign,
+                                     void* stream);
 
 /* ---------------------------------------------------------------------------------------
  * Misc. */

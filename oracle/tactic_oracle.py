@@ -323,6 +323,33 @@ def decode_unit(q: np.ndarray, idx: Index, p: float) -> dict:
 
 
 # ---------------------------------------------------------------------------
+# Multi-step generation.  P:112 (§1): "performs full
+# attention on newly generated tokens" and updates the clustering periodically;
+# SPEC assign_token.
+# ---------------------------------------------------------------------------
+def assign_tokens(K_new: np.ndarray, centroids: np.ndarray) -> np.ndarray:
+    """Nearest centroid of each new key: argmin_j |k - c_j|^2 (reading 4), ties to
+    the lowest id (reading 7); float64."""
+    a, _ = _sq_dist_argmin(np.asarray(K_new, dtype=np.float64), np.asarray(centroids, dtype=np.float64))
+    return a
+
+
+def decode_unit_with_tail(q: np.ndarray, idx: Index, p: float, K_tail: np.ndarray, V_tail: np.ndarray) -> dict:
+    """decode_unit's selection over the clustered tokens (O5-O11 unchanged); every head
+    then attends the union U plus the whole dense tail of appended tokens (O12 over
+    U-tokens + tail)."""
+    r = decode_unit(q, idx, p)
+    K_tail = np.asarray(K_tail, dtype=np.float64).reshape(-1, idx.K.shape[1])
+    V_tail = np.asarray(V_tail, dtype=np.float64).reshape(-1, idx.V.shape[1])
+    K_all = np.concatenate([np.asarray(idx.K, dtype=np.float64), K_tail])
+    V_all = np.concatenate([np.asarray(idx.V, dtype=np.float64), V_tail])
+    toks = np.concatenate([r["tokens"], idx.n + np.arange(K_tail.shape[0])])
+    o, lse = sparse_attention(np.atleast_2d(np.asarray(q, dtype=np.float64)), K_all, V_all, toks)
+    r.update(o=o, lse=lse, tokens=toks)
+    return r
+
+
+# ---------------------------------------------------------------------------
 # Diagnostics (Eq. 4-6, Table 1 methodology) -- test/diagnostic only.
 # ---------------------------------------------------------------------------
 def exact_scores(q_g, K) -> np.ndarray:

@@ -123,7 +123,7 @@ __device__ __forceinline__ UnitSplit unit_split_of(const AttnArgs& a, int cta, i
   const int U = a.units, lane = threadIdx.x & 31;
   auto tok = [&](int v) -> long long {
     if (v >= U) return 0;
-    return DENSE ? (long long)a.n : (long long)pref[(size_t)v * (a.C + 1) + a.C];
+    return DENSE ? (long long)a.n : (long long)pref[(size_t)v * (a.C + 1) + a.C] + a.tail_len;
   };
   long long T = 0;
   for (int v0 = 0; v0 < U; v0 += 32) T += tok(v0 + lane);
@@ -279,6 +279,23 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   if (warp == 0) {
     // ============================ producer (warp-uniform control flow) ============================
     const bool leader = lane == 0;
+    // one run of consecutive layout rows into stage slots [slot, slot + len): the index
+    // layout (rows < n) or the recent-token tail (rows n..)
+    auto issue_run = [&](uint8_t* sK, uint8_t* sV, int slot, int row, int len, int u, uint64_t* bar) {
+      const uint8_t* kb;
+      const uint8_t* vb;
+      if (row >= a.n) {
+        const size_t o = ((size_t)u * a.tail_cap + (row - a.n)) * 256;
+        kb = (const uint8_t*)a.Kt + o;
+        vb = (const uint8_t*)a.Vt + o;
+      } else {
+        const size_t o = ((size_t)u * a.n + row) * 256;
+        kb = (const uint8_t*)a.Kp + o;
+        vb = (const uint8_t*)a.Vp + o;
+      }
+      bulk_g2s(sK + slot * 256, kb, (uint32_t)len * 256u, bar);
+      bulk_g2s(sV + slot * 256, vb, (uint32_t)len * 256u, bar);
+    };
     long long t = unit_mode ? 0 : range_start(cta, T, P);
     const long long t_end = unit_mode ? 0 : range_start(cta + 1, T, P);
     int stage = 0;
@@ -322,7 +339,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       const int* seg_pref = all_lists ? s_list + rows_pad + (size_t)u * (a.C + 1)
                             : list_smem ? s_list + a.C : a.seg_prefix + (size_t)u * (a.C + 1);
       int k = 0, k0 = 0, row = 0, left = 0, w_row = 0, w_end = 0;
-      if (!DENSE) {
+      // the unit's list tokens; tokens past them are the recent-token tail (rows n..)
+      const int ltot = DENSE ? 0 : seg_pref[a.C];
+      if (!DENSE && lt >= ltot) {
+        row = a.n + (lt - ltot);
+        left = ltot + a.tail_len - lt;
+      } else if (!DENSE) {
         if (leader) stamp(43);
         k = k0 = warp_floor_search<int>(seg_pref, a.C, lt);  // largest k with seg_pref[k] <= lt
         w_row = (k0 + lane < a.C) ? seg_row[k0 + lane] : 0;
@@ -357,21 +379,16 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           uint32_t bytes = 0;
           int s = 0;
           int r_slot = -1, r_row = 0, r_len = 0;  // pending run (merged while contiguous)
-          const size_t ubytes = (size_t)u * a.n * 256;
+          (void)0;
           while (s < ATT_TILE && lt < le) {
             const int avail = left < (le - lt) ? left : (le - lt);
             const int s0 = s + ((row - s) & 7);
             if (s0 >= ATT_TILE) break;
             const int L = avail < (ATT_TILE - s0) ? avail : (ATT_TILE - s0);
-            if (r_slot >= 0 && r_slot + r_len == s0 && r_row + r_len == row) {
+            if (r_slot >= 0 && r_slot + r_len == s0 && r_row + r_len == row && (r_row >= a.n) == (row >= a.n)) {
               r_len += L;
             } else {
-              if (r_slot >= 0 && leader) {
-                bulk_g2s(sK + r_slot * 256, (const uint8_t*)a.Kp + ubytes + (size_t)r_row * 256, r_len * 256u,
-                         &full[stage]);
-                bulk_g2s(sV + r_slot * 256, (const uint8_t*)a.Vp + ubytes + (size_t)r_row * 256, r_len * 256u,
-                         &full[stage]);
-              }
+              if (r_slot >= 0 && leader) issue_run(sK, sV, r_slot, r_row, r_len, u, &full[stage]);
               r_slot = s0; r_row = row; r_len = L;
             }
             mask |= (L == 64 ? ~0ull : ((1ull << L) - 1ull)) << s0;
@@ -380,7 +397,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             row += L;
             lt += L;
             left -= L;
-            if (left == 0 && lt < le) {
+            if (left == 0 && lt < le && lt >= ltot) {  // into the tail
+              row = a.n + (lt - ltot);
+              left = ltot + a.tail_len - lt;
+            } else if (left == 0 && lt < le) {
               ++k;
               if (k - k0 == 32) {
                 k0 = k;
@@ -392,10 +412,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             }
           }
           if (leader) {
-            bulk_g2s(sK + r_slot * 256, (const uint8_t*)a.Kp + ubytes + (size_t)r_row * 256, r_len * 256u,
-                     &full[stage]);
-            bulk_g2s(sV + r_slot * 256, (const uint8_t*)a.Vp + ubytes + (size_t)r_row * 256, r_len * 256u,
-                     &full[stage]);
+            issue_run(sK, sV, r_slot, r_row, r_len, u, &full[stage]);
             meta[stage].mask = mask;
             meta[stage].unit = u;
             meta[stage].flags = (first ? FLAG_FIRST : 0) | (lt >= le ? FLAG_LAST : 0);

@@ -78,6 +78,12 @@ struct tactic_index_s {
   int* unit_cnt = nullptr;       // [units] attention arrival counters
   int* all_prefix = nullptr;     // [units][C+1]
   long long* all_unit_prefix = nullptr;  // [units+1]
+  // recent-token tail: tokens appended after the build,
+  // attended in full by every decode; rows n .. n+tail_len-1 of each unit, stored in
+  // separate [units][tail_cap][128] buffers with the same row swizzle as Kp/Vp
+  __nv_bfloat16* Kt = nullptr;
+  __nv_bfloat16* Vt = nullptr;
+  int tail_len = 0, tail_cap = 0;
   // decode workspace
   double* crit = nullptr;        // [units][G][C]
   int* order = nullptr;          // [units][G][C]
@@ -126,6 +132,11 @@ struct AttnArgs {
   float* lse;                      // nullable [units][G]
   unsigned long long* tlog;        // nullable debug timestamps (CTA 0)
   int unit_split;                  // 1: unit-aligned split from seg_prefix totals (units <= CTAs/2)
+  // recent-token tail (sparse): tail_len tokens per unit after each unit's work list,
+  // rows n.. of Kt/Vt ([units][tail_cap][128])
+  const __nv_bfloat16* Kt;
+  const __nv_bfloat16* Vt;
+  int tail_len, tail_cap;
 };
 cudaError_t launch_attention_sparse(const AttnArgs& a, int G, int num_ctas, cudaStream_t s, bool pdl);
 cudaError_t launch_attention_dense(const AttnArgs& a, const CUtensorMap* tmK, const CUtensorMap* tmV, int G,
@@ -133,6 +144,12 @@ cudaError_t launch_attention_dense(const AttnArgs& a, const CUtensorMap* tmK, co
 cudaError_t launch_lse_merge_plain(const float* o_parts, const float* lse_parts, int n_parts, int n_rows,
                                    __nv_bfloat16* out, float* lse, cudaStream_t s);
 size_t attention_smem_bytes();
+
+// ---- recent-token tail and new-token assignment (tail.cu)
+cudaError_t launch_tail_append(const __nv_bfloat16* k_new, const __nv_bfloat16* v_new, int t, tactic_index_s* x,
+                               cudaStream_t s);
+cudaError_t launch_assign(const __nv_bfloat16* k, int t, const tactic_index_s* x, int* assign, cudaStream_t s);
+cudaError_t launch_unit_prefix_fill(long long* up, int units, long long per_unit, cudaStream_t s);
 
 // ---- selection (select.cu)
 struct SelArgs {

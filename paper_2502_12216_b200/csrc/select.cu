@@ -356,6 +356,7 @@ struct FitParams {
   unsigned int* unit_cnt;
   unsigned long long* tlog;  // nullable debug stamps
   int need_unit_prefix;      // global attention split (units > CTAs/2): compute unit_prefix
+  int tail_len;              // recent-token tail per unit (counted in unit_prefix)
 };
 
 // ------------------------------------------------------------------ S5-S7, one CTA per unit
@@ -693,12 +694,12 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
     const int per = (units + nt - 1) / nt;
     const int b0 = tid * per;
     long long loc = 0;
-    for (int v = b0; v < b0 + per && v < units; ++v) loc += __ldcg(P.uprefix + (size_t)v * (C + 1) + C);
+    for (int v = b0; v < b0 + per && v < units; ++v) loc += __ldcg(P.uprefix + (size_t)v * (C + 1) + C) + P.tail_len;
     __shared__ long long s_tot;  // block_exclusive_scan writes the total from one thread
     long long run = block_exclusive_scan<long long>(loc, (long long*)fsm, &s_tot);
     for (int v = b0; v < b0 + per && v < units; ++v) {
       P.unit_prefix[v] = run;
-      run += __ldcg(P.uprefix + (size_t)v * (C + 1) + C);
+      run += __ldcg(P.uprefix + (size_t)v * (C + 1) + C) + P.tail_len;
     }
     if (tid == 0) {
       P.unit_prefix[units] = s_tot;
@@ -1038,6 +1039,7 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
   P.unit_cnt = x->counter;
   P.tlog = x->tlog;
   P.need_unit_prefix = !unit_split_ok(x->units, x->num_ctas);
+  P.tail_len = x->tail_len;
   cudaLaunchAttribute attr[1];
   const size_t smem =
       (size_t)x->G * P.nb * 16 + 16 + (size_t)(x->C + 4) * 4 + (size_t)2 * x->G * x->C * 4 + (size_t)x->C + 64;

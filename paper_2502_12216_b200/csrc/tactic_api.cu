@@ -414,6 +414,69 @@ void tactic_index_destroy(tactic_index_t idx) {
   free_index(idx, &ptrs);
 }
 
+// ------------------------------------------------------------------------ recent-token tail
+tactic_status_t tactic_set_tail_capacity(tactic_index_t idx, int32_t capacity) {
+  if (!idx) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL index");
+  if (capacity < 0) return fail(TACTIC_ERR_INVALID_ARGUMENT, "tail capacity %d < 0", capacity);
+  if (idx->tail_len > 0) return fail(TACTIC_ERR_INVALID_ARGUMENT, "the tail holds %d tokens", idx->tail_len);
+  if (capacity == idx->tail_cap) return TACTIC_OK;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto& ptrs = g_allocs[idx];
+  for (void* p : {(void*)idx->Kt, (void*)idx->Vt}) {
+    if (!p) continue;
+    cudaFree(p);
+    for (auto& q : ptrs)
+      if (q == p) q = nullptr;
+  }
+  idx->Kt = idx->Vt = nullptr;
+  idx->tail_cap = 0;
+  if (capacity == 0) return TACTIC_OK;
+  const size_t bytes = (size_t)idx->units * capacity * 128 * sizeof(__nv_bfloat16);
+  if (cudaMalloc((void**)&idx->Kt, bytes) != cudaSuccess || cudaMalloc((void**)&idx->Vt, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    if (idx->Kt) cudaFree(idx->Kt);
+    idx->Kt = idx->Vt = nullptr;
+    return fail(TACTIC_ERR_OOM, "tail buffers (%zu bytes)", 2 * bytes);
+  }
+  ptrs.push_back(idx->Kt);
+  ptrs.push_back(idx->Vt);
+  idx->tail_cap = capacity;
+  return TACTIC_OK;
+}
+
+tactic_status_t tactic_append(tactic_index_t idx, const void* k_new, const void* v_new, int32_t t, void* stream) {
+  if (!idx || !k_new || !v_new) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (t < 0) return fail(TACTIC_ERR_INVALID_ARGUMENT, "t = %d < 0", t);
+  if (t == 0) return TACTIC_OK;
+  if (idx->tail_cap == 0) {
+    tactic_status_t st = tactic_set_tail_capacity(idx, TACTIC_TAIL_CAPACITY);
+    if (st) return st;
+  }
+  if (idx->tail_len + t > idx->tail_cap)
+    return fail(TACTIC_ERR_SHAPE, "tail full (%d + %d > capacity %d): re-cluster", idx->tail_len, t, idx->tail_cap);
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(tactic::launch_tail_append((const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new, t, idx, s));
+  idx->tail_len += t;
+  // p >= 1 with the global split: every unit holds n + tail tokens
+  CK(tactic::launch_unit_prefix_fill(idx->all_unit_prefix, idx->units, (long long)idx->n + idx->tail_len, s));
+  return TACTIC_OK;
+}
+
+tactic_status_t tactic_index_tail(tactic_index_t idx, int32_t* len, int32_t* capacity) {
+  if (!idx) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL index");
+  if (len) *len = idx->tail_len;
+  if (capacity) *capacity = idx->tail_cap;
+  return TACTIC_OK;
+}
+
+tactic_status_t tactic_assign_tokens(tactic_index_t idx, const void* k, int32_t t, int32_t* assign, void* stream) {
+  if (!idx || !k || !assign) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (t < 0) return fail(TACTIC_ERR_INVALID_ARGUMENT, "t = %d < 0", t);
+  if (t == 0) return TACTIC_OK;
+  CK(tactic::launch_assign((const __nv_bfloat16*)k, t, idx, assign, (cudaStream_t)stream));
+  return TACTIC_OK;
+}
+
 tactic_status_t tactic_index_debug_timing(tactic_index_t idx, uint64_t* host, int32_t count) {
   if (!idx || !host) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
   if (!idx->tlog) return fail(TACTIC_ERR_UNSUPPORTED, "index created without TACTIC_TLOG=1");
@@ -518,6 +581,10 @@ static tactic_status_t run_attention(const void* q, tactic_index_t idx, bool all
   aa.lse = lse;
   aa.tlog = idx->tlog;
   aa.unit_split = unit_split_ok(idx->units, idx->num_ctas);  // else the global split (unit_prefix)
+  aa.Kt = idx->Kt;
+  aa.Vt = idx->Vt;
+  aa.tail_len = idx->tail_len;
+  aa.tail_cap = idx->tail_cap;
   CK(launch_attention_sparse(aa, idx->G, idx->num_ctas, s, ev_mid == nullptr));  // S8 + fused S9
   if (ev_mid) CK(cudaEventRecord(ev_mid, s));
   return TACTIC_OK;

@@ -73,6 +73,10 @@ _SIGS = {
     "tactic_decode_stage2": [_P, _P, _F, _P, _P, _P, _P, _P],
     "tactic_device_check": [ctypes.POINTER(_I)],
     "tactic_index_debug_timing": [_P, _P, _I],
+    "tactic_set_tail_capacity": [_P, _I],
+    "tactic_append": [_P, _P, _P, _I, _P],
+    "tactic_index_tail": [_P, ctypes.POINTER(_I), ctypes.POINTER(_I)],
+    "tactic_assign_tokens": [_P, _P, _I, _P, _P],
 }
 
 
@@ -356,3 +360,98 @@ def decode_stage2(q: torch.Tensor, index: Index, p: float, global_max: torch.Ten
     _check(lib().tactic_decode_stage2(_ptr(q), index.handle, float(p), _ptr(global_max), _ptr(global_mass),
                                       _ptr(o_part), _ptr(lse_part), _stream(stream)))
     return o_part, lse_part
+
+
+# ------------------------------------------------------------------ multi-step generation
+# SURVEY §8(f) NEXT 1; full attention on newly generated tokens, re-clustering
+# every 2048 of them; SPEC assign_token.
+def _kv_new_check(x: torch.Tensor, index: Index) -> int:
+    if x.dtype != torch.bfloat16 or not x.is_cuda or not x.is_contiguous():
+        raise ValueError("new keys / values must be contiguous CUDA bfloat16 tensors")
+    if x.dim() != 3 or x.shape[0] != index.units or x.shape[2] != HEAD_DIM:
+        raise ValueError("new keys / values must be [units, t, 128]")
+    return int(x.shape[1])
+
+
+def set_tail_capacity(index: Index, capacity: int):
+    """tactic_set_tail_capacity: room for `capacity` recent tokens per unit (tail empty)."""
+    _check(lib().tactic_set_tail_capacity(index.handle, int(capacity)))
+
+
+def append(index: Index, k_new: torch.Tensor, v_new: torch.Tensor, stream=None):
+    """tactic_append: t new tokens per unit ([units, t, 128] bf16) into the dense tail."""
+    t = _kv_new_check(k_new, index)
+    if tuple(v_new.shape) != tuple(k_new.shape):
+        raise ValueError("v_new must match k_new")
+    _kv_new_check(v_new, index)
+    _check(lib().tactic_append(index.handle, _ptr(k_new), _ptr(v_new), t, _stream(stream)))
+
+
+def tail_info(index: Index) -> tuple:
+    """(tail length, tail capacity) per unit."""
+    n, c = _I(0), _I(0)
+    _check(lib().tactic_index_tail(index.handle, ctypes.byref(n), ctypes.byref(c)))
+    return n.value, c.value
+
+
+def assign_tokens(index: Index, k: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """tactic_assign_tokens: nearest centroid (int32 [units, t]) of t new keys per unit."""
+    t = _kv_new_check(k, index)
+    if out is None:
+        out = torch.empty((index.units, t), dtype=torch.int32, device=k.device)
+    _check(lib().tactic_assign_tokens(index.handle, _ptr(k), t, _ptr(out), _stream(stream)))
+    return out
+
+
+class DecodeSession:
+    """Multi-step decode over one layer's KV cache: the step's new key/value is appended
+    to the dense tail of recently generated tokens, then the Tactic decode runs (selected
+    clusters plus the whole tail, so the new token attends itself); when the tail is full
+    the whole cache (clustered + tail tokens) is re-clustered (B1-B5) with the same
+    average cluster size first -- the host policy of P:112.
+
+        s = DecodeSession(K, V, n_clusters=1024, tail_capacity=2048)
+        out = s.step(q, k_new, v_new, p=0.9)   # k_new, v_new: [units, 1, 128]
+    """
+
+    def __init__(self, K: torch.Tensor, V: torch.Tensor, n_clusters: int, iters: int = 10, *, group_size: int = 4,
+                 tail_capacity: int = 2048, seed: int = 0):
+        self.B, self.Hkv = K.shape[0], K.shape[1]
+        self.G, self.iters, self.seed = group_size, iters, seed
+        self.cluster_size = K.shape[2] / n_clusters
+        self.tail_capacity = tail_capacity
+        self.K, self.V = K.contiguous(), V.contiguous()   # clustered tokens [B, Hkv, n, 128]
+        self.k_tail, self.v_tail = [], []                 # appended tokens, [units, t, 128] each
+        self.rebuilds = 0
+        self._build(n_clusters)
+
+    def _build(self, C: int):
+        self.index = build_index(self.K, self.V, C, self.iters, group_size=self.G, seed=self.seed)
+        set_tail_capacity(self.index, self.tail_capacity)
+        self.k_tail, self.v_tail = [], []
+
+    @property
+    def seq_len(self) -> int:
+        return self.K.shape[2] + tail_info(self.index)[0]
+
+    def _recluster(self):
+        units = self.B * self.Hkv
+        kt = torch.cat(self.k_tail, dim=1).view(self.B, self.Hkv, -1, HEAD_DIM)
+        vt = torch.cat(self.v_tail, dim=1).view(self.B, self.Hkv, -1, HEAD_DIM)
+        assert kt.shape[0] * kt.shape[1] == units
+        self.K = torch.cat([self.K, kt], dim=2).contiguous()
+        self.V = torch.cat([self.V, vt], dim=2).contiguous()
+        C = max(1, min(self.K.shape[2], int(round(self.K.shape[2] / self.cluster_size)), 4096))
+        self.index.close()
+        self._build(C)
+        self.rebuilds += 1
+
+    def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, p: float,
+             out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        t = _kv_new_check(k_new, self.index)
+        if tail_info(self.index)[0] + t > self.tail_capacity:
+            self._recluster()
+        append(self.index, k_new, v_new)
+        self.k_tail.append(k_new.clone())
+        self.v_tail.append(v_new.clone())
+        return decode(q, self.index, p, out=out)

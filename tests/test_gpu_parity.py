@@ -7,7 +7,7 @@ import pytest
 import torch
 
 from oracle import tactic_oracle as O
-from synth import make_layer, make_unit, uniform_unit
+from synth import bf16_round, make_layer, make_unit, uniform_unit
 from tests._gpu_helpers import (assert_output_close, dev_bf16, j_mismatch_allowed, oracle_layer_clustering)
 
 pytestmark = pytest.mark.gpu
@@ -427,3 +427,98 @@ def test_unit_split_per_unit_list_fallback(T):
             else:
                 o, _ = O.full_attention(qo, K[0, u], V[0, u])
             assert_output_close(got[0, u * G:(u + 1) * G], o, f"C={C} p={p} u={u}")
+
+
+# ----------------------------------------------------------------------------- NEXT 1: multi-step generation
+def _tail_tokens(units, t, seed):
+    rng = np.random.default_rng(seed)
+    kt = bf16_round((rng.standard_normal((units, t, 128)) * 1.5).astype(np.float32))
+    vt = bf16_round(rng.standard_normal((units, t, 128)).astype(np.float32))
+    return kt, vt
+
+
+@pytest.mark.parametrize("B,H,n,C", [(1, 2, 4096, 64),     # unit-aligned split
+                                     (12, 8, 2048, 32)])   # global token split (96 units)
+def test_tail_append_decode_parity(T, B, H, n, C):
+    """Appended tokens (two appends) are attended in full after the selected clusters;
+    the selection itself is unchanged (it ranks the clustered tokens only)."""
+    G = 4
+    K, V, q = _layer(B, H, G, n, 700 + B)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, B)
+    index = _import(T, K, V, cents, asg, G)
+    units = B * H
+    kt1, vt1 = _tail_tokens(units, 21, 1)
+    kt2, vt2 = _tail_tokens(units, 44, 2)
+    T.append(index, dev_bf16(kt1), dev_bf16(vt1))
+    T.append(index, dev_bf16(kt2), dev_bf16(vt2))
+    assert T.tail_info(index)[0] == 65
+    kt, vt = np.concatenate([kt1, kt2], axis=1), np.concatenate([vt1, vt2], axis=1)
+    qd = dev_bf16(q)
+    for p in (0.9, 1.0):
+        res = T.decode_debug(qd, index, p)
+        got = res["out"].float().cpu().numpy()
+        for u in sorted({0, 1, units // 2, units - 1}):
+            b, h = divmod(u, H)
+            qo = q[b, h * G:(h + 1) * G]
+            if p < 1.0:
+                ro = O.decode_unit(qo, idxs[u], p)
+                _check_unit_selection(res, u, G, ro["heads"], p, C)
+                toks = O.cluster_tokens(idxs[u], np.nonzero(res["union_mask"][u])[0])
+                K_all = np.concatenate([K[b, h], kt[u]])
+                V_all = np.concatenate([V[b, h], vt[u]])
+                o, _ = O.sparse_attention(qo, K_all, V_all, np.concatenate([toks, n + np.arange(65)]))
+            else:
+                o, _ = O.full_attention(qo, np.concatenate([K[b, h], kt[u]]), np.concatenate([V[b, h], vt[u]]))
+            assert_output_close(got[b, h * G:(h + 1) * G], o, f"tail p={p} u={u}")
+
+
+def test_tail_capacity_and_errors(T):
+    G, n, C = 4, 1024, 16
+    K, V, q = _layer(1, 1, G, n, 3)
+    cents, asg, _ = oracle_layer_clustering(K, V, C, 2, 3)
+    index = _import(T, K, V, cents, asg, G)
+    T.set_tail_capacity(index, 8)
+    assert T.tail_info(index) == (0, 8)
+    kt, vt = _tail_tokens(1, 5, 4)
+    T.append(index, dev_bf16(kt), dev_bf16(vt))
+    with pytest.raises(T.TacticError):        # 5 + 5 > 8: the caller must re-cluster
+        T.append(index, dev_bf16(kt), dev_bf16(vt))
+    with pytest.raises(T.TacticError):        # capacity changes need an empty tail
+        T.set_tail_capacity(index, 16)
+    assert T.tail_info(index) == (5, 8)
+
+
+def test_assign_tokens_matches_oracle(T):
+    """SPEC assign_token: nearest float32 centroid of new keys, float64."""
+    G, n, C = 4, 8192, 128
+    K, V, q = _layer(1, 4, G, n, 12)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, 12)
+    index = _import(T, K, V, cents, asg, G)
+    kt, _ = _tail_tokens(4, 300, 12)
+    kt[:, :50] = K[0, :, 1000:1050]            # keys resembling the cache
+    got = T.assign_tokens(index, dev_bf16(kt)).cpu().numpy()
+    for u in range(4):
+        ref = O.assign_tokens(kt[u], cents[u].astype(np.float64))
+        d = ((kt[u][:, None, :].astype(np.float64) - cents[u][None].astype(np.float64)) ** 2).sum(-1)
+        for i in np.nonzero(got[u] != ref)[0]:   # only exact-arithmetic near-ties may differ
+            assert abs(d[i, got[u][i]] - d[i, ref[i]]) <= 1e-9 * d[i, ref[i]], (u, i)
+
+
+def test_decode_session_reclusters_and_matches_full_attention(T):
+    """DecodeSession: append -> decode each step; a full tail triggers re-clustering of
+    the whole cache.  At p = 1 every step equals full attention over all tokens so far."""
+    G, n, C, H = 4, 2048, 32, 2
+    K, V, q = _layer(1, H, G, n, 21)
+    Kd, Vd = dev_bf16(K), dev_bf16(V)
+    s = T.DecodeSession(Kd, Vd, C, 3, group_size=G, tail_capacity=6)
+    K_all, V_all = K.copy(), V.copy()
+    for step in range(15):
+        kt, vt = _tail_tokens(H, 1, 100 + step)
+        qs = bf16_round(np.random.default_rng(step).standard_normal((1, H * G, 128)).astype(np.float32))
+        out = s.step(dev_bf16(qs), dev_bf16(kt), dev_bf16(vt), 1.0).float().cpu().numpy()
+        K_all = np.concatenate([K_all, kt[None]], axis=2)
+        V_all = np.concatenate([V_all, vt[None]], axis=2)
+        for h in range(H):
+            o, _ = O.full_attention(qs[0, h * G:(h + 1) * G], K_all[0, h], V_all[0, h])
+            assert_output_close(out[0, h * G:(h + 1) * G], o, f"step {step} h {h}")
+    assert s.rebuilds == 2 and s.seq_len == n + 15

@@ -457,3 +457,55 @@ def test_generator_deterministic_bf16_exact():
     assert 0.7 < vn.min() and vn.max() < 1.3                  # near-constant |v| (Fig. 2)
     uu = uniform_unit(100, 2, 0)
     assert uu["K"].shape == (100, 128)
+
+
+# ----------------------------------------------------------------------------- NEXT 1: multi-step generation
+def test_assign_tokens_is_brute_force_nearest_with_lowest_id_ties():
+    """SPEC assign_token: nearest centroid by direct squared distances,
+    ties to the lowest id -- pinned by a per-pair loop and deliberate duplicate centroids."""
+    rng = np.random.default_rng(11)
+    c = rng.standard_normal((9, 8))
+    c[5] = c[2]                      # exact duplicate: ties must go to id 2
+    k = np.concatenate([rng.standard_normal((40, 8)), c[[2, 7]] + 0.0])
+    got = O.assign_tokens(k, c)
+    for i, ki in enumerate(k):
+        d = [float(((ki - cj) ** 2).sum()) for cj in c]
+        best = min(d)
+        assert got[i] == d.index(best)
+    assert got[-2] == 2 and got[-1] == 7
+
+
+def test_tail_decode_p1_equals_full_attention_over_all_tokens():
+    """p = 1 selects every cluster (reading 15), so decode with a tail of appended tokens
+    equals full attention over the n + t tokens (torch SDPA, independent of the oracle)."""
+    u = make_unit(2048, 4, seed=5)
+    idx, _ = O.build_index(u["K"], u["V"], 32, 3, seed=5)
+    rng = np.random.default_rng(5)
+    Kt = bf16_round(rng.standard_normal((19, 128)).astype(np.float32))
+    Vt = bf16_round(rng.standard_normal((19, 128)).astype(np.float32))
+    r = O.decode_unit_with_tail(u["q"], idx, 1.0, Kt, Vt)
+    K_all = torch.from_numpy(np.concatenate([u["K"], Kt]).astype(np.float64))
+    V_all = torch.from_numpy(np.concatenate([u["V"], Vt]).astype(np.float64))
+    q = torch.from_numpy(u["q"].astype(np.float64))
+    ref = torch.nn.functional.scaled_dot_product_attention(q[None, :, None, :], K_all[None, None].expand(1, 4, -1, -1),
+                                                           V_all[None, None].expand(1, 4, -1, -1))[0, :, 0]
+    np.testing.assert_allclose(r["o"], ref.numpy(), atol=1e-12, rtol=1e-10)
+
+
+def test_tail_decode_is_lse_merge_of_union_and_tail_and_empty_tail_is_plain_decode():
+    """The tail adds one more LSE-mergeable part: attention over U + tail equals the
+    merge of attention over U and attention over the tail; an empty tail changes nothing."""
+    u = make_unit(4096, 4, seed=6)
+    idx, _ = O.build_index(u["K"], u["V"], 64, 3, seed=6)
+    rng = np.random.default_rng(6)
+    Kt = bf16_round(rng.standard_normal((33, 128)).astype(np.float32))
+    Vt = bf16_round(rng.standard_normal((33, 128)).astype(np.float32))
+    base = O.decode_unit(u["q"], idx, 0.9)
+    r = O.decode_unit_with_tail(u["q"], idx, 0.9, Kt, Vt)
+    assert np.array_equal(r["union_mask"], base["union_mask"])   # the selection ignores the tail
+    ot, lt = O.full_attention(u["q"], Kt, Vt)
+    om, lm = O.lse_merge(np.stack([base["o"], ot]), np.stack([base["lse"], lt]))
+    np.testing.assert_allclose(r["o"], om, atol=1e-12)
+    np.testing.assert_allclose(r["lse"], lm, atol=1e-12)
+    r0 = O.decode_unit_with_tail(u["q"], idx, 0.9, np.zeros((0, 128)), np.zeros((0, 128)))
+    np.testing.assert_allclose(r0["o"], base["o"], atol=0)
