@@ -435,6 +435,21 @@ def run_gpu(args, rank, world, local_rank):
     build_ms = float(np.mean(build_ms))
     c3 = measure_c3(T, dev, args.p, args.steps, timed_loop) if (args.c3 and world == 1) else None
 
+    # ---- Table-1 diagnostics (NEXT 3) over the same layers: Optimal /
+    # Cluster-Optimal / Tactic budgets, achieved cumulative score and success rate
+    table1 = None
+    if args.table1 and world == 1:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from table1 import public, table1_stats
+        acc = {}
+        for L in layers:
+            st = public(table1_stats(T, L["q"], L["index"], L["sizes"], (0.5, 0.9)))
+            for pk, d in st.items():
+                for k, v in d.items():
+                    acc.setdefault(pk, {}).setdefault(k, []).append(v)
+        table1 = {pk: {k: (float(np.sum(v)) if k == "instances" else float(np.mean(v))) for k, v in d.items()}
+                  for pk, d in acc.items()}
+
     # ---- target-fraction sweep (BASELINE.json configs[4], C5): same layers, graph per (p,
     # layer), device-timed like the headline, plus the union fraction the GPU selected
     sweep = []
@@ -497,6 +512,7 @@ def run_gpu(args, rank, world, local_rank):
         "speedup_vs_dense": dense_ms / ms,
         "p_sweep": sweep or None,
         "c3": c3,
+        "table1": table1,
         "select_cluster_size": index.info()["select_cluster_size"],
         "build": {"ms": build_ms, "iters_run": iters_run, "alg_tflop": alg_tflop,
                   "alg_tflops": alg_tflop / (build_ms * 1e-3),
@@ -521,6 +537,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sweep", type=int, default=1, help="1: add the C5 target-fraction sweep (p_sweep)")
     ap.add_argument("--c3", type=int, default=1, help="1: add the C3 batch-64 32K measurement (configs[2])")
+    ap.add_argument("--table1", type=int, default=1, help="1: add the Table-1 diagnostics (budgets, success)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -239,6 +239,16 @@ tactic_status_t tactic_assign_tokens(tactic_index_t idx, const void* k, int32_t 
                                      void* stream);
 
 /* ---------------------------------------------------------------------------------------
+ * Table-1 diagnostics: the exact logit of every
+ * clustered token for every query head, l = q . k / sqrt(d), in the index's LAYOUT order
+ * (clusters in id order, tokens of a cluster ascending; cluster j occupies layout rows
+ * [off_j, off_{j+1}) with off from the exported assignment's cluster sizes).
+ *   q device bf16 [B][Hq][128];  logits device float32 [units][G][n].
+ * Measurement tooling (Optimal / Cluster-Optimal budgets, achieved cumulative score),
+ * not part of the decode path.                                                          */
+tactic_status_t tactic_exact_logits(const void* q, tactic_index_t idx, float* logits, void* stream);
+
+/* ---------------------------------------------------------------------------------------
  * Misc. */
 const char* tactic_status_string(tactic_status_t s);
 const char* tactic_last_error(void);             /* thread-local, never NULL            */

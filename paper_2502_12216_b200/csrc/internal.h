@@ -150,6 +150,8 @@ cudaError_t launch_tail_append(const __nv_bfloat16* k_new, const __nv_bfloat16* 
                                cudaStream_t s);
 cudaError_t launch_assign(const __nv_bfloat16* k, int t, const tactic_index_s* x, int* assign, cudaStream_t s);
 cudaError_t launch_unit_prefix_fill(long long* up, int units, long long per_unit, cudaStream_t s);
+// ---- Table-1 diagnostics (diag.cu)
+cudaError_t launch_exact_logits(const __nv_bfloat16* q, const tactic_index_s* x, float* logits, cudaStream_t s);
 
 // ---- selection (select.cu)
 struct SelArgs {

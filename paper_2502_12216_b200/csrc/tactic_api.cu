@@ -477,6 +477,13 @@ tactic_status_t tactic_assign_tokens(tactic_index_t idx, const void* k, int32_t 
   return TACTIC_OK;
 }
 
+// ------------------------------------------------------------------------ Table-1 diagnostics
+tactic_status_t tactic_exact_logits(const void* q, tactic_index_t idx, float* logits, void* stream) {
+  if (!q || !idx || !logits) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  CK(tactic::launch_exact_logits((const __nv_bfloat16*)q, idx, logits, (cudaStream_t)stream));
+  return TACTIC_OK;
+}
+
 tactic_status_t tactic_index_debug_timing(tactic_index_t idx, uint64_t* host, int32_t count) {
   if (!idx || !host) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
   if (!idx->tlog) return fail(TACTIC_ERR_UNSUPPORTED, "index created without TACTIC_TLOG=1");

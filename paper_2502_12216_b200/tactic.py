@@ -77,6 +77,7 @@ _SIGS = {
     "tactic_append": [_P, _P, _P, _I, _P],
     "tactic_index_tail": [_P, ctypes.POINTER(_I), ctypes.POINTER(_I)],
     "tactic_assign_tokens": [_P, _P, _I, _P, _P],
+    "tactic_exact_logits": [_P, _P, _P, _P],
 }
 
 
@@ -455,3 +456,14 @@ class DecodeSession:
         self.k_tail.append(k_new.clone())
         self.v_tail.append(v_new.clone())
         return decode(q, self.index, p, out=out)
+
+
+# ------------------------------------------------------------------ Table-1 diagnostics
+def exact_logits(q: torch.Tensor, index: Index, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """tactic_exact_logits: q . k / sqrt(d) of every clustered token for every query head,
+    float32 [units, G, n] in the index's layout order (measurement tooling, NEXT 3)."""
+    _q_check(q, index)
+    if out is None:
+        out = torch.empty((index.units, index.G, index.n), dtype=torch.float32, device=q.device)
+    _check(lib().tactic_exact_logits(_ptr(q), index.handle, _ptr(out), _stream(stream)))
+    return out

@@ -522,3 +522,36 @@ def test_decode_session_reclusters_and_matches_full_attention(T):
             o, _ = O.full_attention(qs[0, h * G:(h + 1) * G], K_all[0, h], V_all[0, h])
             assert_output_close(out[0, h * G:(h + 1) * G], o, f"step {step} h {h}")
     assert s.rebuilds == 2 and s.seq_len == n + 15
+
+
+# ----------------------------------------------------------------------------- NEXT 3: Table-1 diagnostics
+def test_exact_logits_and_table1_match_oracle(T):
+    """tactic_exact_logits (layout order) and tools/table1.py against the oracle's
+    optimal_budget / cluster_optimal_budget / cumulative_score per head."""
+    import sys
+    sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    from tools.table1 import table1_stats
+    G, n, C = 4, 4096, 64
+    K, V, q = _layer(1, 2, G, n, 31)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, 31)
+    index = _import(T, K, V, cents, asg, G)
+    qd = dev_bf16(q)
+    lg = T.exact_logits(qd, index).cpu().numpy()
+    for u in range(2):
+        ref = (idxs[u].K[idxs[u].perm] @ q[0, u * G:(u + 1) * G].T.astype(np.float64)) / np.sqrt(128)
+        np.testing.assert_allclose(lg[u].T, ref, atol=2e-4, rtol=1e-5)
+    sizes = np.stack([idxs[u].sizes for u in range(2)])
+    st = table1_stats(T, qd, index, sizes, [0.5, 0.9])
+    for p in (0.5, 0.9):
+        ph = st[str(p)]["_per_head"]
+        res = T.decode_debug(qd, index, p)
+        for u in range(2):
+            for g in range(G):
+                qg = q[0, u * G + g]
+                assert abs(ph["optimal"][u, g] - O.optimal_budget(qg, idxs[u].K, p)) <= 1
+                assert abs(ph["cluster_optimal"][u, g] - O.cluster_optimal_budget(qg, idxs[u], p)) <= \
+                    idxs[u].sizes.max()
+                own = res["order"][u, g][:res["J"][u, g]]
+                toks = O.cluster_tokens(idxs[u], own)
+                assert ph["tactic_own"][u, g] == len(toks)
+                assert ph["achieved_own"][u, g] == pytest.approx(O.cumulative_score(qg, idxs[u].K, toks), abs=1e-5)
