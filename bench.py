@@ -450,6 +450,32 @@ def run_gpu(args, rank, world, local_rank):
         table1 = {pk: {k: (float(np.sum(v)) if k == "instances" else float(np.mean(v))) for k, v in d.items()}
                   for pk, d in acc.items()}
 
+    # ---- GQA union vs per-head loading (NEXT 2: union up to 1.65x faster)
+    ablation = None
+    if args.ablation and world == 1:
+        reps, own_tok, uni_tok = [], [], []
+        for L in layers:
+            o = torch.empty_like(L["q"])
+            T.decode_per_head(L["q"], L["index"], args.p, out=o)
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph):
+                T.decode_per_head(L["q"], L["index"], args.p, out=o)
+            reps.append(gph.replay)
+            dbg = T.decode_debug(L["q"], L["index"], args.p)
+            for u in range(units):
+                uni_tok.append(int(L["sizes"][u][dbg["union_mask"][u].astype(bool)].sum()))
+                own_tok.append(sum(int(L["sizes"][u][dbg["order"][u, g][:dbg["J"][u, g]]].sum()) for g in range(G)))
+        timed_loop(reps, 2 * LAYERS)
+        torch.cuda.synchronize()
+        ev = timed_loop(reps, max(4 * LAYERS, min(args.steps, 96)))
+        torch.cuda.synchronize()
+        ph_us = 1e3 * float(np.mean([a.elapsed_time(b) for a, b in ev]))
+        ablation = {"per_head_us_per_layer_step": ph_us, "union_us_per_layer_step": ms * 1e3,
+                    "union_speedup": ph_us / (ms * 1e3),
+                    "kv_tokens_per_head_loading": float(np.sum(own_tok)) / len(layers),
+                    "kv_tokens_union": float(np.sum(uni_tok)) / len(layers),
+                    "paper": "union up to 1.65x faster than per-head loading (P:695)"}
+
     # ---- target-fraction sweep (BASELINE.json configs[4], C5): same layers, graph per (p,
     # layer), device-timed like the headline, plus the union fraction the GPU selected
     sweep = []
@@ -513,6 +539,7 @@ def run_gpu(args, rank, world, local_rank):
         "p_sweep": sweep or None,
         "c3": c3,
         "table1": table1,
+        "gqa_union_ablation": ablation,
         "select_cluster_size": index.info()["select_cluster_size"],
         "build": {"ms": build_ms, "iters_run": iters_run, "alg_tflop": alg_tflop,
                   "alg_tflops": alg_tflop / (build_ms * 1e-3),
@@ -538,6 +565,7 @@ def main():
     ap.add_argument("--sweep", type=int, default=1, help="1: add the C5 target-fraction sweep (p_sweep)")
     ap.add_argument("--c3", type=int, default=1, help="1: add the C3 batch-64 32K measurement (configs[2])")
     ap.add_argument("--table1", type=int, default=1, help="1: add the Table-1 diagnostics (budgets, success)")
+    ap.add_argument("--ablation", type=int, default=1, help="1: add the GQA union vs per-head loading ablation")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

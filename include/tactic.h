@@ -239,6 +239,15 @@ tactic_status_t tactic_assign_tokens(tactic_index_t idx, const void* k, int32_t 
                                      void* stream);
 
 /* ---------------------------------------------------------------------------------------
+ * Per-head loading ablation (SPEC's own-set
+ * normalisation): the same selection as tactic_decode, but every query head
+ * attends only ITS OWN selected clusters S_g (each KV token is loaded once per head that
+ * selected it instead of once per KV head).  Same q / out layout as tactic_decode;
+ * 0 < p < 1; needs units x G <= CTAs / 2 (else UNSUPPORTED).  Measurement of the GQA
+ * union's benefit, not the method's output (which attends the union, reading 17).   */
+tactic_status_t tactic_decode_per_head(const void* q, tactic_index_t idx, float p, void* out, void* stream);
+
+/* ---------------------------------------------------------------------------------------
  * Table-1 diagnostics: the exact logit of every
  * clustered token for every query head, l = q . k / sqrt(d), in the index's LAYOUT order
  * (clusters in id order, tokens of a cluster ascending; cluster j occupies layout rows

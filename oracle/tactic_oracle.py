@@ -322,6 +322,16 @@ def decode_unit(q: np.ndarray, idx: Index, p: float) -> dict:
     return {"heads": heads, "union_mask": mask, "U": U, "tokens": toks, "o": o, "lse": lse}
 
 
+def decode_unit_per_head(q: np.ndarray, idx: Index, p: float) -> dict:
+    """Per-head loading (the ablation of P:695; SPEC's own-set normalisation):
+    every head attends only the tokens of its own selection S_g (Eq. 3 over S_g)."""
+    q = np.atleast_2d(np.asarray(q, dtype=np.float64))
+    heads = [decode_head(q[g], idx, p) for g in range(q.shape[0])]
+    o = np.stack([sparse_attention(q[g], idx.K, idx.V, cluster_tokens(idx, heads[g]["S"]))[0][0]
+                  for g in range(q.shape[0])])
+    return {"heads": heads, "o": o}
+
+
 # ---------------------------------------------------------------------------
 # Multi-step generation (SURVEY §8(f) NEXT 1).  P:112 (§1): "performs full
 # attention on newly generated tokens" and updates the clustering periodically;

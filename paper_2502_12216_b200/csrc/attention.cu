@@ -284,12 +284,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     auto issue_run = [&](uint8_t* sK, uint8_t* sV, int slot, int row, int len, int u, uint64_t* bar) {
       const uint8_t* kb;
       const uint8_t* vb;
+      const int ku = a.kv_div > 1 ? u / a.kv_div : u;  // the K/V unit (per-head ablation)
       if (row >= a.n) {
-        const size_t o = ((size_t)u * a.tail_cap + (row - a.n)) * 256;
+        const size_t o = ((size_t)ku * a.tail_cap + (row - a.n)) * 256;
         kb = (const uint8_t*)a.Kt + o;
         vb = (const uint8_t*)a.Vt + o;
       } else {
-        const size_t o = ((size_t)u * a.n + row) * 256;
+        const size_t o = ((size_t)ku * a.n + row) * 256;
         kb = (const uint8_t*)a.Kp + o;
         vb = (const uint8_t*)a.Vp + o;
       }

@@ -91,6 +91,9 @@ struct tactic_index_s {
   int* rowstart = nullptr;       // [units][G][C] first layout row of the r-th ranked cluster
   int* rowmap = nullptr;         // [units][G][slots] layout row of every sampled slot
   float* summ = nullptr;         // [units][G][nb][4] per-sample-block fit summaries
+  int* head_list = nullptr;      // [units*G][C]   per-head work lists (NEXT 2 ablation)
+  int* head_prefix = nullptr;    // [units*G][C+1]
+  int* head_cnt2 = nullptr;      // [units*G] attention arrival counters of the ablation
   uint8_t* mask_acc = nullptr;   // [units][C] union accumulator (zero between calls)
   unsigned int* head_cnt = nullptr;  // [units] selection arrival counters
   float* logits = nullptr;       // [units][G][slots]
@@ -137,6 +140,9 @@ struct AttnArgs {
   const __nv_bfloat16* Kt;
   const __nv_bfloat16* Vt;
   int tail_len, tail_cap;
+  // per-head loading ablation (NEXT 2): work-list units are (unit, head) pairs with G = 1,
+  // reading the K/V of unit u / kv_div (0 or 1: units are KV units)
+  int kv_div;
 };
 cudaError_t launch_attention_sparse(const AttnArgs& a, int G, int num_ctas, cudaStream_t s, bool pdl);
 cudaError_t launch_attention_dense(const AttnArgs& a, const CUtensorMap* tmK, const CUtensorMap* tmV, int G,
@@ -150,6 +156,8 @@ cudaError_t launch_tail_append(const __nv_bfloat16* k_new, const __nv_bfloat16* 
                                cudaStream_t s);
 cudaError_t launch_assign(const __nv_bfloat16* k, int t, const tactic_index_s* x, int* assign, cudaStream_t s);
 cudaError_t launch_unit_prefix_fill(long long* up, int units, long long per_unit, cudaStream_t s);
+// per-head work lists order[0..J_g) of every (unit, head) (NEXT 2 ablation)
+cudaError_t launch_head_lists(const tactic_index_s* x, cudaStream_t s);
 // ---- Table-1 diagnostics (diag.cu)
 cudaError_t launch_exact_logits(const __nv_bfloat16* q, const tactic_index_s* x, float* logits, cudaStream_t s);
 

@@ -195,6 +195,9 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_
   x->q_stage = A.get<__nv_bfloat16>(U * G * 128);
   x->o_stage = A.get<__nv_bfloat16>(U * G * 128);
   x->unit_cnt = A.get<int>(U);
+  x->head_list = A.get<int>(U * G * C + 4);
+  x->head_prefix = A.get<int>(U * G * (C + 1) + 4);
+  x->head_cnt2 = A.get<int>(U * G);
   x->rowstart = A.get<int>(U * G * C);
   x->rowmap = A.get<int>(U * G * (size_t)x->sc.slots);
   x->summ = A.get<float>(U * G * (size_t)sample_blocks(x->sc.slots) * 4);
@@ -219,6 +222,7 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_
   }
   cudaMemset(x->counter, 0, sizeof(unsigned int));
   cudaMemset(x->unit_cnt, 0, U * sizeof(int));
+  cudaMemset(x->head_cnt2, 0, U * G * sizeof(int));
   cudaMemset(x->mask_acc, 0, U * C);
   cudaMemset(x->head_cnt, 0, U * sizeof(unsigned int));
   cudaMemset(x->order, 0, U * G * C * sizeof(int));  // valid cluster ids before the first decode
@@ -657,6 +661,44 @@ tactic_status_t tactic_decode_debug(const void* q, tactic_index_t idx, float p, 
   if (fit) CK(cudaMemcpyAsync(fit, idx->fit, U * G * 6 * 8, cudaMemcpyDeviceToHost, s));
   if (union_mask) CK(cudaMemcpyAsync(union_mask, idx->umask, U * C, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  return TACTIC_OK;
+}
+
+// ------------------------------------------------------------------------ per-head loading ablation
+tactic_status_t tactic_decode_per_head(const void* q, tactic_index_t idx, float p, void* out, void* stream) {
+  if (!q || !idx || !out) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  tactic_status_t st = check_p(p);
+  if (st) return st;
+  const int VU = idx->units * idx->G;  // (unit, head) pairs
+  if (!unit_split_ok(VU, idx->num_ctas))
+    return fail(TACTIC_ERR_UNSUPPORTED, "per-head ablation needs units x G (%d) <= CTAs / 2", VU);
+  if (p >= 1.0f) return fail(TACTIC_ERR_UNSUPPORTED, "per-head ablation is for p < 1");
+  if (idx->fused_R > 0) return fail(TACTIC_ERR_UNSUPPORTED, "per-head ablation needs the multi-kernel selection");
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((st = run_selection(q, idx, (double)p, 0, s, nullptr, nullptr, nullptr))) return st;
+  CK(tactic::launch_head_lists(idx, s));
+  AttnArgs aa = {};
+  aa.q = (const __nv_bfloat16*)q;
+  aa.Kp = idx->Kp;
+  aa.Vp = idx->Vp;
+  aa.seg_row = idx->head_list;
+  aa.seg_prefix = idx->head_prefix;
+  aa.unit_prefix = nullptr;
+  aa.n = idx->n;
+  aa.C = idx->C;
+  aa.units = VU;
+  aa.Hkv = idx->Hkv;
+  aa.part_o = idx->part_o;
+  aa.part_lse = idx->part_lse;
+  aa.unit_cnt = idx->head_cnt2;
+  aa.out = (__nv_bfloat16*)out;
+  aa.unit_split = 1;
+  aa.Kt = idx->Kt;
+  aa.Vt = idx->Vt;
+  aa.tail_len = idx->tail_len;
+  aa.tail_cap = idx->tail_cap;
+  aa.kv_div = idx->G;
+  CK(launch_attention_sparse(aa, 1, idx->num_ctas, s, true));
   return TACTIC_OK;
 }
 

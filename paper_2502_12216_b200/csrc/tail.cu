@@ -112,4 +112,65 @@ cudaError_t launch_unit_prefix_fill(long long* up, int units, long long per_unit
   return cudaGetLastError();
 }
 
+// Per-head loading ablation (the GQA union loads each KV
+// token once, "up to 1.65x faster than per-head loading").  One CTA per (unit, head):
+// the head's own selected clusters order[0..J) (non-empty), in rank order, as a work
+// list (rows, token prefix) for the attention kernel run with G = 1 per (unit, head).
+__global__ void __launch_bounds__(256) head_lists_kernel(const int* __restrict__ order, const int* __restrict__ J,
+                                                         const int* __restrict__ offsets, int C, int G,
+                                                         int* __restrict__ hl, int* __restrict__ hp) {
+  __shared__ unsigned long long ws[8];
+  const int ug = blockIdx.x, u = ug / G, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int Jg = J[ug];
+  const int* ord = order + (size_t)ug * C;
+  const int* off = offsets + (size_t)u * (C + 1);
+  int* rl = hl + (size_t)ug * C;
+  int* rp = hp + (size_t)ug * (C + 1);
+  int seg_carry = 0, tok_carry = 0;
+  for (int r0 = 0; r0 < Jg; r0 += 256) {
+    const int r = r0 + tid;
+    int o0 = 0, sz = 0;
+    if (r < Jg) {
+      const int cid = ord[r];
+      o0 = off[cid];
+      sz = off[cid + 1] - o0;
+    }
+    // packed (tokens << 20 | segments) block scan of this chunk of 256 ranks
+    const unsigned long long v = sz > 0 ? (((unsigned long long)sz << 20) | 1ull) : 0ull;
+    unsigned long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    if (lane == 31) ws[warp] = incl;
+    __syncthreads();
+    unsigned long long wb = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      wb += w < warp ? ws[w] : 0ull;
+      tot += ws[w];
+    }
+    const unsigned long long ex = wb + incl - v;
+    if (sz > 0) {
+      const int seg = seg_carry + (int)(ex & 0xFFFFFull);
+      rl[seg] = o0;
+      rp[seg] = tok_carry + (int)(ex >> 20);
+    }
+    seg_carry += (int)(tot & 0xFFFFFull);
+    tok_carry += (int)(tot >> 20);
+    __syncthreads();  // ws reuse
+  }
+  for (int k = seg_carry + tid; k <= C; k += blockDim.x) {
+    rp[k] = tok_carry;
+    if (k < C) rl[k] = 0;
+  }
+}
+
+cudaError_t launch_head_lists(const tactic_index_s* x, cudaStream_t s) {
+  head_lists_kernel<<<x->units * x->G, 256, 0, s>>>(x->order, x->J, x->offsets, x->C, x->G, x->head_list,
+                                                    x->head_prefix);
+  return cudaGetLastError();
+}
+
 }  // namespace tactic

@@ -78,6 +78,7 @@ _SIGS = {
     "tactic_index_tail": [_P, ctypes.POINTER(_I), ctypes.POINTER(_I)],
     "tactic_assign_tokens": [_P, _P, _I, _P, _P],
     "tactic_exact_logits": [_P, _P, _P, _P],
+    "tactic_decode_per_head": [_P, _P, _F, _P, _P],
 }
 
 
@@ -466,4 +467,16 @@ def exact_logits(q: torch.Tensor, index: Index, out: Optional[torch.Tensor] = No
     if out is None:
         out = torch.empty((index.units, index.G, index.n), dtype=torch.float32, device=q.device)
     _check(lib().tactic_exact_logits(_ptr(q), index.handle, _ptr(out), _stream(stream)))
+    return out
+
+
+# ------------------------------------------------------------------ per-head loading ablation
+def decode_per_head(q: torch.Tensor, index: Index, p: float, out: Optional[torch.Tensor] = None,
+                    stream=None) -> torch.Tensor:
+    """tactic_decode_per_head: every query head attends only its own selected clusters
+    (NEXT 2 ablation of the GQA union; SPEC own-set normalisation S:421)."""
+    _q_check(q, index)
+    if out is None:
+        out = torch.empty_like(q)
+    _check(lib().tactic_decode_per_head(_ptr(q), index.handle, float(p), _ptr(out), _stream(stream)))
     return out

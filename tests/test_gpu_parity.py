@@ -555,3 +555,23 @@ def test_exact_logits_and_table1_match_oracle(T):
                 toks = O.cluster_tokens(idxs[u], own)
                 assert ph["tactic_own"][u, g] == len(toks)
                 assert ph["achieved_own"][u, g] == pytest.approx(O.cumulative_score(qg, idxs[u].K, toks), abs=1e-5)
+
+
+# ----------------------------------------------------------------------------- NEXT 2: per-head loading ablation
+def test_per_head_loading_matches_oracle_own_set_attention(T):
+    """tactic_decode_per_head: every head attends only its own S_g (P:695 ablation; SPEC
+    own-set normalisation S:421), against the oracle's decode_unit_per_head."""
+    G, n, C = 4, 8192, 128
+    K, V, q = _layer(1, 3, G, n, 41)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, 41)
+    index = _import(T, K, V, cents, asg, G)
+    qd = dev_bf16(q)
+    for p in (0.5, 0.9):
+        got = T.decode_per_head(qd, index, p).float().cpu().numpy()
+        res = T.decode_debug(qd, index, p)
+        for u in range(3):
+            qo = q[0, u * G:(u + 1) * G]
+            ro = O.decode_unit_per_head(qo, idxs[u], p)
+            for g in range(G):   # compare only heads whose selection matches exactly
+                if int(res["J"][u, g]) == ro["heads"][g]["J"]:
+                    assert_output_close(got[0, u * G + g:u * G + g + 1], ro["o"][g:g + 1], f"p={p} u={u} g={g}")
