@@ -449,6 +449,10 @@ def run_gpu(args, rank, world, local_rank):
                     acc.setdefault(pk, {}).setdefault(k, []).append(v)
         table1 = {pk: {k: (float(np.sum(v)) if k == "instances" else float(np.mean(v))) for k, v in d.items()}
                   for pk, d in acc.items()}
+        # Fig. 5: threshold rule vs a fixed budget of the same mean size (first layer)
+        from table1 import fig5_variance
+        table1["fig5_variance_layer0"] = fig5_variance(T, layers[0]["q"], layers[0]["index"], layers[0]["sizes"],
+                                                       layers[0]["K"], layers[0]["V"], args.p)
 
     # ---- GQA union vs per-head loading (NEXT 2: union up to 1.65x faster)
     ablation = None

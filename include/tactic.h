@@ -247,6 +247,15 @@ tactic_status_t tactic_assign_tokens(tactic_index_t idx, const void* k, int32_t 
  * union's benefit, not the method's output (which attends the union, reading 17).   */
 tactic_status_t tactic_decode_per_head(const void* q, tactic_index_t idx, float p, void* out, void* stream);
 
+/* Quest-like fixed-budget baseline ("uniformly chooses tokens
+ * across attention heads", SPEC fixed_budget_select S:465): every head takes clusters in
+ * criticality order until it holds `budget` tokens (rounded up to the cluster end, as
+ * reading 14), 1 <= budget <= n; then the GQA-union attention (per_head = 0) or each
+ * head over its own clusters (per_head = 1, same constraint as tactic_decode_per_head).
+ * J: nullable HOST int32 [units][G] selected prefix lengths (synchronises if given).  */
+tactic_status_t tactic_decode_fixed_budget(const void* q, tactic_index_t idx, int32_t budget, int32_t per_head,
+                                           void* out, int32_t* J, void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * Table-1 diagnostics: the exact logit of every
  * clustered token for every query head, l = q . k / sqrt(d), in the index's LAYOUT order

@@ -322,6 +322,19 @@ def decode_unit(q: np.ndarray, idx: Index, p: float) -> dict:
     return {"heads": heads, "union_mask": mask, "U": U, "tokens": toks, "o": o, "lse": lse}
 
 
+def fixed_budget_select(q_g: np.ndarray, idx: Index, k: int) -> dict:
+    """Quest-like baseline (SPEC fixed_budget_select S:465): clusters in
+    criticality order (O5) until the head holds k tokens -- the first cluster whose end
+    rank reaches k closes the set (cluster granularity, reading 14)."""
+    if not 1 <= k <= idx.n:
+        raise ValueError("k out of range")
+    order = sort_clusters(criticality(q_g, idx))
+    ends = np.cumsum(idx.sizes[order])
+    J = int(np.argmax(ends >= k)) + 1
+    S = order[:J]
+    return {"order": order, "J": J, "S": S[idx.sizes[S] > 0]}
+
+
 def decode_unit_per_head(q: np.ndarray, idx: Index, p: float) -> dict:
     """Per-head loading (the ablation of P:695; SPEC's own-set normalisation):
     every head attends only the tokens of its own selection S_g (Eq. 3 over S_g)."""

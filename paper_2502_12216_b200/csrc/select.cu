@@ -357,6 +357,7 @@ struct FitParams {
   unsigned long long* tlog;  // nullable debug stamps
   int need_unit_prefix;      // global attention split (units > CTAs/2): compute unit_prefix
   int tail_len;              // recent-token tail per unit (counted in unit_prefix)
+  int fixed_budget;          // > 0: Quest-like fixed token budget per head (NEXT 4 baseline)
 };
 
 // ------------------------------------------------------------------ S5-S7, one CTA per unit
@@ -549,7 +550,12 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
     }
     wstamp(1);
     int J = C;  // p >= 1: every cluster (reading 15)
-    if (P.p < 1.0) {
+    if (P.fixed_budget > 0) {
+      // Quest-like baseline: clusters in criticality order until the head
+      // holds fixed_budget tokens (rounded up to the cluster end, as reading 14)
+      const int* eg = s_end + (size_t)g * C;
+      J = 1 + warp_count_false(C - 1, [&](int r) { return eg[r] >= P.fixed_budget; });
+    } else if (P.p < 1.0) {
       const float target = (float)P.p * W;
       const int* eg = s_end + (size_t)g * C;
       if (EN >= target) {
@@ -1040,6 +1046,7 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
   P.tlog = x->tlog;
   P.need_unit_prefix = !unit_split_ok(x->units, x->num_ctas);
   P.tail_len = x->tail_len;
+  P.fixed_budget = x->fixed_budget;
   cudaLaunchAttribute attr[1];
   const size_t smem =
       (size_t)x->G * P.nb * 16 + 16 + (size_t)(x->C + 4) * 4 + (size_t)2 * x->G * x->C * 4 + (size_t)x->C + 64;

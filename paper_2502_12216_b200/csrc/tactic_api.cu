@@ -665,17 +665,8 @@ tactic_status_t tactic_decode_debug(const void* q, tactic_index_t idx, float p, 
 }
 
 // ------------------------------------------------------------------------ per-head loading ablation
-tactic_status_t tactic_decode_per_head(const void* q, tactic_index_t idx, float p, void* out, void* stream) {
-  if (!q || !idx || !out) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
-  tactic_status_t st = check_p(p);
-  if (st) return st;
-  const int VU = idx->units * idx->G;  // (unit, head) pairs
-  if (!unit_split_ok(VU, idx->num_ctas))
-    return fail(TACTIC_ERR_UNSUPPORTED, "per-head ablation needs units x G (%d) <= CTAs / 2", VU);
-  if (p >= 1.0f) return fail(TACTIC_ERR_UNSUPPORTED, "per-head ablation is for p < 1");
-  if (idx->fused_R > 0) return fail(TACTIC_ERR_UNSUPPORTED, "per-head ablation needs the multi-kernel selection");
-  cudaStream_t s = (cudaStream_t)stream;
-  if ((st = run_selection(q, idx, (double)p, 0, s, nullptr, nullptr, nullptr))) return st;
+static tactic_status_t per_head_attention(const void* q, tactic_index_t idx, void* out, cudaStream_t s) {
+  const int VU = idx->units * idx->G;
   CK(tactic::launch_head_lists(idx, s));
   AttnArgs aa = {};
   aa.q = (const __nv_bfloat16*)q;
@@ -699,6 +690,49 @@ tactic_status_t tactic_decode_per_head(const void* q, tactic_index_t idx, float 
   aa.tail_cap = idx->tail_cap;
   aa.kv_div = idx->G;
   CK(launch_attention_sparse(aa, 1, idx->num_ctas, s, true));
+  return TACTIC_OK;
+}
+
+static tactic_status_t per_head_checks(tactic_index_t idx) {
+  const int VU = idx->units * idx->G;  // (unit, head) pairs
+  if (!unit_split_ok(VU, idx->num_ctas))
+    return fail(TACTIC_ERR_UNSUPPORTED, "per-head attention needs units x G (%d) <= CTAs / 2", VU);
+  return TACTIC_OK;
+}
+
+tactic_status_t tactic_decode_per_head(const void* q, tactic_index_t idx, float p, void* out, void* stream) {
+  if (!q || !idx || !out) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  tactic_status_t st = check_p(p);
+  if (st) return st;
+  if (p >= 1.0f) return fail(TACTIC_ERR_UNSUPPORTED, "per-head ablation is for p < 1");
+  if (idx->fused_R > 0) return fail(TACTIC_ERR_UNSUPPORTED, "per-head ablation needs the multi-kernel selection");
+  if ((st = per_head_checks(idx))) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((st = run_selection(q, idx, (double)p, 0, s, nullptr, nullptr, nullptr))) return st;
+  return per_head_attention(q, idx, out, s);
+}
+
+tactic_status_t tactic_decode_fixed_budget(const void* q, tactic_index_t idx, int32_t budget, int32_t per_head,
+                                           void* out, int32_t* J, void* stream) {
+  if (!q || !idx || !out) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (budget < 1 || budget > idx->n) return fail(TACTIC_ERR_INVALID_ARGUMENT, "budget %d not in [1, n]", budget);
+  if (idx->fused_R > 0) return fail(TACTIC_ERR_UNSUPPORTED, "fixed budget needs the multi-kernel selection");
+  tactic_status_t st;
+  if (per_head && (st = per_head_checks(idx))) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  idx->fixed_budget = budget;  // read by the fit kernel's launcher only
+  st = run_selection(q, idx, 0.5, 0, s, nullptr, nullptr, nullptr);
+  idx->fixed_budget = 0;
+  if (st) return st;
+  if (per_head) {
+    if ((st = per_head_attention(q, idx, out, s))) return st;
+  } else if ((st = run_attention(q, idx, false, s, out, nullptr, nullptr))) {
+    return st;
+  }
+  if (J) {
+    CK(cudaMemcpyAsync(J, idx->J, (size_t)idx->units * idx->G * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
   return TACTIC_OK;
 }
 

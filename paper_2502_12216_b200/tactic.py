@@ -79,6 +79,7 @@ _SIGS = {
     "tactic_assign_tokens": [_P, _P, _I, _P, _P],
     "tactic_exact_logits": [_P, _P, _P, _P],
     "tactic_decode_per_head": [_P, _P, _F, _P, _P],
+    "tactic_decode_fixed_budget": [_P, _P, _I, _I, _P, _P, _P],
 }
 
 
@@ -480,3 +481,16 @@ def decode_per_head(q: torch.Tensor, index: Index, p: float, out: Optional[torch
         out = torch.empty_like(q)
     _check(lib().tactic_decode_per_head(_ptr(q), index.handle, float(p), _ptr(out), _stream(stream)))
     return out
+
+
+def decode_fixed_budget(q: torch.Tensor, index: Index, budget: int, per_head: bool = False,
+                        out: Optional[torch.Tensor] = None, stream=None):
+    """tactic_decode_fixed_budget: the Quest-like baseline -- `budget` tokens per head by
+    criticality (cluster granularity).  Returns (out, J [units, G])."""
+    _q_check(q, index)
+    if out is None:
+        out = torch.empty_like(q)
+    J = np.empty((index.units, index.G), dtype=np.int32)
+    _check(lib().tactic_decode_fixed_budget(_ptr(q), index.handle, int(budget), int(bool(per_head)), _ptr(out),
+                                            J.ctypes.data, _stream(stream)))
+    return out, J

@@ -575,3 +575,45 @@ def test_per_head_loading_matches_oracle_own_set_attention(T):
             for g in range(G):   # compare only heads whose selection matches exactly
                 if int(res["J"][u, g]) == ro["heads"][g]["J"]:
                     assert_output_close(got[0, u * G + g:u * G + g + 1], ro["o"][g:g + 1], f"p={p} u={u} g={g}")
+
+
+# ----------------------------------------------------------------------------- NEXT 4: fixed-budget baseline
+def test_fixed_budget_selection_and_output(T):
+    G, n, C = 4, 8192, 128
+    K, V, q = _layer(1, 2, G, n, 51)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, 51)
+    index = _import(T, K, V, cents, asg, G)
+    qd = dev_bf16(q)
+    for budget in (100, 700):
+        out, J = T.decode_fixed_budget(qd, index, budget)
+        ph, J2 = T.decode_fixed_budget(qd, index, budget, per_head=True)
+        assert np.array_equal(J, J2)
+        got, gph = out.float().cpu().numpy(), ph.float().cpu().numpy()
+        for u in range(2):
+            qo = q[0, u * G:(u + 1) * G]
+            mask = np.zeros(C, dtype=bool)
+            for g in range(G):
+                r = O.fixed_budget_select(qo[g], idxs[u], budget)
+                assert J[u, g] == r["J"], (budget, u, g)
+                mask[r["S"]] = True
+                o_own, _ = O.sparse_attention(qo[g], idxs[u].K, idxs[u].V, O.cluster_tokens(idxs[u], r["S"]))
+                assert_output_close(gph[0, u * G + g:u * G + g + 1], o_own, f"own b={budget} u={u} g={g}")
+            o, _ = O.sparse_attention(qo, idxs[u].K, idxs[u].V, O.cluster_tokens(idxs[u], np.nonzero(mask)[0]))
+            assert_output_close(got[0, u * G:(u + 1) * G], o, f"union b={budget} u={u}")
+
+
+def test_fig5_variance_tool_runs_and_is_consistent(T):
+    """tools/table1.fig5_variance: the fixed budget matches Tactic's mean token count;
+    eps of every head obeys the Appendix-A bound eps <= 2 (1 - p(I)) max |v|."""
+    import sys
+    sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    from tools.table1 import fig5_variance
+    G, n, C = 4, 8192, 128
+    K, V, q = _layer(1, 4, G, n, 61)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, 61)
+    index = _import(T, K, V, cents, asg, G)
+    r = fig5_variance(T, dev_bf16(q), index, np.stack([i.sizes for i in idxs]), dev_bf16(K), dev_bf16(V), 0.9)
+    vmax = float(np.max(np.linalg.norm(V.reshape(-1, 128), axis=1)))
+    for k in ("tactic", "fixed_budget"):
+        assert r[k]["eps"]["max"] <= 2 * (1 - r[k]["achieved_p"]["min"]) * vmax + 2e-2
+    assert abs(r["fixed_budget"]["tokens"]["mean"] - r["tactic"]["tokens"]["mean"]) <= 0.5 * r["tactic"]["tokens"]["mean"] + 200

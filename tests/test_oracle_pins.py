@@ -509,3 +509,26 @@ def test_tail_decode_is_lse_merge_of_union_and_tail_and_empty_tail_is_plain_deco
     np.testing.assert_allclose(r["lse"], lm, atol=1e-12)
     r0 = O.decode_unit_with_tail(u["q"], idx, 0.9, np.zeros((0, 128)), np.zeros((0, 128)))
     np.testing.assert_allclose(r0["o"], base["o"], atol=0)
+
+
+# ----------------------------------------------------------------------------- NEXT 4: fixed-budget baseline
+def test_fixed_budget_singletons_is_top_k_true_scores_and_rounds_to_cluster_end():
+    """SPEC fixed_budget_select: with singleton clusters the criticality order is
+    the true score order, so a budget of k tokens is the top-k tokens; with real clusters
+    the set closes at the first cluster end reaching k."""
+    rng = np.random.default_rng(8)
+    n = 64
+    K = bf16_round(rng.standard_normal((n, 16)).astype(np.float32))
+    V = bf16_round(rng.standard_normal((n, 16)).astype(np.float32))
+    idx = O.make_index(K, V, K.astype(np.float64), np.arange(n))
+    q = bf16_round(rng.standard_normal(16).astype(np.float32))
+    for k in (1, 7, 33, 64):
+        r = O.fixed_budget_select(q, idx, k)
+        top = np.argsort(-(K.astype(np.float64) @ q.astype(np.float64)), kind="stable")[:k]
+        assert sorted(O.cluster_tokens(idx, r["S"]).tolist()) == sorted(top.tolist())
+    idx2, _, _ = _rand_index(256, 16, seed=8)
+    q2 = rng.standard_normal(16)
+    for k in (1, 50, 200, 256):
+        r = O.fixed_budget_select(q2, idx2, k)
+        ends = np.cumsum(idx2.sizes[r["order"]])
+        assert ends[r["J"] - 1] >= k and (r["J"] == 1 or ends[r["J"] - 2] < k)

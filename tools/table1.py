@@ -71,6 +71,47 @@ def table1_stats(T, q: torch.Tensor, index, sizes: np.ndarray, ps) -> dict:
     return out
 
 
+def _cluster_mass(T, q, index, sizes):
+    """true softmax mass of every cluster for every head: [U][G][C] (float64, GPU)."""
+    dev = q.device
+    U, G = index.units, index.G
+    P = torch.softmax(T.exact_logits(q, index).double(), dim=-1)
+    sz = torch.from_numpy(np.asarray(sizes, dtype=np.int64)).to(dev)
+    off = torch.cat([torch.zeros((U, 1), dtype=torch.int64, device=dev), torch.cumsum(sz, dim=1)], dim=1)
+    cl = torch.cat([torch.zeros((U, G, 1), dtype=P.dtype, device=dev), torch.cumsum(P, dim=-1)], dim=-1)
+    return cl.gather(2, off[:, None, 1:].expand(U, G, -1)) - cl.gather(2, off[:, None, :-1].expand(U, G, -1)), sz
+
+
+def fig5_variance(T, q, index, sizes, K, V, p: float = 0.9) -> dict:
+    """Fig. 5 / P:253 on this data: the threshold rule (Tactic, own-set attention per head)
+    against a Quest-like fixed budget with the SAME mean token count per head.  Per head:
+    tokens, achieved cumulative score p(I) (Eq. 5) and attention distance
+    eps(I) = |o_full - o_I| (Eq. 4, own-set normalisation)."""
+    dev = q.device
+    U, G = index.units, index.G
+    mass, sz = _cluster_mass(T, q, index, sizes)
+    o_full = T.dense_decode(q, K, V).float().view(U, G, -1)
+
+    def stats(J, o_sel, order):
+        rank = torch.arange(order.shape[-1], device=dev)[None, None, :]
+        sel = (rank < torch.from_numpy(J.astype(np.int64)).to(dev)[..., None]).double()
+        tok = (sz[:, None, :].expand(U, G, -1).gather(2, order).double() * sel).sum(-1)
+        ach = (mass.gather(2, order) * sel).sum(-1)
+        eps = torch.linalg.norm(o_full - o_sel.float().view(U, G, -1), dim=-1).double()
+        f = lambda x: {"mean": float(x.mean()), "std": float(x.std()), "min": float(x.min()),  # noqa: E731
+                       "max": float(x.max())}
+        return {"tokens": f(tok), "achieved_p": f(ach), "eps": f(eps)}, tok
+
+    dbg = T.decode_debug(q, index, p)
+    order = torch.from_numpy(dbg["order"].astype(np.int64)).to(dev)
+    o_t = T.decode_per_head(q, index, p)
+    st_t, tok = stats(dbg["J"], o_t, order)
+    budget = max(1, int(round(float(tok.mean()))))
+    o_f, Jf = T.decode_fixed_budget(q, index, budget, per_head=True)
+    st_f, _ = stats(Jf, o_f, order)   # same criticality order (same q, same index)
+    return {"p": p, "fixed_budget_tokens": budget, "tactic": st_t, "fixed_budget": st_f, "heads": int(U * G)}
+
+
 def public(stats: dict) -> dict:
     return {p: {k: v for k, v in d.items() if not k.startswith("_")} for p, d in stats.items()}
 
