@@ -256,6 +256,14 @@ tactic_status_t tactic_decode_per_head(const void* q, tactic_index_t idx, float 
 tactic_status_t tactic_decode_fixed_budget(const void* q, tactic_index_t idx, int32_t budget, int32_t per_head,
                                            void* out, int32_t* J, void* stream);
 
+/* Selection variants of later decodes on this index:
+ *   TACTIC_OPT_WINDOWS_EXACT  SPEC's reading: the sampled window ranks
+ *     [x_k - w, x_k + w] keep their exact weights in the estimated cumulative mass and in
+ *     W (exact values take precedence over the fit, as for ranks <= N); the default is
+ *     reading 11 (only ranks <= N exact).  0 restores the default.                     */
+#define TACTIC_OPT_WINDOWS_EXACT 1u
+tactic_status_t tactic_index_set_options(tactic_index_t idx, uint32_t options);
+
 /* ---------------------------------------------------------------------------------------
  * Table-1 diagnostics: the exact logit of every
  * clustered token for every query head, l = q . k / sqrt(d), in the index's LAYOUT order

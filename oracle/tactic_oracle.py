@@ -225,9 +225,11 @@ def token_budget(w: np.ndarray, P: float) -> int:
     return int(np.argmax(cum >= P * W)) + 1
 
 
-def decode_head(q_g: np.ndarray, idx: Index, p: float) -> dict:
+def decode_head(q_g: np.ndarray, idx: Index, p: float, windows_exact: bool = False) -> dict:
     """Per query head: O5-O10 (selection) for one unit.  Returns the order pi, the
-    per-cluster end ranks, the fit and the selected cluster set S_g."""
+    per-cluster end ranks, the fit and the selected cluster set S_g.
+    windows_exact: SPEC's variant -- the window ranks keep their exact
+    weights too ("exact values taking precedence"); default reading 11: only i <= N."""
     n, C = idx.n, idx.C
     d = idx.K.shape[1]
     q_g = np.asarray(q_g, dtype=np.float64)
@@ -264,6 +266,9 @@ def decode_head(q_g: np.ndarray, idx: Index, p: float) -> dict:
         a, b = fit_two_point(float(x1), mu1, float(x2), mu2)       # O8
         i = np.arange(N + 1, n + 1, dtype=np.float64)
         what = np.concatenate([e_head, np.maximum(0.0, a / i + b)])  # Alg.1 l.10 + reading 12
+        if windows_exact:
+            what[win1 - 1] = np.exp(l_w1 - m)
+            what[win2 - 1] = np.exp(l_w2 - m)
     cum0 = np.concatenate([[0.0], np.cumsum(what)])                # cum(k), k = 0..n
     W = float(cum0[n])
     cum_end = cum0[ends]
@@ -307,12 +312,12 @@ def cluster_tokens(idx: Index, clusters) -> np.ndarray:
     return np.sort(np.concatenate([idx.perm[idx.offsets[j]:idx.offsets[j + 1]] for j in clusters]))
 
 
-def decode_unit(q: np.ndarray, idx: Index, p: float) -> dict:
+def decode_unit(q: np.ndarray, idx: Index, p: float, windows_exact: bool = False) -> dict:
     """O5-O12 for one unit and its G query heads: per-head selection, GQA union
     U = union_g S_g (§4.5), attention of every head over U (reading 17)."""
     q = np.atleast_2d(np.asarray(q, dtype=np.float64))
     G = q.shape[0]
-    heads = [decode_head(q[g], idx, p) for g in range(G)]
+    heads = [decode_head(q[g], idx, p, windows_exact) for g in range(G)]
     mask = np.zeros(idx.C, dtype=bool)
     for h in heads:
         mask[h["S"]] = True

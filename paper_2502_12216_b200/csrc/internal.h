@@ -95,6 +95,7 @@ struct tactic_index_s {
   int* head_prefix = nullptr;    // [units*G][C+1]
   int* head_cnt2 = nullptr;      // [units*G] attention arrival counters of the ablation
   int fixed_budget = 0;          // > 0 during tactic_decode_fixed_budget (NEXT 4 baseline)
+  uint32_t options = 0;          // TACTIC_OPT_* (tactic_index_set_options)
   uint8_t* mask_acc = nullptr;   // [units][C] union accumulator (zero between calls)
   unsigned int* head_cnt = nullptr;  // [units] selection arrival counters
   float* logits = nullptr;       // [units][G][slots]

@@ -358,6 +358,7 @@ struct FitParams {
   int need_unit_prefix;      // global attention split (units > CTAs/2): compute unit_prefix
   int tail_len;              // recent-token tail per unit (counted in unit_prefix)
   int fixed_budget;          // > 0: Quest-like fixed token budget per head (NEXT 4 baseline)
+  int windows_exact;         // SPEC variant: window ranks keep their exact weights
 };
 
 // ------------------------------------------------------------------ S5-S7, one CTA per unit
@@ -452,6 +453,11 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
   int* s_end = s_off + ((C + 1 + 3) & ~3);           // [G][C] (16-byte aligned for bulk copies)
   int* s_ord = s_end + (size_t)G * C;                // [G][C]
   uint8_t* mask = (uint8_t*)(s_ord + (size_t)G * C); // [C]
+  // windows-exact variant: every head's window logits (slots N .. N + 2 W1), then their
+  // inclusive prefix of exp(l - m) in place: [G][wx_stride] floats, 16-byte aligned
+  const int W1s = 2 * sc.w + 1;
+  const int wx_stride = ((2 * W1s + 3 + 3) & ~3) + 4;
+  float* s_wx = P.windows_exact ? (float*)(((uintptr_t)(mask + C) + 15) & ~(uintptr_t)15) : nullptr;
   const bool stamp_on = P.tlog != nullptr && u == 0;
   auto stamp = [&](int i) {  // debug: CTA of unit 0 at tlog[256 + i]
     if (stamp_on && tid == 0) {
@@ -502,11 +508,24 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
     pdl_wait();
     stamp(1);
     if (tid == 0) tl_mark(P.tlog, 3, 1, u == 0);
-    // stage the sample kernel's summaries (one round trip)
+    // stage the sample kernel's summaries (one round trip; + the window logits of every
+    // head for the windows-exact variant, from the 16-byte aligned slot at or below N)
     if (tid == 0) {
       const uint32_t bs = (uint32_t)G * nb * 16;
-      mbar_arrive_expect_tx(&sbar, bs);
+      uint32_t lb = 0;
+      if (s_wx)
+        for (int g = 0; g < G; ++g) {
+          const size_t st = (ub + g) * sc.slots + sc.N, al = st & ~(size_t)3;
+          lb += (uint32_t)((((st - al) + 2 * W1s) * 4 + 15) & ~(size_t)15);
+        }
+      mbar_arrive_expect_tx(&sbar, bs + lb);
       bulk_g2s(sm, P.summ + ub * nb * 4, bs, &sbar);
+      if (s_wx)
+        for (int g = 0; g < G; ++g) {
+          const size_t st = (ub + g) * sc.slots + sc.N, al = st & ~(size_t)3;
+          bulk_g2s(s_wx + (size_t)g * wx_stride, P.logits + al,
+                   (uint32_t)((((st - al) + 2 * W1s) * 4 + 15) & ~(size_t)15), &sbar);
+        }
     }
     mbar_wait(&sbar, 0);
     __syncthreads();
@@ -548,6 +567,45 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
       tail = make_tail_f(a, b, sc.N, n);
       W = EN + tail(n);
     }
+    // windows-exact variant ("exact values taking precedence"): the window
+    // ranks [lo_w, hi_w] carry their exact weights; xw = in-place inclusive prefix of
+    // exp(l - m) over the head's window slots (window 1 then window 2)
+    float* xw = nullptr;
+    int lo_w[2] = {0, 0}, hi_w[2] = {0, 0};
+    if (s_wx && !sc.fallback) {
+      xw = s_wx + (size_t)g * wx_stride + (((ub + g) * sc.slots + sc.N) & 3);
+      lo_w[0] = sc.x1 - sc.w; hi_w[0] = sc.x1 + sc.w;
+      lo_w[1] = sc.x2 - sc.w; hi_w[1] = sc.x2 + sc.w;
+      for (int wi = 0; wi < 2; ++wi) {
+        float carry = 0.f;
+        for (int i0 = 0; i0 < W1s; i0 += 32) {
+          const int i = wi * W1s + i0 + lane;
+          float v = i0 + lane < W1s ? __expf(xw[i] - m) : 0.f;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const float x = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += x;
+          }
+          if (i0 + lane < W1s) xw[i] = carry + v;
+          carry += __shfl_sync(0xffffffffu, v, 31);
+        }
+      }
+      __syncwarp();
+    }
+    // cumulative estimated mass at rank k > N, with the window correction when enabled
+    auto cum_tail = [&](int k) -> float {
+      float c = EN + tail(k);
+      if (xw) {
+#pragma unroll
+        for (int wi = 0; wi < 2; ++wi) {
+          if (k < lo_w[wi]) continue;
+          const int kk = k < hi_w[wi] ? k : hi_w[wi];
+          c += xw[wi * W1s + (kk - lo_w[wi])] - (tail(kk) - tail(lo_w[wi] - 1));
+        }
+      }
+      return c;
+    };
+    if (xw) W = cum_tail(n);
     wstamp(1);
     int J = C;  // p >= 1: every cluster (reading 15)
     if (P.fixed_budget > 0) {
@@ -613,7 +671,7 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
       } else {
         // past the head: cum(e_r) = EN + tail(e_r) at the cluster ends; the first cluster
         // whose end reaches the target (ends are non-decreasing in rank)
-        const int r = warp_count_false(C, [&](int r) { return eg[r] > sc.N && EN + tail(eg[r]) >= target; });
+        const int r = warp_count_false(C, [&](int r) { return eg[r] > sc.N && cum_tail(eg[r]) >= target; });
         J = r < C ? r + 1 : C;
       }
     }
@@ -1047,9 +1105,11 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
   P.need_unit_prefix = !unit_split_ok(x->units, x->num_ctas);
   P.tail_len = x->tail_len;
   P.fixed_budget = x->fixed_budget;
+  P.windows_exact = (x->options & 1u) ? 1 : 0;
   cudaLaunchAttribute attr[1];
   const size_t smem =
-      (size_t)x->G * P.nb * 16 + 16 + (size_t)(x->C + 4) * 4 + (size_t)2 * x->G * x->C * 4 + (size_t)x->C + 64;
+      (size_t)x->G * P.nb * 16 + 16 + (size_t)(x->C + 4) * 4 + (size_t)2 * x->G * x->C * 4 + (size_t)x->C + 64 +
+      (P.windows_exact ? (size_t)x->G * ((((size_t)2 * (2 * x->sc.w + 1) + 6) & ~(size_t)3) + 4) * 4 + 16 : 0);
   static size_t done = 0;
   cudaError_t e = ensure_smem((const void*)fit_unit_kernel, smem, &done);
   if (e != cudaSuccess) return e;

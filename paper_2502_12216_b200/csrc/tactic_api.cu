@@ -481,6 +481,13 @@ tactic_status_t tactic_assign_tokens(tactic_index_t idx, const void* k, int32_t 
   return TACTIC_OK;
 }
 
+tactic_status_t tactic_index_set_options(tactic_index_t idx, uint32_t options) {
+  if (!idx) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL index");
+  if (options & ~(uint32_t)TACTIC_OPT_WINDOWS_EXACT) return fail(TACTIC_ERR_INVALID_ARGUMENT, "unknown option bits");
+  idx->options = options;
+  return TACTIC_OK;
+}
+
 // ------------------------------------------------------------------------ Table-1 diagnostics
 tactic_status_t tactic_exact_logits(const void* q, tactic_index_t idx, float* logits, void* stream) {
   if (!q || !idx || !logits) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");

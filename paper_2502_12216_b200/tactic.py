@@ -80,6 +80,7 @@ _SIGS = {
     "tactic_exact_logits": [_P, _P, _P, _P],
     "tactic_decode_per_head": [_P, _P, _F, _P, _P],
     "tactic_decode_fixed_budget": [_P, _P, _I, _I, _P, _P, _P],
+    "tactic_index_set_options": [_P, ctypes.c_uint32],
 }
 
 
@@ -494,3 +495,11 @@ def decode_fixed_budget(q: torch.Tensor, index: Index, budget: int, per_head: bo
     _check(lib().tactic_decode_fixed_budget(_ptr(q), index.handle, int(budget), int(bool(per_head)), _ptr(out),
                                             J.ctypes.data, _stream(stream)))
     return out, J
+
+
+OPT_WINDOWS_EXACT = 1
+
+
+def set_options(index: Index, options: int):
+    """tactic_index_set_options: selection variants (OPT_WINDOWS_EXACT: SPEC S:284)."""
+    _check(lib().tactic_index_set_options(index.handle, int(options)))

@@ -617,3 +617,21 @@ def test_fig5_variance_tool_runs_and_is_consistent(T):
     for k in ("tactic", "fixed_budget"):
         assert r[k]["eps"]["max"] <= 2 * (1 - r[k]["achieved_p"]["min"]) * vmax + 2e-2
     assert abs(r["fixed_budget"]["tokens"]["mean"] - r["tactic"]["tokens"]["mean"]) <= 0.5 * r["tactic"]["tokens"]["mean"] + 200
+
+
+def test_windows_exact_variant_matches_oracle(T):
+    G, n, C = 4, 32768, 256
+    K, V, q = _layer(1, 2, G, n, 71)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, 71)
+    index = _import(T, K, V, cents, asg, G)
+    T.set_options(index, T.OPT_WINDOWS_EXACT)
+    qd = dev_bf16(q)
+    for p in (0.5, 0.9, 0.99):
+        res = T.decode_debug(qd, index, p)
+        for u in range(2):
+            ro = O.decode_unit(q[0, u * G:(u + 1) * G], idxs[u], p, windows_exact=True)
+            _check_unit_selection(res, u, G, ro["heads"], p, C)
+    T.set_options(index, 0)
+    res = T.decode_debug(qd, index, 0.9)
+    ro = O.decode_unit(q[0, 0:G], idxs[0], 0.9)
+    _check_unit_selection(res, 0, G, ro["heads"], 0.9, C)

@@ -532,3 +532,26 @@ def test_fixed_budget_singletons_is_top_k_true_scores_and_rounds_to_cluster_end(
         r = O.fixed_budget_select(q2, idx2, k)
         ends = np.cumsum(idx2.sizes[r["order"]])
         assert ends[r["J"] - 1] >= k and (r["J"] == 1 or ends[r["J"] - 2] < k)
+
+
+def test_windows_exact_variant_weights_and_total():
+    """SPEC S:284 / S:297 variant: window ranks carry their exact weights; the estimated
+    total changes by exactly sum(exact - fitted) over the window ranks, the rest of the
+    weights are unchanged, and the selection stays monotone in p."""
+    u = make_unit(8192, 4, seed=9)
+    idx, _ = O.build_index(u["K"], u["V"], 128, 3, seed=9)
+    q = u["q"][0]
+    a = O.decode_head(q, idx, 0.9)
+    b = O.decode_head(q, idx, 0.9, windows_exact=True)
+    sc = O.sample_constants(idx.n)
+    win = np.concatenate([np.arange(sc["x1"] - sc["w"], sc["x1"] + sc["w"] + 1),
+                          np.arange(sc["x2"] - sc["w"], sc["x2"] + sc["w"] + 1)]) - 1
+    tok = O.sorted_tokens(idx, b["order"])
+    ell = (idx.K[tok[win]] @ q.astype(np.float64)) / np.sqrt(128)
+    np.testing.assert_allclose(b["what"][win], np.exp(ell - b["m"]), rtol=1e-12)
+    rest = np.ones(idx.n, dtype=bool)
+    rest[win] = False
+    np.testing.assert_array_equal(a["what"][rest], b["what"][rest])
+    assert b["W"] - a["W"] == pytest.approx(float(b["what"][win].sum() - a["what"][win].sum()), rel=1e-9, abs=1e-12)
+    Js = [O.decode_head(q, idx, p, windows_exact=True)["J"] for p in (0.5, 0.8, 0.9, 0.95, 0.99)]
+    assert Js == sorted(Js)
