@@ -88,7 +88,6 @@ struct tactic_index_s {
   double* crit = nullptr;        // [units][G][C]
   int* order = nullptr;          // [units][G][C]
   int* ends = nullptr;           // [units][G][C]
-  int* rowstart = nullptr;       // [units][G][C] first layout row of the r-th ranked cluster
   int* rowmap = nullptr;         // [units][G][slots] layout row of every sampled slot
   float* summ = nullptr;         // [units][G][nb][4] per-sample-block fit summaries
   int* head_list = nullptr;      // [units*G][C]   per-head work lists (NEXT 2 ablation)

@@ -347,12 +347,10 @@ struct FitParams {
   double p;
   double* fit;
   int* J;
-  uint8_t* mask_acc;
   uint8_t* umask;
   int* ulist;
   int* uprefix;
   long long* unit_prefix;
-  unsigned int* head_cnt;
   unsigned int* unit_cnt;
   unsigned long long* tlog;  // nullable debug stamps
   int need_unit_prefix;      // global attention split (units > CTAs/2): compute unit_prefix
@@ -437,6 +435,24 @@ __device__ __forceinline__ int warp_count_false(int len, Pred pred) {
   }
   const int idx = lo + lane;
   return lo + __popc(__ballot_sync(0xffffffffu, idx < hi && !pred(idx)));
+}
+
+// windows-exact variant: estimated cumulative mass at rank k > N, i.e. E_N + the fitted
+// tail, corrected on the window ranks [x_w - w, x_w + w] to their exact weights (xw: the
+// inclusive prefix of the exact window weights, window 1 then window 2)
+__device__ __noinline__ float windows_cum(float EN, TailF tail, const float* xw, const SampleConsts sc, int k) {
+  float c = EN + tail(k);
+  const int W1 = 2 * sc.w + 1;
+  const int lo0 = sc.x1 - sc.w, hi0 = sc.x1 + sc.w, lo1 = sc.x2 - sc.w, hi1 = sc.x2 + sc.w;
+  if (k >= lo0) {
+    const int kk = k < hi0 ? k : hi0;
+    c += xw[kk - lo0] - (tail(kk) - tail(lo0 - 1));
+  }
+  if (k >= lo1) {
+    const int kk = k < hi1 ? k : hi1;
+    c += xw[W1 + kk - lo1] - (tail(kk) - tail(lo1 - 1));
+  }
+  return c;
 }
 
 constexpr int FITU_THREADS = 256;
@@ -571,11 +587,8 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
     // ranks [lo_w, hi_w] carry their exact weights; xw = in-place inclusive prefix of
     // exp(l - m) over the head's window slots (window 1 then window 2)
     float* xw = nullptr;
-    int lo_w[2] = {0, 0}, hi_w[2] = {0, 0};
     if (s_wx && !sc.fallback) {
       xw = s_wx + (size_t)g * wx_stride + (((ub + g) * sc.slots + sc.N) & 3);
-      lo_w[0] = sc.x1 - sc.w; hi_w[0] = sc.x1 + sc.w;
-      lo_w[1] = sc.x2 - sc.w; hi_w[1] = sc.x2 + sc.w;
       for (int wi = 0; wi < 2; ++wi) {
         float carry = 0.f;
         for (int i0 = 0; i0 < W1s; i0 += 32) {
@@ -591,21 +604,8 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
         }
       }
       __syncwarp();
+      W = windows_cum(EN, tail, xw, sc, n);
     }
-    // cumulative estimated mass at rank k > N, with the window correction when enabled
-    auto cum_tail = [&](int k) -> float {
-      float c = EN + tail(k);
-      if (xw) {
-#pragma unroll
-        for (int wi = 0; wi < 2; ++wi) {
-          if (k < lo_w[wi]) continue;
-          const int kk = k < hi_w[wi] ? k : hi_w[wi];
-          c += xw[wi * W1s + (kk - lo_w[wi])] - (tail(kk) - tail(lo_w[wi] - 1));
-        }
-      }
-      return c;
-    };
-    if (xw) W = cum_tail(n);
     wstamp(1);
     int J = C;  // p >= 1: every cluster (reading 15)
     if (P.fixed_budget > 0) {
@@ -671,7 +671,8 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
       } else {
         // past the head: cum(e_r) = EN + tail(e_r) at the cluster ends; the first cluster
         // whose end reaches the target (ends are non-decreasing in rank)
-        const int r = warp_count_false(C, [&](int r) { return eg[r] > sc.N && cum_tail(eg[r]) >= target; });
+        const int r = xw ? warp_count_false(C, [&](int r) { return eg[r] > sc.N && windows_cum(EN, tail, xw, sc, eg[r]) >= target; })
+                         : warp_count_false(C, [&](int r) { return eg[r] > sc.N && EN + tail(eg[r]) >= target; });
         J = r < C ? r + 1 : C;
       }
     }
@@ -1094,12 +1095,10 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
   P.p = a.p;
   P.fit = x->fit;
   P.J = x->J;
-  P.mask_acc = x->mask_acc;
   P.umask = x->umask;
   P.ulist = x->union_list;
   P.uprefix = x->union_prefix;
   P.unit_prefix = x->unit_prefix;
-  P.head_cnt = x->head_cnt;
   P.unit_cnt = x->counter;
   P.tlog = x->tlog;
   P.need_unit_prefix = !unit_split_ok(x->units, x->num_ctas);

@@ -198,7 +198,6 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_
   x->head_list = A.get<int>(U * G * C + 4);
   x->head_prefix = A.get<int>(U * G * (C + 1) + 4);
   x->head_cnt2 = A.get<int>(U * G);
-  x->rowstart = A.get<int>(U * G * C);
   x->rowmap = A.get<int>(U * G * (size_t)x->sc.slots);
   x->summ = A.get<float>(U * G * (size_t)sample_blocks(x->sc.slots) * 4);
   x->mask_acc = A.get<uint8_t>(U * C);
