@@ -227,6 +227,8 @@ tactic_status_t tactic_decode_stage2(const void* q, tactic_index_t idx, float p,
  *   (TACTIC_TAIL_CAPACITY) on first use; SHAPE if the tail would overflow.  Decodes
  *   enqueued after it on the same stream see the tokens.  A CUDA graph captured before an
  *   append keeps the tail length of its capture: re-capture after appending.
+ *   Sequence-sharded mode: append to ONE shard's index (the tail is attended by the shard
+ *   that holds it, like any of its tokens; appending everywhere would count it per shard).
  * tactic_index_tail: host outputs (nullable) tail length / capacity.
  * tactic_assign_tokens: SPEC assign_token: for t new keys per unit
  *   (device bf16 [units][t][128]) the nearest centroid by squared Euclidean distance in
