@@ -26,7 +26,7 @@ distribution (the paper prints no worked example of Alg. 1); see DESIGN.md.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Dict, List, Optional
 
 import numpy as np

@@ -4,8 +4,9 @@ The compute path lives in libtactic.so (hand-written sm_100a CUDA behind the C A
 include/tactic.h); `tactic` is its argument-marshalling binding.
 """
 from . import tactic  # noqa: F401
-from .tactic import (Index, TacticError, build_index, decode, decode_debug, decode_host,  # noqa: F401
-                     decode_stage1, decode_stage1b, decode_stage2, dense_decode, device_check,
-                     import_index, lse_merge, version)
+from .tactic import (DecodeSession, Index, TacticError, append, assign_tokens, build_index, decode,  # noqa: F401
+                     decode_debug, decode_fixed_budget, decode_host, decode_per_head, decode_stage1,
+                     decode_stage1b, decode_stage2, dense_decode, device_check, exact_logits, import_index,
+                     lse_merge, set_options, set_tail_capacity, tail_info, version)
 
 __version__ = "0.1.0"

@@ -1,7 +1,6 @@
 """Host-side checks that need no GPU: the C-ABI library loads and exports every symbol
 include/tactic.h declares, the binding declares a signature for each, and status
 strings are stable.  No compute call is made here."""
-import ctypes
 import os
 import re
 
