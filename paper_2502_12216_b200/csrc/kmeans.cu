@@ -26,7 +26,9 @@ namespace tactic {
 constexpr int KM_BLK = 1024;         // tokens per histogram / scatter block
 constexpr int TC_STAGE = 65536;      // one centroid tile image: hi 32 KB | lo 32 KB
 constexpr int TC_A = 32768;          // 128 keys x 128 dims bf16
-constexpr size_t TC_SMEM = 1024 + TC_A + 2 * (size_t)TC_STAGE + 256;
+constexpr int TC_KA = 2;             // A tiles (128 keys each) per CTA: every centroid tile
+                                     // streamed from L2 feeds 256 keys (halves B traffic)
+constexpr size_t TC_SMEM = 1024 + TC_KA * (size_t)TC_A + 2 * (size_t)TC_STAGE + 256;
 
 __device__ __forceinline__ const __nv_bfloat16* krow(const __nv_bfloat16* K, long long sb, long long sh,
                                                      long long sn, int Hkv, int u, int i) {
@@ -90,8 +92,8 @@ __global__ void __launch_bounds__(192, 1) km_assign_tc_kernel(const KmArgs a, in
   const int u = blockIdx.y;
   if (a.converged[u] != 0) return;
   uint8_t* sm = (uint8_t*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sA = sm;
-  uint8_t* sB = sm + TC_A;
+  uint8_t* sA = sm;                       // [TC_KA][128 keys x 128 dims], SWIZZLE_128B K-major
+  uint8_t* sB = sm + TC_KA * TC_A;
   uint64_t* bars = (uint64_t*)(sB + 2 * TC_STAGE);
   uint64_t* full = bars;          // [2]
   uint64_t* empty = bars + 2;     // [2]
@@ -100,19 +102,21 @@ __global__ void __launch_bounds__(192, 1) km_assign_tc_kernel(const KmArgs a, in
   uint32_t* tmem_slot = (uint32_t*)(bars + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row0 = blockIdx.x * 128;
+  const int row0 = blockIdx.x * (128 * TC_KA);
   const int ntiles = a.Cpad / 128;
 
-  // A tile: 128 keys, SWIZZLE_128B K-major (two 64-dim column blocks), loaded by the
-  // epilogue warps with cp.async; rows past n are zero.
+  // A tiles: 128 * TC_KA keys, SWIZZLE_128B K-major (two 64-dim column blocks per tile),
+  // loaded by the epilogue warps with cp.async; rows past n are zero.
   if (warp >= 2) {
     const int t = threadIdx.x - 64;  // 0..127
-    for (int c = t; c < 128 * 16; c += 128) {
-      const int r = c >> 4, ch = c & 15;
+    for (int c = t; c < TC_KA * 128 * 16; c += 128) {
+      const int ra = c >> 4, ch = c & 15;
+      const int at = ra >> 7, r = ra & 127;
       const int cb = ch >> 3, cc = ch & 7;
-      const bool valid = row0 + r < a.n;
-      const __nv_bfloat16* src = krow(a.K, a.sb, a.sh, a.sn, a.Hkv, u, valid ? row0 + r : 0) + ch * 8;
-      cp_async16(sA + cb * 16384 + (r >> 3) * 1024 + (r & 7) * 128 + ((cc ^ (r & 7)) << 4), src, valid);
+      const bool valid = row0 + ra < a.n;
+      const __nv_bfloat16* src = krow(a.K, a.sb, a.sh, a.sn, a.Hkv, u, valid ? row0 + ra : 0) + ch * 8;
+      cp_async16(sA + at * TC_A + cb * 16384 + (r >> 3) * 1024 + (r & 7) * 128 + ((cc ^ (r & 7)) << 4), src,
+                 valid);
     }
     cp_async_commit();
   }
@@ -125,7 +129,8 @@ __global__ void __launch_bounds__(192, 1) km_assign_tc_kernel(const KmArgs a, in
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 256);
+  // accumulators: [2 buffers][TC_KA A tiles][128 columns]
+  if (warp == 1) tmem_alloc(tmem_slot, 256 * TC_KA);
   if (warp >= 2) cp_async_wait_all();
   fence_proxy_async_smem();
   tc_fence_before();
@@ -147,7 +152,6 @@ __global__ void __launch_bounds__(192, 1) km_assign_tc_kernel(const KmArgs a, in
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       const uint32_t idesc = umma_idesc_bf16(128, 128);
-      const uint32_t aaddr = smem_u32(sA);
       for (int t = 0; t < ntiles; ++t) {
         const int s = t & 1, acc = t & 1;
         const uint32_t ph = (t >> 1) & 1;
@@ -155,24 +159,32 @@ __global__ void __launch_bounds__(192, 1) km_assign_tc_kernel(const KmArgs a, in
         mbar_wait(&full[s], ph);
         tc_fence_after();
         const uint32_t baddr = smem_u32(sB + s * TC_STAGE);
-        const uint32_t dcol = tmem + acc * 128;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t koff = (kk >> 2) * 16384 + (kk & 3) * 32;
-          const uint64_t ad = umma_desc_sw128(aaddr + koff);
-          tc_mma_f16(dcol, ad, umma_desc_sw128(baddr + koff), idesc, kk > 0 ? 1u : 0u);
-          tc_mma_f16(dcol, ad, umma_desc_sw128(baddr + 32768 + koff), idesc, 1u);
+        for (int at = 0; at < TC_KA; ++at) {
+          const uint32_t aaddr = smem_u32(sA + at * TC_A);
+          const uint32_t dcol = tmem + acc * (128 * TC_KA) + at * 128;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t koff = (kk >> 2) * 16384 + (kk & 3) * 32;
+            const uint64_t ad = umma_desc_sw128(aaddr + koff);
+            tc_mma_f16(dcol, ad, umma_desc_sw128(baddr + koff), idesc, kk > 0 ? 1u : 0u);
+            tc_mma_f16(dcol, ad, umma_desc_sw128(baddr + 32768 + koff), idesc, 1u);
+          }
         }
         tc_commit(&empty[s]);
         tc_commit(&tfull[acc]);
       }
     }
   } else {
-    // epilogue: thread <-> key row (TMEM lane); argmin over all centroid columns
+    // epilogue: thread <-> key row (TMEM lane) of every A tile; argmin over all centroids
     const int q = warp & 3;
-    const int row = row0 + q * 32 + lane;
-    float best = INFINITY;
-    int arg = 0;
+    float best[TC_KA];
+    int arg[TC_KA];
+#pragma unroll
+    for (int at = 0; at < TC_KA; ++at) {
+      best[at] = INFINITY;
+      arg[at] = 0;
+    }
     const float* cn = a.cnorm + (size_t)u * a.Cpad;
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t & 1;
@@ -181,14 +193,23 @@ __global__ void __launch_bounds__(192, 1) km_assign_tc_kernel(const KmArgs a, in
       tc_fence_after();
 #pragma unroll 1
       for (int ch = 0; ch < 4; ++ch) {
-        uint32_t v[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * 128 + ch * 32, v);
-        tmem_ld_wait();
         const int jb = t * 128 + ch * 32;
+        float cv[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float dist = fmaf(-2.f, __uint_as_float(v[i]), __ldg(cn + jb + i));
-          if (dist < best) { best = dist; arg = jb + i; }
+        for (int i = 0; i < 8; ++i) {
+          const float4 c4 = __ldg(reinterpret_cast<const float4*>(cn + jb) + i);
+          cv[4 * i] = c4.x; cv[4 * i + 1] = c4.y; cv[4 * i + 2] = c4.z; cv[4 * i + 3] = c4.w;
+        }
+#pragma unroll
+        for (int at = 0; at < TC_KA; ++at) {
+          uint32_t v[32];
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * (128 * TC_KA) + at * 128 + ch * 32, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float dist = fmaf(-2.f, __uint_as_float(v[i]), cv[i]);
+            if (dist < best[at]) { best[at] = dist; arg[at] = jb + i; }
+          }
         }
       }
       tc_fence_before();
@@ -196,10 +217,14 @@ __global__ void __launch_bounds__(192, 1) km_assign_tc_kernel(const KmArgs a, in
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
     int ch = 0;
-    if (row < a.n) {
-      int* ap = a.assign + (size_t)u * a.n + row;
-      ch = (*ap != arg) ? 1 : 0;
-      *ap = arg;
+#pragma unroll
+    for (int at = 0; at < TC_KA; ++at) {
+      const int row = row0 + at * 128 + q * 32 + lane;
+      if (row < a.n) {
+        int* ap = a.assign + (size_t)u * a.n + row;
+        ch += (*ap != arg[at]) ? 1 : 0;
+        *ap = arg[at];
+      }
     }
     ch = __reduce_add_sync(0xffffffffu, ch);
     if (lane == 0 && ch) atomicAdd(&changed[(size_t)iter * a.units + u], ch);
@@ -207,7 +232,7 @@ __global__ void __launch_bounds__(192, 1) km_assign_tc_kernel(const KmArgs a, in
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, 256);
+  if (warp == 1) tmem_dealloc(tmem, 256 * TC_KA);
 }
 
 // ---------------------------------------------------------------- B2 (CUDA cores, debug)
@@ -505,6 +530,7 @@ cudaError_t km_init_centroids(const KmArgs& a, const int* init_dev, cudaStream_t
 
 cudaError_t km_assign(const KmArgs& a, int iter, bool simt, cudaStream_t s) {
   const dim3 grid((a.n + 127) / 128, a.units);
+  const dim3 grid_tc((a.n + 128 * TC_KA - 1) / (128 * TC_KA), a.units);
   if (simt) {
     km_assign_simt_kernel<<<grid, 128, 0, s>>>(a, iter, a.changed);
     return cudaGetLastError();
@@ -516,7 +542,7 @@ cudaError_t km_assign(const KmArgs& a, int iter, bool simt, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  km_assign_tc_kernel<<<grid, 192, TC_SMEM, s>>>(a, iter, a.changed);
+  km_assign_tc_kernel<<<grid_tc, 192, TC_SMEM, s>>>(a, iter, a.changed);
   return cudaGetLastError();
 }
 
