@@ -393,30 +393,45 @@ __global__ void km_scatter_kernel(const KmArgs a, int iter) {
 }
 
 // ---------------------------------------------------------------- B3 means
-__global__ void km_update_kernel(const KmArgs a, int iter) {
-  const int u = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// One CTA per cluster: its 8 warps take every 8th member row (8 independent gather
+// streams per cluster instead of one dependent walk), fp64 per-warp partial sums, combined
+// in warp order -- deterministic; the member mean in fp64 as before.
+__global__ void __launch_bounds__(256) km_update_kernel(const KmArgs a, int iter) {
+  __shared__ double part[8][128];
+  const int u = blockIdx.y, j = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (km_skip(a, u, iter)) return;
-  const int j = blockIdx.x * (blockDim.x >> 5) + warp;
   if (j >= a.C) return;
   const int* off = a.offsets + (size_t)u * (a.C + 1);
   const int* perm = a.perm + (size_t)u * a.n;
   const int s = off[j], e = off[j + 1];
-  float4 c;
-  if (e > s) {
-    double acc[4] = {0, 0, 0, 0};
-    for (int r = s; r < e; ++r) {
-      const __nv_bfloat16* k = krow(a.K, a.sb, a.sh, a.sn, a.Hkv, u, perm[r]) + lane * 4;
-      const uint2 raw = *reinterpret_cast<const uint2*>(k);
-      const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-      const float2 f0 = __bfloat1622float2(k2[0]), f1 = __bfloat1622float2(k2[1]);
-      acc[0] += f0.x; acc[1] += f0.y; acc[2] += f1.x; acc[3] += f1.y;
+  if (e <= s) {
+    if (warp == 0) {
+      const float4 c = *reinterpret_cast<const float4*>(a.cent + ((size_t)u * a.C + j) * 128 + lane * 4);
+      store_centroid(a, u, j, c);
     }
-    const double inv = (double)(e - s);
-    c = make_float4((float)(acc[0] / inv), (float)(acc[1] / inv), (float)(acc[2] / inv), (float)(acc[3] / inv));
-  } else {
-    c = *reinterpret_cast<const float4*>(a.cent + ((size_t)u * a.C + j) * 128 + lane * 4);
+    return;
   }
-  store_centroid(a, u, j, c);
+  double acc[4] = {0, 0, 0, 0};
+  for (int r = s + warp; r < e; r += 8) {
+    const __nv_bfloat16* k = krow(a.K, a.sb, a.sh, a.sn, a.Hkv, u, perm[r]) + lane * 4;
+    const uint2 raw = *reinterpret_cast<const uint2*>(k);
+    const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+    const float2 f0 = __bfloat1622float2(k2[0]), f1 = __bfloat1622float2(k2[1]);
+    acc[0] += f0.x; acc[1] += f0.y; acc[2] += f1.x; acc[3] += f1.y;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) part[warp][lane * 4 + i] = acc[i];
+  __syncthreads();
+  if (warp == 0) {
+    double t[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int w = 0; w < 8; ++w)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) t[i] += part[w][lane * 4 + i];
+    const double inv = (double)(e - s);
+    store_centroid(a, u, j, make_float4((float)(t[0] / inv), (float)(t[1] / inv), (float)(t[2] / inv),
+                                        (float)(t[3] / inv)));
+  }
 }
 
 // ---------------------------------------------------------------- B5 / B6
@@ -554,7 +569,7 @@ cudaError_t km_count_scan_scatter(const KmArgs& a, int iter, cudaStream_t s) {
 }
 
 cudaError_t km_update(const KmArgs& a, int iter, cudaStream_t s) {
-  km_update_kernel<<<dim3((a.C + 7) / 8, a.units), 256, 0, s>>>(a, iter);
+  km_update_kernel<<<dim3(a.C, a.units), 256, 0, s>>>(a, iter);
   return cudaGetLastError();
 }
 
