@@ -314,7 +314,7 @@ __global__ void km_count_kernel(const KmArgs a, int iter, const int* __restrict_
 }
 
 // per-cluster exclusive prefix over blocks (in place) + cluster offsets
-__global__ void km_scan_kernel(const KmArgs a, int iter) {
+__global__ void __launch_bounds__(1024) km_scan_kernel(const KmArgs a, int iter) {
   __shared__ int red[32];
   __shared__ int total_sh;
   const int u = blockIdx.x;
@@ -325,12 +325,18 @@ __global__ void km_scan_kernel(const KmArgs a, int iter) {
   for (int k = 0; k < per && k < 4; ++k) {
     const int j = j0 + k;
     if (j >= a.C) break;
+    // column scan over the blocks, 16 independent loads in flight per batch
     int run = 0;
-    for (int b = 0; b < a.nblk; ++b) {
-      int* p = a.blk_counts + ((size_t)u * a.nblk + b) * a.C + j;
-      const int v = *p;
-      *p = run;
-      run += v;
+    int* col = a.blk_counts + (size_t)u * a.nblk * a.C + j;
+    for (int b0 = 0; b0 < a.nblk; b0 += 16) {
+      int v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = b0 + q < a.nblk ? col[(size_t)(b0 + q) * a.C] : 0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if (b0 + q < a.nblk) col[(size_t)(b0 + q) * a.C] = run;
+        run += v[q];
+      }
     }
     tot[k] = run;
   }
