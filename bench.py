@@ -435,6 +435,38 @@ def run_gpu(args, rank, world, local_rank):
     build_ms = float(np.mean(build_ms))
     c3 = measure_c3(T, dev, args.p, args.steps, timed_loop) if (args.c3 and world == 1) else None
 
+    # ---- C4 (BASELINE.json configs[3]: 1M tokens sequence-sharded over 8 GPUs): on this
+    # single GPU, one shard's compute per decode step (a C2-shaped shard: 131072 tokens x
+    # 8 KV heads, C = 1024) through the three sharded stages + the final LSE merge, with the
+    # three collectives (MAX all-reduce, SUM all-reduce, all-gather) absent (world size 1)
+    c4 = None
+    if args.c4 and world == 1:
+        L = layers[0]
+        lm = torch.empty((units, G, 2), dtype=torch.float64, device=dev)
+        ms_ = torch.empty((units, G, 1 + T.SHARD_GRID_T), dtype=torch.float64, device=dev)
+        op = torch.empty((units, G, 128), dtype=torch.float32, device=dev)
+        lp = torch.empty((units, G), dtype=torch.float32, device=dev)
+        mo = torch.empty((units * G, 128), dtype=torch.bfloat16, device=dev)
+
+        def shard_step():
+            T.decode_stage1(L["q"], L["index"], lm)
+            T.decode_stage1b(L["index"], lm, ms_)
+            T.decode_stage2(L["q"], L["index"], args.p, lm, ms_, op, lp)
+            T.lse_merge(op.view(1, units * G, 128), lp.view(1, units * G), out=mo)
+
+        shard_step()
+        gs = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gs):
+            shard_step()
+        timed_loop([gs.replay], 5)
+        torch.cuda.synchronize()
+        ev = timed_loop([gs.replay], max(20, min(args.steps, 100)))
+        torch.cuda.synchronize()
+        c4 = {"workload": "C4 shard: 131072 tokens x 8 KV heads (one of 8 shards of a 1M-token context), C = 1024, "
+                          f"p={args.p}; stage1 + stage1b + stage2 + LSE merge on 1 GPU, collectives not included",
+              "us_per_shard_step": 1e3 * float(np.mean([a.elapsed_time(b) for a, b in ev])),
+              "dense_us_per_shard_step": dense_ms * 1e3}
+
     # ---- Table-1 diagnostics (NEXT 3) over the same layers: Optimal /
     # Cluster-Optimal / Tactic budgets, achieved cumulative score and success rate
     table1 = None
@@ -542,6 +574,7 @@ def run_gpu(args, rank, world, local_rank):
         "speedup_vs_dense": dense_ms / ms,
         "p_sweep": sweep or None,
         "c3": c3,
+        "c4_shard": c4,
         "table1": table1,
         "gqa_union_ablation": ablation,
         "select_cluster_size": index.info()["select_cluster_size"],
@@ -569,6 +602,7 @@ def main():
     ap.add_argument("--sweep", type=int, default=1, help="1: add the C5 target-fraction sweep (p_sweep)")
     ap.add_argument("--c3", type=int, default=1, help="1: add the C3 batch-64 32K measurement (configs[2])")
     ap.add_argument("--table1", type=int, default=1, help="1: add the Table-1 diagnostics (budgets, success)")
+    ap.add_argument("--c4", type=int, default=1, help="1: add the C4 per-shard sequence-sharded measurement")
     ap.add_argument("--ablation", type=int, default=1, help="1: add the GQA union vs per-head loading ablation")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 timeout 900 python bench.py > gpurun_out/bench_$R.json 2> gpurun_out/bench_$R.err
 tail -1 gpurun_out/bench_$R.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
-  --log-file gpurun_out/launches_$R.csv python bench.py --steps 8 --warmup 3 --no-cpu-baseline --sweep 0 --c3 0 --table1 0 --ablation 0 \
+  --log-file gpurun_out/launches_$R.csv python bench.py --steps 8 --warmup 3 --no-cpu-baseline --sweep 0 --c3 0 --table1 0 --ablation 0 --c4 0 \
   > gpurun_out/launches_$R.log 2>&1
 echo "launch list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on \

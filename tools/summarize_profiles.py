@@ -48,7 +48,7 @@ if os.path.exists(lp):
     tot = sum(sum(v) / len(v) for v in decode.values()) or 1.0
     with open(os.path.join(PROF, f"{R}_launches.txt"), "w") as f:
         f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none launch list of `python bench.py "
-                f"--steps 8 --warmup 3 --no-cpu-baseline --sweep 0 --c3 0 --table1 0 --ablation 0` ({R}).\n# Per-launch times are cold-cache and "
+                f"--steps 8 --warmup 3 --no-cpu-baseline --sweep 0 --c3 0 --table1 0 --ablation 0 --c4 0` ({R}).\n# Per-launch times are cold-cache and "
                 f"serialised (no PDL overlap): compare shares, not absolutes.\n")
         f.write(f"{'launches':>8} {'mean us':>9} {'share of decode':>16}  kernel\n")
         for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
