@@ -560,8 +560,8 @@ def run_gpu(args, rank, world, local_rank):
         "metric": METRIC, "value": value_us, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": _config(args, world),
-        # per decode step: score+rank, sample, fit, attention (fused selection: 1 + attention)
-        "gpu_launches": (1 if args.p >= 1 else (2 if index.info()["select_cluster_size"] else 4)) * args.steps,
+        # per decode step: score+rank, sample, fit, attention
+        "gpu_launches": (1 if args.p >= 1 else 4) * args.steps,
         "roofline": {"bound": "hbm", "kernel": "attention_kernel<4,false> (S8 sparse split-KV)",
                      "achieved": att_gbs, "peak": hbm, "unit": "GB/s", "frac": att_gbs / hbm,
                      "traffic": traffic, "peak_source": peak_src,
@@ -577,7 +577,6 @@ def run_gpu(args, rank, world, local_rank):
         "c4_shard": c4,
         "table1": table1,
         "gqa_union_ablation": ablation,
-        "select_cluster_size": index.info()["select_cluster_size"],
         "build": {"ms": build_ms, "iters_run": iters_run, "alg_tflop": alg_tflop,
                   "alg_tflops": alg_tflop / (build_ms * 1e-3),
                   "exec_tflops_split_bf16": 2 * alg_tflop / (build_ms * 1e-3)},

@@ -79,8 +79,8 @@ typedef struct {
 typedef struct {
   int32_t units, batch, num_kv_heads, group_size, seq_len, n_clusters;
   int32_t iters_requested;
-  int32_t select_cluster_size;  /* CTAs per unit of the fused S1-S7 cluster kernel (0 = the
-                                   multi-kernel selection path)                          */
+  int32_t select_cluster_size;  /* always 0 (the retired single-kernel selection); kept for
+                                   ABI stability                                         */
   int64_t device_bytes;         /* bytes the index holds on the device                   */
 } tactic_index_info_t;
 
@@ -123,9 +123,10 @@ tactic_status_t tactic_index_export(tactic_index_t idx, float* centroids, int32_
                                     double* inertia, int32_t* iters_run, void* stream);
 
 tactic_status_t tactic_index_info(tactic_index_t idx, tactic_index_info_t* info);
-/* Debug: per-phase %globaltimer stamps of the fused selection kernel's last launch,
- * host uint64 [units][16][8] (CTA rank < 16, phase < 8).  Only for indices created with
- * the environment variable TACTIC_TLOG=1; synchronises the device.                   */
+/* Debug: the %globaltimer / clock stamps the decode kernels leave in the index's timing
+ * log (kernel timeline, per-phase stamps of CTA 0 of each kernel; tools/phase_timing.py
+ * decodes them), host uint64 [count].  Only for indices created with the environment
+ * variable TACTIC_TLOG=1; synchronises the device.                                   */
 tactic_status_t tactic_index_debug_timing(tactic_index_t idx, uint64_t* host, int32_t count);
 void tactic_index_destroy(tactic_index_t idx);
 

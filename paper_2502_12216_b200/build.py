@@ -19,7 +19,7 @@ LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libtactic.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["tactic_api.cu", "attention.cu", "select.cu", "select_fused.cu", "rank_cluster.cu", "kmeans.cu",
+SOURCES = ["tactic_api.cu", "attention.cu", "select.cu", "rank_cluster.cu", "kmeans.cu",
            "tail.cu", "diag.cu"]
 HEADERS = ["common.cuh", "internal.h"]
 

@@ -112,7 +112,6 @@ struct tactic_index_s {
   __nv_bfloat16* q_stage = nullptr;  // [units][G][128] (host-buffer decode)
   __nv_bfloat16* o_stage = nullptr;
   long long device_bytes = 0;
-  int fused_R = 0;               // CTAs per unit of the fused selection kernel (0: multi-kernel path)
   unsigned long long* tlog = nullptr;  // [units][16][8] phase timestamps (TACTIC_TLOG=1)
 };
 
@@ -182,8 +181,6 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl);
 int sample_blocks(int slots);
 cudaError_t launch_stage1b(const SelArgs& a, cudaStream_t s);
 // fused S1-S7 (select_fused.cu)
-cudaError_t launch_select_fused(const __nv_bfloat16* q, tactic_index_s* x, double p, cudaStream_t s, bool pdl);
-int choose_fused_R(tactic_index_s* x);
 
 // ---- k-means / layout (kmeans.cu)
 struct KmArgs {

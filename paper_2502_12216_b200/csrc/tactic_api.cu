@@ -227,9 +227,6 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_
   }
   x->device_bytes = A.bytes;
   {
-    // selection path: TACTIC_SELECT=fused (cluster kernel) | multi (default, 4 kernels)
-    const char* sel = getenv("TACTIC_SELECT");
-    x->fused_R = (sel && strcmp(sel, "fused") == 0) ? choose_fused_R(x) : 0;
     const char* tl = getenv("TACTIC_TLOG");
     if (tl && tl[0] == '1' && cudaMalloc((void**)&x->tlog, tlog_entries(U) * 8) == cudaSuccess) {
       cudaMemset(x->tlog, 0, tlog_entries(U) * 8);
@@ -531,7 +528,7 @@ tactic_status_t tactic_index_info(tactic_index_t idx, tactic_index_info_t* info)
   info->n_clusters = idx->C;
   info->iters_requested = idx->iters_req;
   info->device_bytes = idx->device_bytes;
-  info->select_cluster_size = idx->fused_R;
+  info->select_cluster_size = 0;  // (the fused single-kernel selection was retired in round 1)
   return TACTIC_OK;
 }
 
@@ -580,10 +577,6 @@ static tactic_status_t run_selection(const void* q, tactic_index_t idx, double p
   sa.gmass = gmass;
   sa.local_max = local_max;
   const bool pdl = true;
-  if (mode == 0 && idx->fused_R > 0) {  // one cluster-launched kernel for S1-S7
-    CK(launch_select_fused((const __nv_bfloat16*)q, idx, p, s, pdl));
-    return TACTIC_OK;
-  }
   if (mode != 1) {
     CK(launch_score_rank(sa.q, idx, s, pdl));  // S1, S2, S3 (+ sampled-slot row map)
     CK(launch_sample(sa, s, pdl));             // S4 (+ per-block fit summaries)
@@ -729,7 +722,6 @@ tactic_status_t tactic_decode_per_head(const void* q, tactic_index_t idx, float 
   tactic_status_t st = check_p(p);
   if (st) return st;
   if (p >= 1.0f) return fail(TACTIC_ERR_UNSUPPORTED, "per-head ablation is for p < 1");
-  if (idx->fused_R > 0) return fail(TACTIC_ERR_UNSUPPORTED, "per-head ablation needs the multi-kernel selection");
   if ((st = per_head_checks(idx))) return st;
   cudaStream_t s = (cudaStream_t)stream;
   if ((st = run_selection(q, idx, (double)p, 0, s, nullptr, nullptr, nullptr))) return st;
@@ -740,7 +732,6 @@ tactic_status_t tactic_decode_fixed_budget(const void* q, tactic_index_t idx, in
                                            void* out, int32_t* J, void* stream) {
   if (!q || !idx || !out) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
   if (budget < 1 || budget > idx->n) return fail(TACTIC_ERR_INVALID_ARGUMENT, "budget %d not in [1, n]", budget);
-  if (idx->fused_R > 0) return fail(TACTIC_ERR_UNSUPPORTED, "fixed budget needs the multi-kernel selection");
   tactic_status_t st;
   if (per_head && (st = per_head_checks(idx))) return st;
   cudaStream_t s = (cudaStream_t)stream;

@@ -341,48 +341,6 @@ def test_c2_full_size_sampled_parity(T):
         assert_output_close(out1[0, u * G:(u + 1) * G], o, f"C2 p=1 unit {u}")
 
 
-# ----------------------------------------------------------------------------- fused selection kernel
-@pytest.mark.parametrize("units", [8, 12, 30, 60, 100])
-def test_fused_selection_cluster_sizes(T, units, monkeypatch):
-    """units -> cluster size R of the fused S1-S7 kernel (16/8/4/2/1 as co-residency allows)."""
-    G, n, C = 4, 2048, 32
-    K, V, q = _layer(units, 1, G, n, 100 + units)
-    cents, asg, idxs = oracle_layer_clustering(K, V, C, 4, units)
-    monkeypatch.setenv("TACTIC_SELECT", "fused")
-    index = _import(T, K, V, cents, asg, G)
-    assert index.info()["select_cluster_size"] >= 1
-    res = T.decode_debug(dev_bf16(q), index, 0.9)
-    got = res["out"].float().cpu().numpy()
-    for u in sorted({0, units // 2, units - 1}):
-        ro = O.decode_unit(q[u, 0:G], idxs[u], 0.9)
-        _check_unit_selection(res, u, G, ro["heads"], 0.9, C)
-        toks = O.cluster_tokens(idxs[u], np.nonzero(res["union_mask"][u])[0])
-        o, _ = O.sparse_attention(q[u, 0:G], idxs[u].K, idxs[u].V, toks)
-        assert_output_close(got[u, 0:G], o, f"units={units} u={u}")
-
-
-def test_fused_matches_multikernel_path(T, monkeypatch):
-    G, n, C = 4, 8192, 128
-    K, V, q = _layer(1, 4, G, n, 77)
-    cents, asg, _ = oracle_layer_clustering(K, V, C, 5, 77)
-    monkeypatch.setenv("TACTIC_SELECT", "fused")
-    fused = _import(T, K, V, cents, asg, G)
-    assert fused.info()["select_cluster_size"] > 0
-    monkeypatch.setenv("TACTIC_SELECT", "multi")
-    multi = _import(T, K, V, cents, asg, G)
-    assert multi.info()["select_cluster_size"] == 0
-    qd = dev_bf16(q)
-    for p in [0.5, 0.9, 0.99]:
-        a, b = T.decode_debug(qd, fused, p), T.decode_debug(qd, multi, p)
-        assert np.array_equal(a["order"], b["order"])
-        assert np.array_equal(a["J"], b["J"])
-        assert np.array_equal(a["union_mask"], b["union_mask"])
-        # fp32 tensor-core vs fp32 FMA logits, different summation trees: same decisions,
-        # fit values equal to ~1e-5 relative (b ~ 0 compared absolutely)
-        np.testing.assert_allclose(a["fit"], b["fit"], rtol=1e-4, atol=1e-7)
-        assert torch.allclose(a["out"].float(), b["out"].float(), atol=1e-2)
-
-
 # ----------------------------------------------------------------------------- attention work-split modes
 @pytest.mark.parametrize("B,H,n,C", [(12, 8, 2048, 32),    # 96 units > CTAs/2: global token split,
                                      (64, 8, 1024, 16)])   # C3-like unit count (512 units)

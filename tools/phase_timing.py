@@ -1,19 +1,17 @@
 """In-kernel %globaltimer stamps of the decode kernels on the C2 workload (TACTIC_TLOG=1).
 
-    python tools/phase_timing.py [--select fused|multi]
-Debug aid only: prints the fit-kernel phases (multi path) or the fused-kernel phases,
-and CTA 0 of the attention kernel (tiles issued / consumed), relative times in us.
+    python tools/phase_timing.py [--no-flush]
+Debug aid only: prints the kernel timeline, the score_rank / fit phases and CTA 0 of the
+attention kernel (setup, tiles issued / consumed, merges), relative times in us.
 """
 import argparse
 import os
 import sys
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--select", default="multi")
 ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between calls")
 args = ap.parse_args()
 os.environ["TACTIC_TLOG"] = "1"
-os.environ["TACTIC_SELECT"] = args.select
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import numpy as np  # noqa: E402
@@ -30,8 +28,7 @@ K, V, q = make_layer(1, 8, G, n, seed=0)
 to = lambda a: torch.from_numpy(a).cuda().to(torch.bfloat16)  # noqa: E731
 Kd, Vd, qd = to(K), to(V), to(q)
 idx = T.build_index(Kd, Vd, C, 10, group_size=G)
-R = idx.info()["select_cluster_size"]
-print("select cluster size R =", R)
+R = 0  # multi-kernel selection (the only path)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 out = torch.empty_like(qd)
 T.decode(qd, idx, 0.9, out=out)
@@ -84,15 +81,6 @@ for it in range(4):
                                                                for i, nm in enumerate(names) if hs[i] > 0))
             ck = full[1709:1715]
             print("  fit warp 0 (cycles after staged): " + "  ".join(f"{nm} {ck[i + 1] - ck[0]}" for i, nm in enumerate(names) if hs[i] > 0))
-    else:
-        t = full.reshape(-1, 16, 8)[:, :R, :]
-        t0 = t[:, :, 0].min()
-        names = ["start", "ph1 done", "sync1", "ph2 done", "ph3 done", "sync2", "ph4 done", "sync4"]
-        for k, nm in enumerate(names):
-            v = (t[:, :, k] - t0) / 1000.0
-            ok = t[:, :, k] > 0
-            if ok.any():
-                print(f"  {nm:10s} min {v[ok].min():7.2f}  median {np.median(v[ok]):7.2f}  max {v[ok].max():7.2f} us")
     at = full[192:192 + 35]
     if at[0] > 0:
         b0 = at[0]
