@@ -593,3 +593,25 @@ def test_windows_exact_variant_matches_oracle(T):
     res = T.decode_debug(qd, index, 0.9)
     ro = O.decode_unit(q[0, 0:G], idxs[0], 0.9)
     _check_unit_selection(res, 0, G, ro["heads"], 0.9, C)
+
+
+def test_per_head_loading_with_tail(T):
+    """Per-head loading (G = 1 work units reading unit u / G) attends its own clusters plus
+    the whole recent-token tail of its KV unit."""
+    G, n, C = 4, 4096, 64
+    K, V, q = _layer(1, 2, G, n, 81)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, 81)
+    index = _import(T, K, V, cents, asg, G)
+    kt, vt = _tail_tokens(2, 29, 81)
+    T.append(index, dev_bf16(kt), dev_bf16(vt))
+    got = T.decode_per_head(dev_bf16(q), index, 0.9).float().cpu().numpy()
+    res = T.decode_debug(dev_bf16(q), index, 0.9)
+    for u in range(2):
+        qo = q[0, u * G:(u + 1) * G]
+        ro = O.decode_unit_per_head(qo, idxs[u], 0.9)
+        for g in range(G):
+            if int(res["J"][u, g]) != ro["heads"][g]["J"]:
+                continue
+            toks = np.concatenate([O.cluster_tokens(idxs[u], ro["heads"][g]["S"]), n + np.arange(29)])
+            o, _ = O.sparse_attention(qo[g], np.concatenate([K[0, u], kt[u]]), np.concatenate([V[0, u], vt[u]]), toks)
+            assert_output_close(got[0, u * G + g:u * G + g + 1], o, f"u={u} g={g}")
