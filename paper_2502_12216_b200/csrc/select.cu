@@ -643,30 +643,31 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
           before = carry;
         }
         const int s0 = bs * SB, s1 = min(nex, s0 + SB);
-        float w[SB / 32];
+        constexpr int PER = SB / 32;  // consecutive slots per lane
+        float w[PER];
 #pragma unroll
-        for (int k = 0; k < SB / 32; ++k) {  // slot s0 + 4 lane + k: 4 consecutive per lane
-          const int s = s0 + 4 * lane + k;
+        for (int k = 0; k < PER; ++k) {
+          const int s = s0 + PER * lane + k;
           w[k] = s < s1 ? __expf(__ldcg(P.logits + (ub + g) * sc.slots + s) - m) : 0.f;
         }
 #pragma unroll
-        for (int k = 1; k < SB / 32; ++k) w[k] += w[k - 1];
-        float v = w[SB / 32 - 1];
+        for (int k = 1; k < PER; ++k) w[k] += w[k - 1];
+        float v = w[PER - 1];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const float x = __shfl_up_sync(0xffffffffu, v, o);
           if (lane >= o) v += x;
         }
-        const float excl = before + v - w[SB / 32 - 1];
-        int kl = SB / 32;
+        const float excl = before + v - w[PER - 1];
+        int kl = PER;
 #pragma unroll
-        for (int k = SB / 32 - 1; k >= 0; --k)
-          if (s0 + 4 * lane + k < s1 && excl + w[k] >= target) kl = k;
-        const unsigned hit = __ballot_sync(0xffffffffu, kl < SB / 32);
+        for (int k = PER - 1; k >= 0; --k)
+          if (s0 + PER * lane + k < s1 && excl + w[k] >= target) kl = k;
+        const unsigned hit = __ballot_sync(0xffffffffu, kl < PER);
         const int hl = hit ? __ffs(hit) - 1 : 31;
         const int kls = __shfl_sync(0xffffffffu, kl, hl);
         // k* = the 1-based rank of the crossing slot (rounding guard: the block's last slot)
-        const int kstar = hit ? s0 + 4 * hl + kls + 1 : s1;
+        const int kstar = hit ? s0 + PER * hl + kls + 1 : s1;
         J = 1 + warp_count_false(C - 1, [&](int r) { return eg[r] >= kstar; });
       } else {
         // past the head: cum(e_r) = EN + tail(e_r) at the cluster ends; the first cluster
