@@ -48,8 +48,11 @@ def _config(args, n_gpus):
                         f"1024 clusters/KV head, p={args.p}",
             "global_batch": n_gpus, "seq_len": CFG["n"], "n_clusters": CFG["C"], "p": args.p,
             "parallelism": f"batch x KV-head sharded over {n_gpus} GPU(s), no data-path collective",
-            "l2": "cold L2 before every timed step: 256 MiB buffer written, then a 256 MiB buffer read (write-back drained)",
-            "inputs": f"tactic-synth-v1 (synth/), {LAYERS} layers per GPU (seeds {LAYERS} rank + l), steps cycle over them"}
+            "l2": "cold L2 before every timed step: 256 MiB buffer written, then a 256 MiB buffer read (write-back drained); "
+                  "within a step each layer reads its own K/V (512 MB per layer > L2)",
+            "step": f"one decode step through all {LAYERS} synthetic layers, one CUDA graph, layers serialised "
+                    f"(no cross-layer overlap); value = step time / {LAYERS}",
+            "inputs": f"tactic-synth-v1 (synth/), {LAYERS} layers per GPU (seeds {LAYERS} rank + l)"}
 
 
 def _peaks():
@@ -350,27 +353,56 @@ def run_gpu(args, rank, world, local_rank):
             b.record()
         return evs
 
-    replays = [L["graph"].replay for L in layers]
-    timed_loop(replays, args.warmup)
+    # ---- one step = one decode step through all LAYERS synthetic layers, captured as ONE
+    # CUDA graph (as a serving engine captures its decode step); every layer's decode starts
+    # only after the previous layer's has completed (the entry kernel takes no programmatic
+    # dependency), each layer reads its own K/V (512 MB per layer > L2) and L2 is flushed
+    # before every step.  value = step time / LAYERS.
+    def model_graph(fn):
+        for L in layers:
+            fn(L)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for L in layers:
+                fn(L)
+        torch.cuda.synchronize()
+        return g
+
+    def per_layer_us(evs):
+        return 1e3 * float(np.mean([a.elapsed_time(b) for a, b in evs])) / len(layers)
+
+    gmodel = model_graph(lambda L: T.decode(L["q"], L["index"], args.p, out=L["out"]))
+    timed_loop([gmodel.replay], args.warmup)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
-        evs = timed_loop(replays, args.steps)
+        evs = timed_loop([gmodel.replay], args.steps)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         # keep the GPU busy a little longer for the clock sampler (not part of the number)
-        timed_loop(replays, min(args.steps, 200))
+        timed_loop([gmodel.replay], min(args.steps, 100))
         torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in evs]
-    ms = float(np.mean(step_ms))
+    ms = float(np.mean(step_ms)) / len(layers)   # per layer-step
+    ms_model_step = float(np.mean(step_ms))
+
+    # the same layer-step as its own graph (one graph launch per layer, as in r01)
+    replays = [L["graph"].replay for L in layers]
+    timed_loop(replays, 2 * LAYERS)
+    torch.cuda.synchronize()
+    iso_ev = timed_loop(replays, max(4 * LAYERS, min(args.steps, 200)))
+    torch.cuda.synchronize()
+    iso_us = 1e3 * float(np.mean([a.elapsed_time(b) for a, b in iso_ev]))
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms_model_step], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms_model_step = float(t.item())
+        ms = ms_model_step / len(layers)
 
     # ---- per-stage breakdown (selection / attention / merge), events between stages
     st = []
@@ -407,7 +439,13 @@ def run_gpu(args, rank, world, local_rank):
     torch.cuda.synchronize()
     devs = timed_loop(dgraphs, max(2 * LAYERS, min(args.steps, 100)))
     torch.cuda.synchronize()
-    dense_ms = float(np.mean([a.elapsed_time(b) for a, b in devs]))
+    dense_iso_ms = float(np.mean([a.elapsed_time(b) for a, b in devs]))
+    gdm = model_graph(lambda L: T.dense_decode(L["q"], L["K"], L["V"], out=L["dout"]))
+    timed_loop([gdm.replay], 3)
+    torch.cuda.synchronize()
+    dev_m = timed_loop([gdm.replay], max(10, min(args.steps, 50)))
+    torch.cuda.synchronize()
+    dense_ms = per_layer_us(dev_m) * 1e-3
     dense_bytes = 2 * units * n * 128 * 2 + 2 * units * G * 128 * 2
 
     # ---- e2e through the C ABI with host buffers (H2D q, D2H out inside the timed region)
@@ -489,23 +527,20 @@ def run_gpu(args, rank, world, local_rank):
     # ---- GQA union vs per-head loading (NEXT 2: union up to 1.65x faster)
     ablation = None
     if args.ablation and world == 1:
-        reps, own_tok, uni_tok = [], [], []
+        own_tok, uni_tok = [], []
         for L in layers:
-            o = torch.empty_like(L["q"])
-            T.decode_per_head(L["q"], L["index"], args.p, out=o)
-            gph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gph):
-                T.decode_per_head(L["q"], L["index"], args.p, out=o)
-            reps.append(gph.replay)
+            L["o_ph"] = torch.empty_like(L["q"])
+        gph = model_graph(lambda L: T.decode_per_head(L["q"], L["index"], args.p, out=L["o_ph"]))
+        for L in layers:
             dbg = T.decode_debug(L["q"], L["index"], args.p)
             for u in range(units):
                 uni_tok.append(int(L["sizes"][u][dbg["union_mask"][u].astype(bool)].sum()))
                 own_tok.append(sum(int(L["sizes"][u][dbg["order"][u, g][:dbg["J"][u, g]]].sum()) for g in range(G)))
-        timed_loop(reps, 2 * LAYERS)
+        timed_loop([gph.replay], 3)
         torch.cuda.synchronize()
-        ev = timed_loop(reps, max(4 * LAYERS, min(args.steps, 96)))
+        ev = timed_loop([gph.replay], max(10, min(args.steps, 50)))
         torch.cuda.synchronize()
-        ph_us = 1e3 * float(np.mean([a.elapsed_time(b) for a, b in ev]))
+        ph_us = per_layer_us(ev)
         ablation = {"per_head_us_per_layer_step": ph_us, "union_us_per_layer_step": ms * 1e3,
                     "union_speedup": ph_us / (ms * 1e3),
                     "kv_tokens_per_head_loading": float(np.sum(own_tok)) / len(layers),
@@ -517,19 +552,15 @@ def run_gpu(args, rank, world, local_rank):
     sweep = []
     if args.sweep and world == 1:
         for p in (0.5, 0.8, 0.9, 0.95, 0.99, 1.0):
-            reps = []
             for L in layers:
-                o = torch.empty_like(L["q"])
-                T.decode(L["q"], L["index"], p, out=o)
-                gp = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(gp):
-                    T.decode(L["q"], L["index"], p, out=o)
-                reps.append(gp.replay)
-            timed_loop(reps, 2 * LAYERS)
+                L["o_sw"] = torch.empty_like(L["q"])
+            gp = model_graph(lambda L: T.decode(L["q"], L["index"], p, out=L["o_sw"]))
+            timed_loop([gp.replay], 3)
             torch.cuda.synchronize()
-            ev = timed_loop(reps, max(4 * LAYERS, min(args.steps, 96)))
+            ev = timed_loop([gp.replay], max(10, min(args.steps, 50)))
             torch.cuda.synchronize()
-            us = 1e3 * float(np.mean([a.elapsed_time(b) for a, b in ev]))
+            us = per_layer_us(ev)
+            del gp
             uf = []
             for L in layers:
                 if p >= 1.0:
@@ -558,10 +589,10 @@ def run_gpu(args, rank, world, local_rank):
     value_us = ms * 1e3 / world
     line = {
         "metric": METRIC, "value": value_us, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_model_step, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": _config(args, world),
         # per decode step: score+rank, sample, fit, attention
-        "gpu_launches": (1 if args.p >= 1 else 4) * args.steps,
+        "gpu_launches": (1 if args.p >= 1 else 4) * LAYERS * args.steps,
         "roofline": {"bound": "hbm", "kernel": "attention_kernel<4,false> (S8 sparse split-KV)",
                      "achieved": att_gbs, "peak": hbm, "unit": "GB/s", "frac": att_gbs / hbm,
                      "traffic": traffic, "peak_source": peak_src,
@@ -572,6 +603,9 @@ def run_gpu(args, rank, world, local_rank):
         "dense": {"us_per_layer_step": dense_ms * 1e3, "gbs": dense_bytes / (dense_ms * 1e-3) / 1e9,
                   "frac": dense_bytes / (dense_ms * 1e-3) / 1e9 / hbm, "bytes": dense_bytes},
         "speedup_vs_dense": dense_ms / ms,
+        "isolated_layer_graph": {"us_per_layer_step": iso_us, "dense_us_per_layer_step": dense_iso_ms * 1e3,
+                                 "speedup_vs_dense": dense_iso_ms * 1e3 / iso_us,
+                                 "what": "each layer-step as its own CUDA graph, L2 flushed before each (includes one graph launch per layer)"},
         "p_sweep": sweep or None,
         "c3": c3,
         "c4_shard": c4,

@@ -34,9 +34,14 @@
 namespace tactic {
 
 constexpr int ATT_TILE = 64;
+// pipeline depth: 6 stages (192 KB) when the work lists are not staged in shared memory
+// (dense, global split), 4 when they are (the lists take the place of stages 4 and 5)
 constexpr int ATT_STAGES = 4;
+constexpr int ATT_LIST_STAGES = 4;
 constexpr int ATT_CWARPS = 4;
-constexpr int ATT_THREADS = 32 * (ATT_CWARPS + 1);
+// warp 0 producer, warps 1..ATT_CWARPS consumers, last warp the piece epilogue (global split)
+constexpr int ATT_THREADS = 32 * (ATT_CWARPS + 2);
+constexpr int ATT_EPI_WARP = ATT_CWARPS + 1;
 constexpr int ATT_STAGE_BYTES = ATT_TILE * 256 * 2;  // K + V
 constexpr int FLAG_FIRST = 1, FLAG_LAST = 2, FLAG_END = 4;
 
@@ -51,9 +56,15 @@ constexpr int SCRATCH_FLOATS = ATT_CWARPS * (8 * 128 + 16);
 // (or, when they fit, every unit's lists: one bulk copy of each array, no separate round
 // trip for the per-unit totals of the split)
 constexpr int LIST_INTS = 16400;
-constexpr size_t ATT_SMEM = (size_t)ATT_STAGES * ATT_STAGE_BYTES + ATT_STAGES * sizeof(StageMeta) +
-                            3 * ATT_STAGES * sizeof(uint64_t) + SCRATCH_FLOATS * sizeof(float) +
-                            LIST_INTS * sizeof(int) + 1024;
+constexpr size_t ATT_BODY = (size_t)ATT_STAGES * ATT_STAGE_BYTES >
+                                    (size_t)ATT_LIST_STAGES * ATT_STAGE_BYTES + LIST_INTS * sizeof(int)
+                                ? (size_t)ATT_STAGES * ATT_STAGE_BYTES
+                                : (size_t)ATT_LIST_STAGES * ATT_STAGE_BYTES + LIST_INTS * sizeof(int);
+constexpr size_t ATT_SMEM = ATT_BODY + ATT_STAGES * sizeof(StageMeta) + 4 * ATT_STAGES * sizeof(uint64_t) +
+                            SCRATCH_FLOATS * sizeof(float) + 1024;
+static_assert(ATT_BODY % 16 == 0, "stage metadata alignment");
+static_assert(ATT_SMEM <= 227 * 1024, "attention shared memory");
+static_assert(LIST_INTS >= 2 * SCRATCH_FLOATS, "epilogue buffers in the list area");
 
 size_t attention_smem_bytes() { return ATT_SMEM; }
 
@@ -92,6 +103,26 @@ __device__ __forceinline__ int warp_floor_search(const T* arr, int count, T key)
     len = (nb + stride < end ? nb + stride : end) - nb;
   }
   const bool ok = lane < len && arr[base + lane] <= key;
+  const unsigned bal = __ballot_sync(0xffffffffu, ok);
+  return base + (31 - __clz(bal));
+}
+
+// warp_floor_search over arr[i] + i x (arr non-decreasing, x >= 0)
+__device__ __forceinline__ int warp_floor_search_off(const long long* arr, int count, long long key, long long x) {
+  const int lane = threadIdx.x & 31;
+  int base = 0, len = count;
+  while (len > 32) {
+    const int stride = (len + 31) >> 5;
+    const int idx = base + lane * stride;
+    const bool ok = idx < base + len && arr[idx] + (long long)idx * x <= key;
+    const unsigned bal = __ballot_sync(0xffffffffu, ok);
+    const int h = 31 - __clz(bal);
+    const int nb = base + h * stride;
+    const int end = base + len;
+    base = nb;
+    len = (nb + stride < end ? nb + stride : end) - nb;
+  }
+  const bool ok = lane < len && arr[base + lane] + (long long)(base + lane) * x <= key;
   const unsigned bal = __ballot_sync(0xffffffffu, ok);
   return base + (31 - __clz(bal));
 }
@@ -165,11 +196,84 @@ __device__ __forceinline__ UnitSplit unit_split_of(const AttnArgs& a, int cta, i
   return r;
 }
 
+// S9 for one head g of unit u (global split): LSE-weighted merge of the partial slots
+// c0 + i + soff, i < span (ranges that held no token of the unit are skipped), by one warp;
+// lanes hold 4 dims.  Piece weights are computed 32 at a time (one per lane) and
+// broadcast, so the o loads are independent; chunks of 32 pieces: the lane's piece lse and
+// the chunk's first 16 partial rows are loaded together, the running max is rescaled
+// online across chunks.
+template <int G>
+__device__ __forceinline__ void merge_head_global(const AttnArgs& a, int u, int g, int c0, int span, int soff,
+                                               bool unit_mode, long long T, int P) {
+  const int lane = threadIdx.x & 31;
+  float mx = -INFINITY, sum = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i0 = 0; i0 < span; i0 += 32) {
+    const int i = i0 + lane;
+    const bool live = i < span && (unit_mode || T >= P ||
+                                   range_start(c0 + i, T, P) != range_start(c0 + i + 1, T, P));
+    const unsigned lmask = __ballot_sync(0xffffffffu, live);
+    const int cnt = span - i0 < 32 ? span - i0 : 32;
+    const float l = live ? __ldcg(a.part_lse + ((size_t)(c0 + i) + soff) * G + g) : -INFINITY;
+    float4 v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const float4* src =
+          reinterpret_cast<const float4*>(a.part_o + (((size_t)(c0 + i0 + k) + soff) * G + g) * 128) + lane;
+      v[k] = (k < cnt && ((lmask >> k) & 1u)) ? __ldcg(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float nm = fmaxf(mx, warp_max(l));
+    const float sc = mx == -INFINITY ? 0.f : __expf(mx - nm);
+    acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
+    sum *= sc;
+    mx = nm;
+    const float wl = (live && l > -INFINITY) ? __expf(l - mx) : 0.f;
+    sum += warp_sum(wl);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const float w = __shfl_sync(0xffffffffu, wl, k);
+      acc.x = fmaf(w, v[k].x, acc.x);
+      acc.y = fmaf(w, v[k].y, acc.y);
+      acc.z = fmaf(w, v[k].z, acc.z);
+      acc.w = fmaf(w, v[k].w, acc.w);
+    }
+    if (cnt > 16) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int j = 16 + k;
+        const float4* src =
+            reinterpret_cast<const float4*>(a.part_o + (((size_t)(c0 + i0 + j) + soff) * G + g) * 128) + lane;
+        v[k] = (j < cnt && ((lmask >> j) & 1u)) ? __ldcg(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float w = __shfl_sync(0xffffffffu, wl, 16 + k);
+        acc.x = fmaf(w, v[k].x, acc.x);
+        acc.y = fmaf(w, v[k].y, acc.y);
+        acc.z = fmaf(w, v[k].z, acc.z);
+        acc.w = fmaf(w, v[k].w, acc.w);
+      }
+    }
+  }
+  const float inv = 1.f / sum;
+  const size_t orow = ((size_t)u * G + g) * 128 + lane * 4;
+  if (a.out) {
+    __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(a.out + orow);
+    ob[0] = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+    ob[1] = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+  }
+  if (a.out_f32)
+    *reinterpret_cast<float4*>(a.out_f32 + orow) =
+        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+  if (a.lse && lane == 0) a.lse[(size_t)u * G + g] = mx + logf(sum);
+}
+
 // the unit-aligned split's merge stages the unit's contiguous partials in the idle stage
 // buffers (a CTA of that split holds one piece, so no copy is in flight at its end)
 template <int G>
 __device__ __forceinline__ bool smem_merge_ok(bool unit_mode, int np) {
-  return unit_mode && np * G * 4 + 16 <= 1024 && (size_t)np * G * 512 + 1024 <= (size_t)ATT_STAGES * ATT_STAGE_BYTES;
+  return unit_mode && np * G * 4 + 16 <= 1024 &&
+         (size_t)np * G * 512 + 1024 <= (size_t)ATT_LIST_STAGES * ATT_STAGE_BYTES;
 }
 
 template <int G, bool DENSE>
@@ -179,18 +283,24 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* stages = smem;
-  StageMeta* meta = (StageMeta*)(stages + ATT_STAGES * ATT_STAGE_BYTES);
+  StageMeta* meta = (StageMeta*)(stages + ATT_BODY);
   uint64_t* full = (uint64_t*)(meta + ATT_STAGES);
   uint64_t* empty = full + ATT_STAGES;
-  uint64_t* mbar = empty + ATT_STAGES;  // [0]: merge staging (unit-aligned split)
-  float* scratch = (float*)(empty + 2 * ATT_STAGES);
-  int* s_list = (int*)(scratch + SCRATCH_FLOATS);  // seg_row [C] | seg_prefix [C+1]
+  uint64_t* mbar = empty + ATT_STAGES;  // [0]: merge staging, [1]: lists, [2..5]: epilogue
+  uint64_t* ep_full = mbar + 2;          // [2] piece handed to the epilogue warp (global split)
+  uint64_t* ep_empty = mbar + 4;         // [2] epilogue buffer free again
+  float* scratch = (float*)(empty + 3 * ATT_STAGES);
+  int* s_list = (int*)(stages + ATT_LIST_STAGES * ATT_STAGE_BYTES);  // seg_row [C] | seg_prefix [C+1]
+  // global split (no lists in smem): two piece buffers for the epilogue warp in the list area
+  float* ep_buf = (float*)s_list;
   __shared__ int s_merge;
+  __shared__ int ep_meta[2];  // unit of the piece in each epilogue buffer; -1: end of stream
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) tl_mark(a.tlog, 4, 0, blockIdx.x == 0);
   // zero the stage buffers once: never-written slots must hold finite values (0 * NaN)
-  for (int i = threadIdx.x; i < ATT_STAGES * ATT_STAGE_BYTES / 16; i += ATT_THREADS)
+  const int nst = (!DENSE && a.unit_split != 0) ? ATT_LIST_STAGES : ATT_STAGES;  // stages in use
+  for (int i = threadIdx.x; i < nst * ATT_STAGE_BYTES / 16; i += ATT_THREADS)
     reinterpret_cast<uint4*>(stages)[i] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     for (int i = 0; i < ATT_STAGES; ++i) {
@@ -199,6 +309,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     }
     mbar_init(mbar, 1);
     mbar_init(mbar + 1, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&ep_full[i], ATT_CWARPS);
+      mbar_init(&ep_empty[i], 1);
+    }
     fence_barrier_init();
   }
   fence_proxy_async_smem();
@@ -249,7 +363,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   UnitSplit us_ = {0, 0, 1, 0, 0};
   if (unit_mode) us_ = unit_split_of<DENSE>(a, cta, P, pref_src);
   if (threadIdx.x == 0) stamp(40);
-  const long long T = unit_mode ? 0 : (DENSE ? dense_total : a.unit_prefix[a.units]);
+  // sparse global split: every unit carries ATT_PIECE_TOKENS virtual tokens after its work
+  // list, so the split prices the fixed cost of a piece (combine, arrival, merge); a CTA
+  // whose range holds only virtual tokens of a unit contributes an empty piece
+  const long long X = (!DENSE && !unit_mode) ? ATT_PIECE_TOKENS : 0;
+  auto vpre = [&](int v) -> long long { return a.unit_prefix[v] + (long long)v * X; };
+  const long long T = unit_mode ? 0 : (DENSE ? dense_total : vpre(a.units));
   // unit-aligned sparse split: the CTA's unit's whole work list into smem with one round
   // trip of independent loads (all threads), so the producer's segment search and run
   // walk never wait on L2
@@ -297,19 +416,22 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       bulk_g2s(sK + slot * 256, kb, (uint32_t)len * 256u, bar);
       bulk_g2s(sV + slot * 256, vb, (uint32_t)len * 256u, bar);
     };
-    long long t = unit_mode ? 0 : range_start(cta, T, P);
-    const long long t_end = unit_mode ? 0 : range_start(cta + 1, T, P);
     int stage = 0;
     uint32_t phase = 0;
+    // the global split: CTA cta covers tokens [rs(cta), rs(cta + 1)) of the unit stream
+    long long t = unit_mode ? 0 : range_start(cta, T, P);
+    const long long t_end = unit_mode ? 0 : range_start(cta + 1, T, P);
     int u = us_.u;
     if (!unit_mode && t < t_end) {
       if (DENSE) {
         u = (int)(t / a.n);
-      } else {  // largest u with unit_prefix[u] <= t
-        u = warp_floor_search<long long>(a.unit_prefix, a.units, t);
+      } else {  // largest u with unit_prefix[u] + u X <= t
+        u = warp_floor_search_off(a.unit_prefix, a.units, t, X);
       }
     }
     bool more = unit_mode || t < t_end;
+    bool pf_ok = false;
+    int pf_row = 0, pf_end = 0, pf_tot = 0;
     while (more) {
       long long pend = 0;
       int lt, le;
@@ -317,13 +439,18 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         lt = us_.lo;
         le = us_.hi;
       } else {
-        const long long ubase = DENSE ? (long long)u * a.n : a.unit_prefix[u];
-        const long long uend = DENSE ? ubase + a.n : a.unit_prefix[u + 1];
+        const long long ubase = DENSE ? (long long)u * a.n : vpre(u);
+        const long long uend = DENSE ? ubase + a.n : vpre(u + 1);
         pend = uend < t_end ? uend : t_end;
         lt = (int)(t - ubase);
         le = (int)(pend - ubase);
+        if (X) {  // clip the virtual tokens
+          const int real = (int)(a.unit_prefix[u + 1] - a.unit_prefix[u]);
+          lt = lt < real ? lt : real;
+          le = le < real ? le : real;
+        }
       }
-      if (lt >= le) {  // empty piece (unit mode, T_v < n_v): a partial with no tokens
+      if (lt >= le) {  // empty piece (T_v < n_v, or virtual tokens only): no tokens
         mbar_wait(&empty[stage], phase ^ 1);
         if (leader) {
           meta[stage].mask = 0;
@@ -331,8 +458,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           meta[stage].flags = FLAG_FIRST | FLAG_LAST;
           mbar_arrive(&full[stage]);
         }
-        if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
-        break;
+        if (++stage == nst) { stage = 0; phase ^= 1; }
+        if (unit_mode) break;
+        t = pend;
+        ++u;
+        more = t < t_end;
+        pf_ok = false;
+        continue;
       }
       // sparse: run table window of 32 segments (lane i holds segment k0 + i)
       const int* seg_row = all_lists ? s_list + (size_t)u * a.C
@@ -341,10 +473,16 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
                             : list_smem ? s_list + a.C : a.seg_prefix + (size_t)u * (a.C + 1);
       int k = 0, k0 = 0, row = 0, left = 0, w_row = 0, w_end = 0;
       // the unit's list tokens; tokens past them are the recent-token tail (rows n..)
-      const int ltot = DENSE ? 0 : seg_pref[a.C];
+      const bool use_pf = !DENSE && pf_ok;  // this unit's head window was prefetched (lt = 0)
+      const int ltot = DENSE ? 0 : (use_pf ? pf_tot : seg_pref[a.C]);
       if (!DENSE && lt >= ltot) {
         row = a.n + (lt - ltot);
         left = ltot + a.tail_len - lt;
+      } else if (use_pf) {  // lt = 0: window at segment 0 (empty segments are stepped over)
+        w_row = pf_row;
+        w_end = pf_end;
+        row = __shfl_sync(0xffffffffu, w_row, 0);
+        left = __shfl_sync(0xffffffffu, w_end, 0);
       } else if (!DENSE) {
         if (leader) stamp(43);
         k = k0 = warp_floor_search<int>(seg_pref, a.C, lt);  // largest k with seg_pref[k] <= lt
@@ -354,6 +492,17 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         row = __shfl_sync(0xffffffffu, w_row, 0) + (lt - sp);
         left = __shfl_sync(0xffffffffu, w_end, 0) - lt;
         if (leader) stamp(44);
+      }
+      // global split: when the range runs on into unit u + 1, load that unit's head window
+      // now, so the unit switch does not wait on L2 (consumed in the next iteration)
+      pf_ok = false;
+      if (!DENSE && !unit_mode && pend < t_end && u + 1 < a.units) {
+        const int* nr = a.seg_row + (size_t)(u + 1) * a.C;
+        const int* npf = a.seg_prefix + (size_t)(u + 1) * (a.C + 1);
+        pf_row = lane < a.C ? __ldcg(nr + lane) : 0;
+        pf_end = lane < a.C ? __ldcg(npf + lane + 1) : 0;
+        pf_tot = __ldcg(npf + a.C);
+        pf_ok = true;
       }
       bool first = true;
       while (lt < le) {
@@ -423,7 +572,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         first = false;
         if (leader && ntile_dbg < 16) stamp(2 + ntile_dbg);
         ++ntile_dbg;
-        if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
+        if (++stage == nst) { stage = 0; phase ^= 1; }
       }
       if (unit_mode) break;
       t = pend;
@@ -441,6 +590,67 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     return;
   }
 
+  if (warp == ATT_EPI_WARP) {
+    // ============================ piece epilogue (global split) ============================
+    // The consumers hand each finished piece (per-warp m, l, o) over in one of two smem
+    // buffers and go on streaming; this warp combines it across the consumer warps, writes
+    // the partial, counts the unit's arrival and, for the unit's last piece, merges (S9).
+    if (unit_mode) return;  // one piece per CTA: the consumers finish it themselves
+    for (int ne = 0;; ++ne) {
+      const int b = ne & 1;
+      mbar_wait(&ep_full[b], (uint32_t)((ne >> 1) & 1));
+      const int u = ep_meta[b];
+      if (u < 0) break;
+      const size_t slot = (size_t)cta + u;  // cta + unit: unique per piece (ranges are contiguous)
+      const float* base = ep_buf + b * SCRATCH_FLOATS;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float mw[ATT_CWARPS], mf = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < ATT_CWARPS; ++w) {
+          mw[w] = base[w * (8 * 128 + 16) + 8 * 128 + g];
+          mf = fmaxf(mf, mw[w]);
+        }
+        const bool none = mf == -INFINITY;  // empty piece: zero weight in the merge
+        float lf = 0.f;
+        float4 of = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int w = 0; w < ATT_CWARPS; ++w) {
+          const float* sww = base + w * (8 * 128 + 16);
+          const float e = none ? 0.f : exp2f(mw[w] - mf);
+          lf += sww[8 * 128 + 8 + g] * e;
+          const float4 v = reinterpret_cast<const float4*>(sww + g * 128)[lane];
+          of.x = fmaf(v.x, e, of.x);
+          of.y = fmaf(v.y, e, of.y);
+          of.z = fmaf(v.z, e, of.z);
+          of.w = fmaf(v.w, e, of.w);
+        }
+        const float il = none ? 0.f : 1.f / lf;
+        reinterpret_cast<float4*>(a.part_o + (slot * G + g) * 128)[lane] =
+            make_float4(of.x * il, of.y * il, of.z * il, of.w * il);
+        if (lane == 0) a.part_lse[slot * G + g] = none ? -INFINITY : (mf + log2f(lf)) * 0.6931471805599453f;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ep_empty[b]);
+      // arrival: __syncwarp orders the lanes' partial stores before lane 0's gpu-scope
+      // release; the last arrival acquires, and __syncwarp passes that on to the lanes
+      const long long us = DENSE ? (long long)u * a.n : vpre(u);
+      const long long ue = DENSE ? us + a.n : vpre(u + 1);
+      int c0 = 0;
+      const int np = pieces_of_unit(us, ue, T, P, &c0);
+      int last = 0;
+      if (lane == 0) last = atom_add_acq_rel_gpu(&a.unit_cnt[u], 1) == np - 1;
+      last = __shfl_sync(0xffffffffu, last, 0);
+      __syncwarp();
+      if (last) {
+        const int span = cta_of(ue - 1, T, P) - c0 + 1;
+        for (int g = 0; g < G; ++g) merge_head_global<G>(a, u, g, c0, span, u, false, T, P);
+        if (lane == 0) a.unit_cnt[u] = 0;  // self-reset for the next call
+      }
+    }
+    return;
+  }
+
   // ============================ consumers ============================
   const int cw = warp - 1;
   const int ct = threadIdx.x - 32;          // 0..127 consumer thread index
@@ -451,6 +661,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   float o[8][4];
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
   int cur_unit = -1;
+  int ep_n = 0;  // pieces handed to the epilogue warp
   int stage = 0;
   uint32_t phase = 0;
 
@@ -533,9 +744,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
-    if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
+    if (++stage == nst) { stage = 0; phase ^= 1; }
 
     if (md.flags & FLAG_LAST) {
+      unsigned long long t_last0 = 0;
+      if (a.tlog && ct == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_last0));
       // ---- cross-warp combine of this piece -> partial slot (cta + unit)
       float L0 = l0, L1 = l1;
 #pragma unroll
@@ -543,7 +756,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         L0 += __shfl_xor_sync(0xffffffffu, L0, off);
         L1 += __shfl_xor_sync(0xffffffffu, L1, off);
       }
-      float* sw = scratch + cw * (8 * 128 + 16);
+      int ep_b = 0;
+      if (!unit_mode) {  // hand the piece to the epilogue warp (buffer ep_n & 1)
+        ep_b = ep_n & 1;
+        mbar_wait(&ep_empty[ep_b], (uint32_t)(((ep_n >> 1) & 1) ^ 1));
+      }
+      float* sw = (unit_mode ? scratch : ep_buf + ep_b * SCRATCH_FLOATS) + cw * (8 * 128 + 16);
       if (lane < 4) {
         sw[8 * 128 + h0] = m0;
         sw[8 * 128 + h0 + 1] = m1;
@@ -558,6 +776,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         sw[h0 * 128 + d0 + 8] = o[mt][2];
         sw[(h0 + 1) * 128 + d0 + 8] = o[mt][3];
       }
+      if (!unit_mode) {
+        if (ct == 0) ep_meta[ep_b] = md.unit;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ep_full[ep_b]);
+        ++ep_n;
+      }
+     if (unit_mode) {
       asm volatile("bar.sync 1, %0;" ::"n"(ATT_CWARPS * 32));
       const int u = md.unit;
       // partial slot: the CTA index (unit-aligned split: one piece per CTA) or cta + unit
@@ -587,8 +812,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       long long ue = 0;
       int c0 = cta - us_.j, np = us_.n;
       if (!unit_mode) {
-        const long long us = DENSE ? (long long)u * a.n : a.unit_prefix[u];
-        ue = DENSE ? us + a.n : a.unit_prefix[u + 1];
+        const long long us = DENSE ? (long long)u * a.n : vpre(u);
+        ue = DENSE ? us + a.n : vpre(u + 1);
         np = pieces_of_unit(us, ue, T, P, &c0);
       }
       if (ct == 0) {
@@ -615,25 +840,57 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       if (s_merge && smem_merge_ok<G>(unit_mode, np)) {
         // ---- S9 (unit-aligned split): merge the staged pieces from shared memory
         mbar_wait(mbar, 0);
-        const float* sl = reinterpret_cast<const float*>(stages) + ((c0 * G) & 3);
-        const float* so = reinterpret_cast<const float*>(stages + 1024);
+        if (a.tlog && ct == 0 && u < 8) {  // debug: pieces staged
+          unsigned long long t_;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+          a.tlog[980 + u] = t_;
+          a.tlog[990 + u] = (unsigned long long)np;
+        }
+        float* sl = reinterpret_cast<float*>(stages) + ((c0 * G) & 3);
+        const float4* so = reinterpret_cast<const float4*>(stages + 1024);
         for (int g = cw; g < G; g += ATT_CWARPS) {
           float mx = -INFINITY;
           for (int i = lane; i < np; i += 32) mx = fmaxf(mx, sl[i * G + g]);
           mx = warp_max(mx);
+          // piece weights one per lane, written over the lse they come from (each element
+          // is read and written by the same lane), then the o rows in two FMA chains
           float sum = 0.f;
-          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-          for (int i = 0; i < np; ++i) {
+          for (int i = lane; i < np; i += 32) {
             const float l = sl[i * G + g];
             const float w = l > -INFINITY ? __expf(l - mx) : 0.f;
-            const float4 v = reinterpret_cast<const float4*>(so + ((size_t)i * G + g) * 128)[lane];
+            sl[i * G + g] = w;
             sum += w;
-            acc.x = fmaf(w, v.x, acc.x);
-            acc.y = fmaf(w, v.y, acc.y);
-            acc.z = fmaf(w, v.z, acc.z);
-            acc.w = fmaf(w, v.w, acc.w);
           }
+          sum = warp_sum(sum);
+          __syncwarp();
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = make_float4(0.f, 0.f, 0.f, 0.f);
+          int i = 0;
+#pragma unroll 2
+          for (; i + 1 < np; i += 2) {
+            const float w0 = sl[i * G + g], w1 = sl[(i + 1) * G + g];
+            const float4 v0 = so[((size_t)i * G + g) * 32 + lane];
+            const float4 v1 = so[((size_t)(i + 1) * G + g) * 32 + lane];
+            acc.x = fmaf(w0, v0.x, acc.x);
+            acc.y = fmaf(w0, v0.y, acc.y);
+            acc.z = fmaf(w0, v0.z, acc.z);
+            acc.w = fmaf(w0, v0.w, acc.w);
+            acc1.x = fmaf(w1, v1.x, acc1.x);
+            acc1.y = fmaf(w1, v1.y, acc1.y);
+            acc1.z = fmaf(w1, v1.z, acc1.z);
+            acc1.w = fmaf(w1, v1.w, acc1.w);
+          }
+          if (i < np) {
+            const float w0 = sl[i * G + g];
+            const float4 v0 = so[((size_t)i * G + g) * 32 + lane];
+            acc.x = fmaf(w0, v0.x, acc.x);
+            acc.y = fmaf(w0, v0.y, acc.y);
+            acc.z = fmaf(w0, v0.z, acc.z);
+            acc.w = fmaf(w0, v0.w, acc.w);
+          }
+          acc.x += acc1.x;
+          acc.y += acc1.y;
+          acc.z += acc1.z;
+          acc.w += acc1.w;
           const float inv = 1.f / sum;
           const size_t orow = ((size_t)u * G + g) * 128 + lane * 4;
           if (a.out) {
@@ -658,71 +915,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         // 32 at a time (one per lane) and broadcast, so the o loads are independent.
         const int span = unit_mode ? np : cta_of(ue - 1, T, P) - c0 + 1;
         const int soff = unit_mode ? 0 : u;  // slot = c + soff
-        for (int g = cw; g < G; g += ATT_CWARPS) {
-          // chunks of 32 pieces: the lane's piece lse and the chunk's first 16 partial rows
-          // are loaded together (the row loads do not depend on the lse), the running max
-          // is rescaled online across chunks
-          float mx = -INFINITY, sum = 0.f;
-          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (int i0 = 0; i0 < span; i0 += 32) {
-            const int i = i0 + lane;
-            const bool live = i < span && (unit_mode || T >= P ||
-                                           range_start(c0 + i, T, P) != range_start(c0 + i + 1, T, P));
-            const unsigned lmask = __ballot_sync(0xffffffffu, live);
-            const int cnt = span - i0 < 32 ? span - i0 : 32;
-            const float l = live ? __ldcg(a.part_lse + ((size_t)(c0 + i) + soff) * G + g) : -INFINITY;
-            float4 v[16];
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const float4* src =
-                  reinterpret_cast<const float4*>(a.part_o + (((size_t)(c0 + i0 + k) + soff) * G + g) * 128) + lane;
-              v[k] = (k < cnt && ((lmask >> k) & 1u)) ? __ldcg(src) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            const float nm = fmaxf(mx, warp_max(l));
-            const float sc = mx == -INFINITY ? 0.f : __expf(mx - nm);
-            acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
-            sum *= sc;
-            mx = nm;
-            const float wl = (live && l > -INFINITY) ? __expf(l - mx) : 0.f;
-            sum += warp_sum(wl);
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const float w = __shfl_sync(0xffffffffu, wl, k);
-              acc.x = fmaf(w, v[k].x, acc.x);
-              acc.y = fmaf(w, v[k].y, acc.y);
-              acc.z = fmaf(w, v[k].z, acc.z);
-              acc.w = fmaf(w, v[k].w, acc.w);
-            }
-            if (cnt > 16) {
-#pragma unroll
-              for (int k = 0; k < 16; ++k) {
-                const int j = 16 + k;
-                const float4* src =
-                    reinterpret_cast<const float4*>(a.part_o + (((size_t)(c0 + i0 + j) + soff) * G + g) * 128) + lane;
-                v[k] = (j < cnt && ((lmask >> j) & 1u)) ? __ldcg(src) : make_float4(0.f, 0.f, 0.f, 0.f);
-              }
-#pragma unroll
-              for (int k = 0; k < 16; ++k) {
-                const float w = __shfl_sync(0xffffffffu, wl, 16 + k);
-                acc.x = fmaf(w, v[k].x, acc.x);
-                acc.y = fmaf(w, v[k].y, acc.y);
-                acc.z = fmaf(w, v[k].z, acc.z);
-                acc.w = fmaf(w, v[k].w, acc.w);
-              }
-            }
-          }
-          const float inv = 1.f / sum;
-          const size_t orow = ((size_t)u * G + g) * 128 + lane * 4;
-          if (a.out) {
-            __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(a.out + orow);
-            ob[0] = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
-            ob[1] = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
-          }
-          if (a.out_f32)
-            *reinterpret_cast<float4*>(a.out_f32 + orow) =
-                make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-          if (a.lse && lane == 0) a.lse[(size_t)u * G + g] = mx + logf(sum);
-        }
+        for (int g = cw; g < G; g += ATT_CWARPS) merge_head_global<G>(a, u, g, c0, span, soff, unit_mode, T, P);
         if (ct == 0) a.unit_cnt[u] = 0;  // self-reset for the next call
         if (a.tlog && ct == 0 && u < 8) {
           unsigned long long t_;
@@ -730,11 +923,26 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           a.tlog[965 + 2 * u] = t_;
         }
       }
+     }
+      if (a.tlog && ct == 0 && cta < 148) {  // debug: time in piece ends / merges, merge count
+        unsigned long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+        a.tlog[2100 + cta] += t_ - t_last0;
+        a.tlog[2300 + cta] += (unit_mode && s_merge) ? 1ull : 0ull;
+        a.tlog[2500 + cta] += 1ull;
+      }
       m0 = m1 = -INFINITY;
       l0 = l1 = 0.f;
 #pragma unroll
       for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
     }
+  }
+  if (!unit_mode) {  // end marker for the epilogue warp
+    const int b = ep_n & 1;
+    mbar_wait(&ep_empty[b], (uint32_t)(((ep_n >> 1) & 1) ^ 1));
+    if (ct == 0) ep_meta[b] = -1;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ep_full[b]);
   }
   if (ct == 0) stamp(34);
   if (a.tlog && ct == 0 && 2 * cta + 1 < 512) {

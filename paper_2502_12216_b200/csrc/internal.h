@@ -33,7 +33,7 @@ inline bool unit_split_ok(int units, int ctas) { return 2 * units <= ctas; }
 // griddepcontrol.wait, last CTA end (atomicMax); k = 0 score, 1 rank, 2 sample, 3 fit,
 // 4 attention
 constexpr int TL_BASE = 1536;
-inline size_t tlog_entries(int units) { return (size_t)(units * 128 > 2048 ? units * 128 : 2048); }
+inline size_t tlog_entries(int units) { return (size_t)(units * 128 > 4096 ? units * 128 : 4096); }
 #ifdef __CUDACC__
 // what: 0 start, 1 past the wait (first CTA only), 2 end (every CTA; the max survives).
 // Called by one thread per CTA.
@@ -119,6 +119,10 @@ namespace tactic {
 
 
 // ---- attention (attention.cu)
+// sparse global split: virtual tokens per unit that stand for a piece's fixed cost
+// (the epilogue warp takes the combine, arrival and merge off the consumers; what is left
+// is the pipeline bubble at a unit switch and the epilogue backlog of short pieces)
+constexpr int ATT_PIECE_TOKENS = 128;
 struct AttnArgs {
   const __nv_bfloat16* q;          // [units][G][128]
   const __nv_bfloat16* Kp;         // sparse mode: swizzled [units][n][128]

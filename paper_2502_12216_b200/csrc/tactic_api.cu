@@ -576,12 +576,15 @@ static tactic_status_t run_selection(const void* q, tactic_index_t idx, double p
   sa.gmax = gmax;
   sa.gmass = gmass;
   sa.local_max = local_max;
+  // The entry kernel waits for everything before it on the stream to complete (no PDL):
+  // a caller's preceding kernel produces q.  The later kernels overlap their prologues
+  // with the previous kernel's tail through programmatic dependent launch.
   const bool pdl = true;
   if (mode != 1) {
-    CK(launch_score_rank(sa.q, idx, s, pdl));  // S1, S2, S3 (+ sampled-slot row map)
+    CK(launch_score_rank(sa.q, idx, s, false));  // S1, S2, S3 (+ sampled-slot row map)
     CK(launch_sample(sa, s, pdl));             // S4 (+ per-block fit summaries)
   } else {
-    CK(launch_score(sa, s, pdl));              // S1 only (sharded stage 2)
+    CK(launch_score(sa, s, false));            // S1 only (sharded stage 2)
   }
   if (mode == 0) CK(launch_fit(sa, s, pdl));     // S5-S7
   else CK(launch_select(sa, s, pdl));            // sharded stage rules
@@ -589,7 +592,8 @@ static tactic_status_t run_selection(const void* q, tactic_index_t idx, double p
 }
 
 static tactic_status_t run_attention(const void* q, tactic_index_t idx, bool all, cudaStream_t s, void* out,
-                                     float* out_f32, float* lse, cudaEvent_t ev_mid = nullptr) {
+                                     float* out_f32, float* lse, cudaEvent_t ev_mid = nullptr,
+                                     bool entry = false) {
   AttnArgs aa = {};
   aa.q = (const __nv_bfloat16*)q;
   aa.Kp = idx->Kp;
@@ -613,7 +617,7 @@ static tactic_status_t run_attention(const void* q, tactic_index_t idx, bool all
   aa.Vt = idx->Vt;
   aa.tail_len = idx->tail_len;
   aa.tail_cap = idx->tail_cap;
-  CK(launch_attention_sparse(aa, idx->G, idx->num_ctas, s, ev_mid == nullptr));  // S8 + fused S9
+  CK(launch_attention_sparse(aa, idx->G, idx->num_ctas, s, ev_mid == nullptr && !entry));  // S8 + fused S9
   if (ev_mid) CK(cudaEventRecord(ev_mid, s));
   return TACTIC_OK;
 }
@@ -628,7 +632,7 @@ tactic_status_t tactic_decode_ex(const void* q, tactic_index_t idx, float p, voi
   tactic_status_t st = check_p(p);
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  if (p >= 1.0f) return run_attention(q, idx, true, s, out, nullptr, lse);  // reading 15
+  if (p >= 1.0f) return run_attention(q, idx, true, s, out, nullptr, lse, nullptr, true);  // reading 15
   if ((st = run_selection(q, idx, (double)p, 0, s, nullptr, nullptr, nullptr))) return st;
   return run_attention(q, idx, false, s, out, nullptr, lse);
 }
@@ -826,7 +830,7 @@ tactic_status_t tactic_dense_decode(const void* q, const void* K, const void* V,
   aa.out = (__nv_bfloat16*)out;
   aa.lse = lse;
   aa.unit_split = unit_split_ok((int)units, P);
-  CK(launch_attention_dense(aa, &mk, &mv, r.G, P, s, true));  // S10 + fused merge
+  CK(launch_attention_dense(aa, &mk, &mv, r.G, P, s, false));  // S10 + fused merge (entry: no PDL)
   return TACTIC_OK;
 }
 

@@ -10,6 +10,7 @@ import sys
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between calls")
+ap.add_argument("--c3", action="store_true", help="C3 workload (batch 64, 32K, C = 256) instead of C2")
 args = ap.parse_args()
 os.environ["TACTIC_TLOG"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -23,11 +24,18 @@ from synth import make_layer  # noqa: E402
 B.build()
 from paper_2502_12216_b200 import tactic as T  # noqa: E402
 
-G, n, C = 4, 131072, 1024
-K, V, q = make_layer(1, 8, G, n, seed=0)
-to = lambda a: torch.from_numpy(a).cuda().to(torch.bfloat16)  # noqa: E731
-Kd, Vd, qd = to(K), to(V), to(q)
-idx = T.build_index(Kd, Vd, C, 10, group_size=G)
+if args.c3:
+    import bench  # noqa: E402
+    G, n, C = 4, 32768, 256
+    L = bench.make_layers([9000], torch.device("cuda", 0), B=64, Hkv=8, n=n)[0]
+    Kd, Vd, qd = L["K"], L["V"], L["q"]
+    idx = T.build_index(Kd, Vd, C, 10, group_size=G, seed=9000)
+else:
+    G, n, C = 4, 131072, 1024
+    K, V, q = make_layer(1, 8, G, n, seed=0)
+    to = lambda a: torch.from_numpy(a).cuda().to(torch.bfloat16)  # noqa: E731
+    Kd, Vd, qd = to(K), to(V), to(q)
+    idx = T.build_index(Kd, Vd, C, 10, group_size=G)
 R = 0  # multi-kernel selection (the only path)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 out = torch.empty_like(qd)
@@ -43,6 +51,10 @@ for it in range(4):
     graph.replay()
     torch.cuda.synchronize()
     full = idx.debug_timing().astype(np.int64).reshape(-1)
+    acc_now = full[2100:2700].copy()  # per-CTA accumulators: report this call's increment
+    if it > 0:
+        full[2100:2700] -= acc_prev
+    acc_prev = acc_now
     if it < 2:
         continue
     print(f"--- iteration {it}")
@@ -102,6 +114,17 @@ for it in range(4):
             order = np.argsort(-en)[:8]
             print("   slowest CTAs (cta, end us, tiles):", [(int(c), round(float(en[c]), 2), int(nt_[c])) for c in order])
             print("   tiles per CTA: min %d median %d max %d" % (nt_.min(), np.median(nt_), nt_.max()))
+            pe = full[2100:2248] / 1e3
+            nm_ = full[2300:2448]
+            npc_ = full[2500:2648]
+            print("   piece-end us per CTA: min %.2f median %.2f max %.2f; merges per CTA: min %d median %d max %d; "
+                  "pieces per CTA: median %d" % (pe.min(), np.median(pe), pe.max(), nm_.min(), np.median(nm_), nm_.max(),
+                                                 np.median(npc_)))
+            print("   slowest CTAs (cta, end, piece-end us, merges, pieces):",
+                  [(int(c), round(float(en[c]), 1), round(float(pe[c]), 2), int(nm_[c]), int(npc_[c])) for c in order])
+            fast = np.argsort(en)[:5]
+            print("   fastest CTAs (cta, end, piece-end us, merges, pieces, tiles):",
+                  [(int(c), round(float(en[c]), 1), round(float(pe[c]), 2), int(nm_[c]), int(npc_[c]), int(nt_[c])) for c in fast])
             mg = full[964:964 + 16].reshape(8, 2)
             print("   merges (start, end) us:", [(round((s - b0) / 1e3, 2), round((e - b0) / 1e3, 2)) for s, e in mg if s > 0])
             cp = full[980:988]
