@@ -122,4 +122,22 @@ if os.path.exists(fp):
     if traffic:
         traffic["source"] = f"profiles/{R}_ncu_full.txt (dram__bytes_read.sum + dram__bytes_write.sum)"
         json.dump(traffic, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
+# ---- C3 launch list (tools/profile_c3.py: 3 decodes + 1 dense decode, batch 64 x 32K)
+cp = os.path.join(OUT, f"c3_launches_{R}.csv")
+if os.path.exists(cp):
+    rows = list(csv.reader(open(cp)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h = rows[hi]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    agg = collections.defaultdict(list)
+    for r in rows[hi + 1:]:
+        if len(r) > vi:
+            agg[r[ki]].append(float(r[vi].replace(",", "")) / 1000.0)
+    with open(os.path.join(PROF, f"{R}_c3_launches.txt"), "w") as f:
+        f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none launch list of "
+                f"`python tools/profile_c3.py` ({R}): C3 = batch 64 x 8 KV heads x 32K tokens (512 units), "
+                f"C = 256, p = 0.9; 3 sparse decodes + 1 dense decode, cold L2 (ncu flushes).\n")
+        f.write(f"{'launches':>8} {'mean us':>9}  kernel\n")
+        for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
+            f.write(f"{len(v):8d} {sum(v) / len(v):9.2f}  {k[:110]}\n")
 print(open(os.path.join(PROF, f"{R}_launches.txt")).read() if os.path.exists(lp) else "no launch list")
