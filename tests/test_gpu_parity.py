@@ -44,6 +44,24 @@ def test_dense_decode_matches_full_attention(T, B, H, G, n):
             np.testing.assert_allclose(lse[b, h * G:(h + 1) * G].cpu().numpy(), l, rtol=0, atol=2e-3)
 
 
+@pytest.mark.parametrize("B,H,G,n,ctas", [(16, 8, 4, 333, 0),   # 128 units > CTAs/2: global split
+                                          (2, 4, 4, 2000, 5),   # 8 units over 5 CTAs: several pieces per CTA
+                                          (3, 2, 2, 517, 3)])
+def test_dense_decode_global_split_epilogue(T, B, H, G, n, ctas):
+    """Global token split: CTAs end several pieces, handed to the epilogue warp (combine,
+    arrival, merge) while the consumers stream on; every unit against full attention."""
+    K, V, q = _layer(B, H, G, n, seed=7 * n + B)
+    lse = torch.empty((B, H * G), dtype=torch.float32, device="cuda")
+    out = T.dense_decode(dev_bf16(q), dev_bf16(K), dev_bf16(V), lse=lse, num_ctas=ctas)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            o, l = O.full_attention(q[b, h * G:(h + 1) * G], K[b, h], V[b, h])
+            assert_output_close(got[b, h * G:(h + 1) * G], o, f"dense global b{b} h{h}")
+            np.testing.assert_allclose(lse[b, h * G:(h + 1) * G].cpu().numpy(), l, rtol=0, atol=2e-3)
+
+
 def test_dense_decode_strided_view(T):
     B, H, G, n = 1, 2, 4, 3000
     K, V, q = _layer(B, H, G, n, seed=5)
