@@ -417,6 +417,18 @@ def run_gpu(args, rank, world, local_rank):
     att_us = 1e3 * float(np.mean([e[1].elapsed_time(e[2]) for e in st]))
     mrg_us = 1e3 * float(np.mean([e[2].elapsed_time(e[3]) for e in st]))
 
+    # ---- the attention kernel's launch duration for the roofline: S8 + S9 alone over each
+    # layer's work list (left by the decodes above), the 8 layers' launches back to back in
+    # one graph (8 distinct unions, together larger than L2), cold L2 before each replay
+    for L in layers:
+        T.decode(L["q"], L["index"], args.p, out=L["out"])
+    gatt = model_graph(lambda L: T.decode_attention_only(L["q"], L["index"], L["out"]))
+    timed_loop([gatt.replay], 3)
+    torch.cuda.synchronize()
+    att_ev = timed_loop([gatt.replay], max(10, min(args.steps, 50)))
+    torch.cuda.synchronize()
+    att_launch_us = per_layer_us(att_ev)
+
     # ---- algorithmic bytes from the selections the GPU made (mean over layers)
     bms = []
     for L in layers:
@@ -579,7 +591,7 @@ def run_gpu(args, rank, world, local_rank):
     peak_src = "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING)"
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     attn_bytes = bm["union_kv"] + bm["q_out"] // 2 + (n_sm + index.units) * G * 129 * 4   # K/V, q, partials
-    att_gbs = attn_bytes / (att_us * 1e-6) / 1e9
+    att_gbs = attn_bytes / (att_launch_us * 1e-6) / 1e9
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -596,7 +608,10 @@ def run_gpu(args, rank, world, local_rank):
         "roofline": {"bound": "hbm", "kernel": "attention_kernel<4,false> (S8 sparse split-KV)",
                      "achieved": att_gbs, "peak": hbm, "unit": "GB/s", "frac": att_gbs / hbm,
                      "traffic": traffic, "peak_source": peak_src,
-                     "bytes_per_launch": attn_bytes, "us_per_launch": att_us},
+                     "bytes_per_launch": attn_bytes, "us_per_launch": att_launch_us,
+                     "timing": "S8+S9 alone, 8 layers' launches back to back in one graph (no PDL), cold L2 "
+                               "per replay, CUDA events; mean per launch",
+                     "us_per_launch_event_bracketed_in_step": att_us},
         "step_roofline": {"bytes_per_step": bm["total"], "achieved_gbs": bm["total"] / (ms * 1e-3) / 1e9,
                           "frac": bm["total"] / (ms * 1e-3) / 1e9 / hbm, "bytes": bm},
         "stages_us": {"selection_S1_S7": sel_us, "attention_S8": att_us, "merge_S9": mrg_us},

@@ -172,6 +172,13 @@ tactic_status_t tactic_decode_debug(const void* q, tactic_index_t idx, float p, 
 tactic_status_t tactic_decode_profiled(const void* q, tactic_index_t idx, float p, void* out,
                                        void* const* events, int32_t n_events, void* stream);
 
+/* Measurement aid: S8 + S9 alone (the sparse split-KV attention kernel with its fused
+ * merge), over the work lists the last selection on this index left on the device (call
+ * tactic_decode / tactic_decode_ex first with the same q; p < 1).  q, out: as in
+ * tactic_decode.  Launched without a programmatic dependency, so back-to-back calls on
+ * one stream time the kernel's launch duration.  Errors: TACTIC_ERR_INVALID_ARGUMENT. */
+tactic_status_t tactic_decode_attention_only(const void* q, tactic_index_t idx, void* out, void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * The library's own dense baseline (full attention, Eq. 1-2):
  * split-KV flash-decode over all n tokens of every unit of the caller's K/V, then LSE

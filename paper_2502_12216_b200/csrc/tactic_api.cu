@@ -637,6 +637,11 @@ tactic_status_t tactic_decode_ex(const void* q, tactic_index_t idx, float p, voi
   return run_attention(q, idx, false, s, out, nullptr, lse);
 }
 
+tactic_status_t tactic_decode_attention_only(const void* q, tactic_index_t idx, void* out, void* stream) {
+  if (!q || !idx || !out) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  return run_attention(q, idx, false, (cudaStream_t)stream, out, nullptr, nullptr, nullptr, true);
+}
+
 tactic_status_t tactic_decode_profiled(const void* q, tactic_index_t idx, float p, void* out,
                                        void* const* events, int32_t n_events, void* stream) {
   if (!q || !idx || !out || !events || n_events != 4) return fail(TACTIC_ERR_INVALID_ARGUMENT, "bad arguments");

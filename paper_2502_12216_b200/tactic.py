@@ -65,6 +65,7 @@ _SIGS = {
     "tactic_decode_host": [_P, _P, _F, _P, _P],
     "tactic_decode_debug": [_P, _P, _F, _P, _P, _P, _P, _P, _P, _P],
     "tactic_decode_profiled": [_P, _P, _F, _P, ctypes.POINTER(_P), _I, _P],
+    "tactic_decode_attention_only": [_P, _P, _P, _P],
     "tactic_dense_workspace_size": [ctypes.POINTER(KvDesc), _I, ctypes.POINTER(ctypes.c_size_t)],
     "tactic_dense_decode": [_P, _P, _P, ctypes.POINTER(KvDesc), _P, _P, _P, ctypes.c_size_t, _I, _P],
     "tactic_lse_merge": [_P, _P, _I, _I, _P, _P, _P],
@@ -296,6 +297,14 @@ def decode_profiled(q: torch.Tensor, index: Index, p: float, events, out: Option
             e.record(stream if stream is not None else torch.cuda.current_stream())
     arr = (_P * 4)(*[ctypes.c_void_p(e.cuda_event) for e in events])
     _check(lib().tactic_decode_profiled(_ptr(q), index.handle, float(p), _ptr(out), arr, 4, _stream(stream)))
+    return out
+
+
+def decode_attention_only(q: torch.Tensor, index: Index, out: torch.Tensor, stream=None) -> torch.Tensor:
+    """tactic_decode_attention_only: S8 + S9 over the work lists of the last selection on
+    this index (measurement aid; run decode with the same q first)."""
+    _q_check(q, index)
+    _check(lib().tactic_decode_attention_only(_ptr(q), index.handle, _ptr(out), _stream(stream)))
     return out
 
 
