@@ -371,17 +371,20 @@ struct FitParams {
 // H(k) - H(j) = sum_{i=j+1}^{k} 1/i for 0 <= j <= k: exact terms below 16, above that
 // log1p of the ratio plus the difference of the asymptotic series 1/2x - 1/12x^2 + 1/120x^4
 // (the next term is < 2.4e-10 at x = 16).
+// (Reciprocals by __frcp_rn, correctly rounded like 1.f / x, without the IEEE division
+// sequence: the J search evaluates this on the warp's critical path.)
 __device__ __forceinline__ float harm_diff_f(int k, int j) {
   if (k <= j) return 0.f;
   float s = 0.f;
-  while (j < 16 && j < k) s += 1.f / (float)(++j);  // tiny n only
+  while (j < 16 && j < k) s += __frcp_rn((float)(++j));  // tiny n only
   if (k <= j) return s;
   const float xk = (float)k, xj = (float)j;
-  auto t = [](float x) {
-    const float r = 1.f / x, r2 = r * r;
+  const float rk = __frcp_rn(xk), rj = __frcp_rn(xj);
+  auto t = [](float r) {
+    const float r2 = r * r;
     return r * 0.5f - r2 * (1.f / 12.f - r2 * (1.f / 120.f));
   };
-  return s + log1pf((xk - xj) / xj) + (t(xk) - t(xj));
+  return s + log1pf((xk - xj) * rj) + (t(rk) - t(rj));
 }
 
 // sum_{i=N+1}^{k} max(0, a/i + b): the positive terms of the monotone a/i + b form one

@@ -76,6 +76,10 @@ for it in range(4):
         names = ["head0 last chunk", "staged", "fitted", "marked", "unit0 compact start", "unit0 compact end"]
         print("  sample_fit (us from first start): " + "  ".join(f"{nm} {(fs[i] - z) / 1e3:6.2f}" for i, nm in enumerate(names)
                                                               if fs[i] > 0))
+        hs = full[1700:1705]
+        if hs[0] > 0:
+            print("  fit warp 0 (us after summaries staged): " + "  ".join(
+                f"{nm} {(hs[i] - fs[2]) / 1e3:.2f}" for i, nm in enumerate(["sums", "W", "-", "J", "marked"]) if hs[i] > 0))
         cs = full[264:268]
         print("  compaction (us from first start): " + "  ".join(f"{nm} {(cs[i] - z) / 1e3:6.2f}" for i, nm in
               enumerate(["pass1", "scan", "pass2", "fill"]) if cs[i] > 0))
