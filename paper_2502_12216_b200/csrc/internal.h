@@ -177,6 +177,8 @@ struct SelArgs {
   double* local_max;               // stage 1
 };
 cudaError_t launch_score(const SelArgs& a, cudaStream_t s, bool pdl);
+// S1 for every (unit, head) into x->crit (score_kernel), q: [units][G][128]
+cudaError_t launch_score_all(const __nv_bfloat16* q, tactic_index_s* x, cudaStream_t s, bool pdl);
 // S1 + S2 + S3 (rank_cluster.cu): crit, order, ends, sampled-slot row map
 cudaError_t launch_score_rank(const __nv_bfloat16* q, tactic_index_s* x, cudaStream_t s, bool pdl);
 cudaError_t launch_sample(const SelArgs& a, cudaStream_t s, bool pdl);

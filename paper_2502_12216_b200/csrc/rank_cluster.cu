@@ -55,20 +55,23 @@ struct __align__(16) RunEnt {
   unsigned long long pre;
 };
 
-template <int M, int R>
+// PS (prescored): S1 ran in score_kernel (select.cu: one read of a unit's centroids for all
+// G heads, bit-identical crit); this kernel loads crit and holds no centroid slice, so more
+// clusters fit per SM.  Used when the launch spans several waves (batch 64, C3).
+template <int M, int R, bool PS>
 constexpr size_t sr_smem() {
-  return (size_t)M * 512 + (size_t)R * (M + 1) * sizeof(RunEnt) + 2 * (size_t)M * 8 + 2 * (size_t)M * 4 + 64;
+  return (PS ? 0 : (size_t)M * 512) + (size_t)R * (M + 1) * sizeof(RunEnt) + 2 * (size_t)M * 8 + 2 * (size_t)M * 4 + 64;
 }
 
-template <int M, int R>
+template <int M, int R, bool PS>
 __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
   constexpr int NW = M / 32;
   const int c = blockIdx.x, g = blockIdx.y, u = blockIdx.z;  // the cluster spans grid x (R CTAs)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int C = P.C;
   extern __shared__ __align__(128) uint8_t sm[];
-  float* s_cent = (float*)sm;                                // [M][128]
-  RunEnt* runs = (RunEnt*)(s_cent + M * 128);                 // [R][M+1]
+  float* s_cent = (float*)sm;                                // [M][128] (not PS)
+  RunEnt* runs = (RunEnt*)(sm + (PS ? 0 : M * 512));          // [R][M+1]
   unsigned long long* bk = (unsigned long long*)(runs + R * (M + 1));  // [2][M]
   int* s_size = (int*)(bk + 2 * M);                           // [M]
   int* s_row = s_size + M;                                    // [M]
@@ -96,12 +99,14 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
   __syncthreads();
   cluster_arrive_relaxed();  // every CTA has started (and initialised rbar) before any st.async
   if (tid == 0) {
-    const uint32_t bytes = (uint32_t)nval * 512u;
-    mbar_arrive_expect_tx(&bar, bytes);
-    const uint8_t* src = (const uint8_t*)(P.cent + ((size_t)u * C + (size_t)c * M) * 128);
-    for (uint32_t o = 0; o < bytes; o += 16384u) {
-      const uint32_t b = bytes - o < 16384u ? bytes - o : 16384u;
-      bulk_g2s((uint8_t*)s_cent + o, src + o, b, &bar);
+    if (!PS) {
+      const uint32_t bytes = (uint32_t)nval * 512u;
+      mbar_arrive_expect_tx(&bar, bytes);
+      const uint8_t* src = (const uint8_t*)(P.cent + ((size_t)u * C + (size_t)c * M) * 128);
+      for (uint32_t o = 0; o < bytes; o += 16384u) {
+        const uint32_t b = bytes - o < 16384u ? bytes - o : 16384u;
+        bulk_g2s((uint8_t*)s_cent + o, src + o, b, &bar);
+      }
     }
     mbar_arrive_expect_tx(&rbar, (uint32_t)(R * (M + 1) * sizeof(RunEnt)));
   }
@@ -115,38 +120,43 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
   if (tid == 0) tl_mark(P.tlog, 1, 1, tl_first);
 
   // ---- S1: crit of the warp's 32 centroids (lane L ends up with centroid 32 w + L)
-  double qd[4];
-  {
-    const uint2 raw = *reinterpret_cast<const uint2*>(P.q + ((size_t)u * P.G + g) * 128 + lane * 4);
-    const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-    const float2 a = __bfloat1622float2(q2[0]), b = __bfloat1622float2(q2[1]);
-    qd[0] = a.x; qd[1] = a.y; qd[2] = b.x; qd[3] = b.y;
-  }
-  mbar_wait(&bar, 0);
-  pstamp(0);
-  double v[32];
-#pragma unroll
-  for (int jj = 0; jj < 32; ++jj) {
-    const int lc = warp * 32 + jj;
-    const float4 cv = lc < nval ? reinterpret_cast<const float4*>(s_cent + lc * 128)[lane]
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
-    double s = qd[0] * (double)cv.x;
-    s = fma(qd[1], (double)cv.y, s);
-    s = fma(qd[2], (double)cv.z, s);
-    s = fma(qd[3], (double)cv.w, s);
-    v[jj] = s;
-  }
-#pragma unroll
-  for (int o = 16, half = 16; o >= 1; o >>= 1, half >>= 1) {
-    const bool upper = (lane & o) != 0;
-#pragma unroll
-    for (int i = 0; i < half; ++i) {
-      const double send = upper ? v[i] : v[i + half];
-      const double keep = upper ? v[i + half] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+  double crit;
+  if constexpr (PS) {
+    crit = valid ? __ldcg(P.crit + ((size_t)u * P.G + g) * C + j) : 0.0;
+  } else {
+      double qd[4];
+    {
+      const uint2 raw = *reinterpret_cast<const uint2*>(P.q + ((size_t)u * P.G + g) * 128 + lane * 4);
+      const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      const float2 a = __bfloat1622float2(q2[0]), b = __bfloat1622float2(q2[1]);
+      qd[0] = a.x; qd[1] = a.y; qd[2] = b.x; qd[3] = b.y;
     }
+    mbar_wait(&bar, 0);
+    pstamp(0);
+    double v[32];
+  #pragma unroll
+    for (int jj = 0; jj < 32; ++jj) {
+      const int lc = warp * 32 + jj;
+      const float4 cv = lc < nval ? reinterpret_cast<const float4*>(s_cent + lc * 128)[lane]
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+      double s = qd[0] * (double)cv.x;
+      s = fma(qd[1], (double)cv.y, s);
+      s = fma(qd[2], (double)cv.z, s);
+      s = fma(qd[3], (double)cv.w, s);
+      v[jj] = s;
+    }
+  #pragma unroll
+    for (int o = 16, half = 16; o >= 1; o >>= 1, half >>= 1) {
+      const bool upper = (lane & o) != 0;
+  #pragma unroll
+      for (int i = 0; i < half; ++i) {
+        const double send = upper ? v[i] : v[i + half];
+        const double keep = upper ? v[i + half] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    crit = v[0];
   }
-  const double crit = v[0];
   pstamp(1);
 
   // ---- S2: local bitonic sort (ascending packed keys = descending crit, then id)
@@ -199,7 +209,7 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
     if (tid == M - 1) st_async_v2u64(dsmem_addr(runs + c * (M + 1) + M, (uint32_t)cc), ~0ull, (unsigned long long)tot, rb);
   }
   const size_t ug = (size_t)u * P.G + g;
-  if (valid) P.crit[ug * C + j] = crit;
+  if (!PS && valid) P.crit[ug * C + j] = crit;
   pstamp(3);
   mbar_wait(&rbar, 0);
   pstamp(4);
@@ -264,15 +274,15 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
   pdl_launch_dependents();
 }
 
-template <int M, int R>
-static cudaError_t launch_sr(const SRParams& P, int units, cudaStream_t s, bool pdl) {
-  constexpr size_t smem = sr_smem<M, R>();
+template <int M, int R, bool PS>
+static cudaError_t launch_sr_t(const SRParams& P, int units, cudaStream_t s, bool pdl) {
+  constexpr size_t smem = sr_smem<M, R, PS>();
   static bool done = false;
   if (!done) {
-    cudaError_t e = cudaFuncSetAttribute(score_rank_kernel<M, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(score_rank_kernel<M, R, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (R > 8) {
-      e = cudaFuncSetAttribute(score_rank_kernel<M, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      e = cudaFuncSetAttribute(score_rank_kernel<M, R, PS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
     }
     done = true;
@@ -291,7 +301,12 @@ static cudaError_t launch_sr(const SRParams& P, int units, cudaStream_t s, bool 
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = (pdl && pdl_enabled()) ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, score_rank_kernel<M, R>, P);
+  return cudaLaunchKernelEx(&cfg, score_rank_kernel<M, R, PS>, P);
+}
+
+template <int M, int R>
+static cudaError_t launch_sr(const SRParams& P, int units, cudaStream_t s, bool pdl, bool ps) {
+  return ps ? launch_sr_t<M, R, true>(P, units, s, pdl) : launch_sr_t<M, R, false>(P, units, s, pdl);
 }
 
 cudaError_t launch_score_rank(const __nv_bfloat16* q, tactic_index_s* x, cudaStream_t s, bool pdl) {
@@ -310,12 +325,24 @@ cudaError_t launch_score_rank(const __nv_bfloat16* q, tactic_index_s* x, cudaStr
   P.tlog = x->tlog;
   // M clusters per CTA, R = pow2 >= ceil(C / M) CTAs per cluster (TACTIC_MAX_CLUSTERS = 4096)
   const int C = x->C, U = x->units;
-  if (C <= 128) return launch_sr<128, 1>(P, U, s, pdl);
-  if (C <= 256) return launch_sr<128, 2>(P, U, s, pdl);
-  if (C <= 512) return launch_sr<128, 4>(P, U, s, pdl);
-  if (C <= 1024) return launch_sr<128, 8>(P, U, s, pdl);
-  if (C <= 2048) return launch_sr<256, 8>(P, U, s, pdl);
-  return launch_sr<256, 16>(P, U, s, pdl);
+  // several waves of clusters (C3: 4096 CTAs): score all G heads from one read of the
+  // centroids first (score_kernel), then rank from crit with the smaller footprint
+  const int M = C <= 1024 ? 128 : 256;
+  const int R = (C + M - 1) / M;
+  const int sms = x->num_sms > 0 ? x->num_sms : 148;
+  const bool g_ok = x->G == 1 || x->G == 2 || x->G == 4 || x->G == 8;  // score_kernel's G
+  const bool ps = g_ok && (long long)R * x->G * U > 6LL * sms;
+  if (ps) {
+    cudaError_t e = launch_score_all(q, x, s, pdl);
+    if (e != cudaSuccess) return e;
+    pdl = true;  // the rank kernel's prologue overlaps the scoring
+  }
+  if (C <= 128) return launch_sr<128, 1>(P, U, s, pdl, ps);
+  if (C <= 256) return launch_sr<128, 2>(P, U, s, pdl, ps);
+  if (C <= 512) return launch_sr<128, 4>(P, U, s, pdl, ps);
+  if (C <= 1024) return launch_sr<128, 8>(P, U, s, pdl, ps);
+  if (C <= 2048) return launch_sr<256, 8>(P, U, s, pdl, ps);
+  return launch_sr<256, 16>(P, U, s, pdl, ps);
 }
 
 }  // namespace tactic

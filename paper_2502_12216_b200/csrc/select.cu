@@ -1048,8 +1048,10 @@ static cudaLaunchConfig_t make_cfg(dim3 grid, dim3 block, size_t smem, cudaStrea
   return cfg;
 }
 
-cudaError_t launch_score(const SelArgs& a, cudaStream_t s, bool pdl) {
-  tactic_index_s* x = a.idx;
+cudaError_t launch_score(const SelArgs& a, cudaStream_t s, bool pdl) { return launch_score_all(a.q, a.idx, s, pdl); }
+
+cudaError_t launch_score_all(const __nv_bfloat16* q, tactic_index_s* x, cudaStream_t s, bool pdl) {
+  struct { const __nv_bfloat16* q; } a = {q};
   cudaLaunchAttribute attr[1];
   const int per_block = 8 * (32 / x->G);
   auto cfg = make_cfg(dim3((x->C + per_block - 1) / per_block, x->units), dim3(256), 0, s, pdl, attr);
