@@ -232,7 +232,7 @@ __device__ __forceinline__ int slot_rank(int slot, const SampleConsts& sc) {
 // then computed on the tensor cores (mma.sync m16n8k16, q in the n=8 dimension, only
 // column 0 live).  The CTA also emits a summary for the fit: its local max logit and the
 // sums of exp(l - m_local) over its exact-head, window-1 and window-2 slots.
-constexpr int SB = 128;
+constexpr int SB = 64;
 
 __global__ void __launch_bounds__(SB) sample_kernel(const __nv_bfloat16* __restrict__ q,
                                                     const __nv_bfloat16* __restrict__ Kp,
