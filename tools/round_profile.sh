@@ -14,6 +14,6 @@ timeout 900 ncu --set full --clock-control none --import-source on \
   -o gpurun_out/full_$R -f python tools/profile_decode.py > gpurun_out/full_$R.log 2>&1
 echo "full capture rc=$?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none \
-  -k regex:"score_rank|sample_kernel|fit_unit|attention_kernel" --csv \
+  -k regex:"score_kernel|score_rank|sample_kernel|fit_unit|attention_kernel" --csv \
   --log-file gpurun_out/c3_launches_$R.csv python tools/profile_c3.py > gpurun_out/c3_launches_$R.log 2>&1
 echo "c3 launch list rc=$?"
