@@ -633,3 +633,20 @@ def test_per_head_loading_with_tail(T):
             toks = np.concatenate([O.cluster_tokens(idxs[u], ro["heads"][g]["S"]), n + np.arange(29)])
             o, _ = O.sparse_attention(qo[g], np.concatenate([K[0, u], kt[u]]), np.concatenate([V[0, u], vt[u]]), toks)
             assert_output_close(got[0, u * G + g:u * G + g + 1], o, f"u={u} g={g}")
+
+
+def test_attention_only_reproduces_decode(T):
+    """tactic_decode_attention_only (the bench's roofline timing) reruns S8 + S9 over the
+    work lists of the last selection: bit-identical output, also when called repeatedly."""
+    B, H, G, n, C = 1, 2, 4, 8192, 64
+    K, V, q = _layer(B, H, G, n, 321)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, B)
+    index = _import(T, K, V, cents, asg, G)
+    qd = dev_bf16(q)
+    ref = T.decode(qd, index, 0.9)
+    out = torch.empty_like(ref)
+    for _ in range(3):
+        out.zero_()
+        T.decode_attention_only(qd, index, out)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
