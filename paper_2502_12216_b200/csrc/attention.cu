@@ -8,7 +8,8 @@
 // contiguous ranges, one per CTA (unit-aligned split, see UnitSplit), so head-level
 // imbalance becomes plain sequence imbalance.  With more units than CTAs/2 the lists of
 // all units form one global list cut into equal ranges instead (a CTA may then hold
-// pieces of two units).
+// pieces of several units; every unit also carries ATT_PIECE_TOKENS virtual tokens so the
+// split prices a piece's fixed cost).
 //
 // Per CTA: 1 producer warp streams 64-token stages of K and V into shared memory
 //   sparse: cp.async.bulk (1-D TMA, UBLKCP) of contiguous cluster runs from the
@@ -24,7 +25,11 @@
 // A piece (the part of one unit inside a CTA's range) ends with a cross-warp LSE
 // combine and one partial (o, lse) per head written to slot blockIdx.x (unit-aligned) or
 // blockIdx.x + unit (global split); a per-unit
-// arrival counter elects the last CTA of the unit, which merges its pieces (S9).
+// arrival counter elects the last CTA of the unit, which merges its pieces (S9).  In the
+// unit-aligned split the consumers do this themselves (one piece per CTA, at its end); in
+// the global split a sixth warp (the piece epilogue) takes each finished piece from the
+// consumers through two shared-memory buffers, so the stream does not stop at unit
+// switches.
 #include <cuda.h>
 #include <cuda_bf16.h>
 

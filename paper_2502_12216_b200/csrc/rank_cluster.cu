@@ -56,7 +56,7 @@ struct __align__(16) RunEnt {
 };
 
 // PS (prescored): S1 ran in score_kernel (select.cu: one read of a unit's centroids for all
-// G heads, bit-identical crit); this kernel loads crit and holds no centroid slice, so more
+// G heads, the same products and butterfly tree: bit-identical crit); this kernel loads crit and holds no centroid slice, so more
 // clusters fit per SM.  Used when the launch spans several waves (batch 64, C3).
 template <int M, int R, bool PS>
 constexpr size_t sr_smem() {
