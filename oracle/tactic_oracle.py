@@ -179,15 +179,35 @@ def build_index(K, V, C: int, iters: int = 10, init=None, seed: int = 0, unit: i
 # Decode (per unit, per query head).  §4.3 querying, §4.4 fitting (Alg. 1,
 # P:747-766), §4.5 GQA union, §4.6 attention on selected tokens.
 # ---------------------------------------------------------------------------
-def sample_constants(n: int) -> dict:
+DEFAULT_SAMPLING = {"exact_frac": 0.02, "p1": 0.10, "p2": 0.60, "window_half_frac": 0.0025}
+
+
+def _ppm(f: float) -> int:
+    """A sampling fraction quantised to parts per million (round half up): the
+    integer the rule below works with, so that every party derives the same N, x1,
+    x2, w from the same fractions whatever their floating-point width."""
+    return int(np.floor(float(f) * 1e6 + 0.5))
+
+
+def sample_constants(n: int, exact_frac: float = 0.02, p1: float = 0.10, p2: float = 0.60,
+                     window_half_frac: float = 0.0025) -> dict:
     """O6: integer N (exact head), window centres x1, x2 and half-width w.
-    exact_frac = 0.02 (reading 10, "1-2%"), p1 = 0.1, p2 = 0.6 (P:373
-    "e.g., 10% and 60%"), window_half_frac = 0.0025 (reading 8).  fallback =
-    exact weights for every rank when the windows collide (tiny n)."""
-    N = (2 * n + 99) // 100
-    x1 = (n + 5) // 10
-    x2 = (6 * n + 5) // 10
-    w = max(1, (25 * n + 5000) // 10000)
+
+    P:376: the first N = "1-2% of total tokens" ranks are exact (reading 10: the upper
+    end, exact_frac = 0.02).  P:373: the windows sit at "e.g., 10% and 60%" of the
+    sorted tokens (p1, p2).  Reading 8: the window half-width is a fraction of n
+    (window_half_frac = 0.25%).  With e, q1, q2, h the fractions in ppm:
+        N  = ceil(e n / 1e6),   x_k = round_half_up(q_k n / 1e6),
+        w  = max(1, round_half_up(h n / 1e6)).
+    fallback = exact weights for every rank when the windows collide with the head,
+    with each other or with the end (tiny n)."""
+    e, q1, q2, h = _ppm(exact_frac), _ppm(p1), _ppm(p2), _ppm(window_half_frac)
+    if not (e >= 1 and h >= 1 and 1 <= q1 < q2 < 1000000):
+        raise ValueError("need exact_frac, window_half_frac > 0 and 0 < p1 < p2 < 1")
+    N = (e * n + 999999) // 1000000
+    x1 = (2 * q1 * n + 1000000) // 2000000
+    x2 = (2 * q2 * n + 1000000) // 2000000
+    w = max(1, (2 * h * n + 1000000) // 2000000)
     fallback = (x1 - w <= N) or (x1 + w >= x2 - w) or (x2 + w > n)
     return {"N": N, "x1": x1, "x2": x2, "w": w, "fallback": bool(fallback)}
 
@@ -225,11 +245,13 @@ def token_budget(w: np.ndarray, P: float) -> int:
     return int(np.argmax(cum >= P * W)) + 1
 
 
-def decode_head(q_g: np.ndarray, idx: Index, p: float, windows_exact: bool = False) -> dict:
+def decode_head(q_g: np.ndarray, idx: Index, p: float, windows_exact: bool = False,
+                sampling: Optional[dict] = None) -> dict:
     """Per query head: O5-O10 (selection) for one unit.  Returns the order pi, the
     per-cluster end ranks, the fit and the selected cluster set S_g.
     windows_exact: SPEC's variant -- the window ranks keep their exact
-    weights too ("exact values taking precedence"); default reading 11: only i <= N."""
+    weights too ("exact values taking precedence"); default reading 11: only i <= N.
+    sampling: the fractions of sample_constants (default DEFAULT_SAMPLING)."""
     n, C = idx.n, idx.C
     d = idx.K.shape[1]
     q_g = np.asarray(q_g, dtype=np.float64)
@@ -239,7 +261,7 @@ def decode_head(q_g: np.ndarray, idx: Index, p: float, windows_exact: bool = Fal
     ends = np.cumsum(sizes_sorted)                 # e_r, r = 1..C (1-based ranks)
     starts = ends - sizes_sorted                   # s_r
     tok = sorted_tokens(idx, order)                # tau(i) = tok[i-1]
-    sc = sample_constants(n)
+    sc = sample_constants(n, **(sampling or {}))
     N, x1, x2, w = sc["N"], sc["x1"], sc["x2"], sc["w"]
     scale = 1.0 / np.sqrt(d)
 
@@ -312,12 +334,13 @@ def cluster_tokens(idx: Index, clusters) -> np.ndarray:
     return np.sort(np.concatenate([idx.perm[idx.offsets[j]:idx.offsets[j + 1]] for j in clusters]))
 
 
-def decode_unit(q: np.ndarray, idx: Index, p: float, windows_exact: bool = False) -> dict:
+def decode_unit(q: np.ndarray, idx: Index, p: float, windows_exact: bool = False,
+                sampling: Optional[dict] = None) -> dict:
     """O5-O12 for one unit and its G query heads: per-head selection, GQA union
     U = union_g S_g (§4.5), attention of every head over U (reading 17)."""
     q = np.atleast_2d(np.asarray(q, dtype=np.float64))
     G = q.shape[0]
-    heads = [decode_head(q[g], idx, p, windows_exact) for g in range(G)]
+    heads = [decode_head(q[g], idx, p, windows_exact, sampling) for g in range(G)]
     mask = np.zeros(idx.C, dtype=bool)
     for h in heads:
         mask[h["S"]] = True

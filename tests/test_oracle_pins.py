@@ -250,6 +250,102 @@ def test_sample_constants_follow_paper_fractions():
     assert O.sample_constants(10)["fallback"]
 
 
+def test_sample_constants_ppm_rule_defaults_are_the_integer_formulas():
+    """Readings 8-10: with the default fractions the ppm rule reproduces the integer
+    formulas N = (2n+99) div 100, x1 = (n+5) div 10, x2 = (6n+5) div 10,
+    w = max(1, (25n+5000) div 10000) for every n (checked exhaustively to 2^17 and on
+    a sample up to 2^20), whether the fractions arrive as float64 or float32."""
+    ns = list(range(1, 1 << 17)) + list(np.random.default_rng(0).integers(1 << 17, (1 << 20) + 1, 3000))
+    for f32 in (False, True):
+        conv = (lambda v: float(np.float32(v))) if f32 else float
+        kw = {k: conv(v) for k, v in O.DEFAULT_SAMPLING.items()}
+        for n in ns[:: (1 if not f32 else 7)]:
+            n = int(n)
+            sc = O.sample_constants(n, **kw)
+            assert (sc["N"], sc["x1"], sc["x2"], sc["w"]) == (
+                (2 * n + 99) // 100, (n + 5) // 10, (6 * n + 5) // 10, max(1, (25 * n + 5000) // 10000)), n
+
+
+def test_sample_constants_custom_fractions():
+    # P:376 "1-2%": the lower end; windows at 20% / 50% with a 1% half-width (SPEC S:217)
+    sc = O.sample_constants(100000, exact_frac=0.01, p1=0.2, p2=0.5, window_half_frac=0.01)
+    assert (sc["N"], sc["x1"], sc["x2"], sc["w"], sc["fallback"]) == (1000, 20000, 50000, 1000, False)
+    sc = O.sample_constants(999, exact_frac=0.015, p1=0.25, p2=0.75, window_half_frac=0.001)
+    assert (sc["N"], sc["x1"], sc["x2"], sc["w"]) == (15, 250, 749, 1)   # 14.985 up, 249.75, 749.25, 0.999
+    for bad in [dict(p1=0.6, p2=0.1), dict(exact_frac=0.0), dict(window_half_frac=0.0), dict(p2=1.0)]:
+        with pytest.raises(ValueError):
+            O.sample_constants(1000, **bad)
+
+
+def test_splitmix64_known_answer_vector():
+    """The init sampler's generator is SplitMix64 (reading 3): its published first outputs
+    from state 0 (Steele, Lea & Flood's reference stream)."""
+    g = O._splitmix64_stream(0)
+    assert [next(g) for _ in range(5)] == [0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F,
+                                           0xF88BB8A8724C81EC, 0x1B39896A51A8749B]
+
+
+def _planted_harmonic_unit(n, a_star, b_star, seed=0, d=128):
+    """Singleton clusters whose exact weight at sorted rank i is proportional to
+    a*/i + b*: key i has component 0 = log(a*/r_i + b*) for a random rank r_i (the
+    other components random), the query points along component 0 with |q| = sqrt(d),
+    so the logit q.k/sqrt(d) is that log up to rounding."""
+    rng = np.random.default_rng(seed)
+    ranks = rng.permutation(n) + 1                    # token i has rank ranks[i]
+    K = rng.standard_normal((n, d)) * 0.3
+    K[:, 0] = np.log(a_star / ranks + b_star)
+    V = rng.standard_normal((n, d))
+    q = np.zeros(d)
+    q[0] = np.sqrt(d)
+    idx = O.make_index(K, V, K, np.arange(n))         # C = n, centroid = key
+    return idx, q, ranks
+
+
+@pytest.mark.parametrize("n,a_star,b_star", [(2000, 3.0, 0.01), (2000, 0.5, 0.0), (12345, 7.0, 0.002)])
+def test_window_means_and_fit_on_planted_harmonic_weights(n, a_star, b_star):
+    """O7 pinned independently (Alg. 1 l.4): on an
+    instance whose exp-logit at sorted rank i is exactly proportional to a*/i + b*, the
+    shift m is the rank-1 logit, the exact head is (a*/i + b*)/y_1 for i <= N, and each
+    window mean is the harmonic closed form
+        mu_k = (a* (H(x_k + w) - H(x_k - w - 1)) / (2w + 1) + b*) / y_1,
+    with H from scipy's digamma; the fitted a/x + b passes through (x_k, mu_k).  A
+    sum instead of a mean, a window shifted by one rank, or a wrong shift fails it."""
+    idx, q, ranks = _planted_harmonic_unit(n, a_star, b_star)
+    h = O.decode_head(q, idx, 0.9)
+    N, x1, x2, w = h["N"], h["x1"], h["x2"], h["w"]
+    assert not h["fallback"]
+    y1 = a_star + b_star
+    # the order is descending weight: rank r holds the token with ranks[token] == r
+    tok = np.argsort(ranks)
+    assert np.array_equal(h["order"], tok)
+    assert h["m"] == pytest.approx(np.log(y1), abs=1e-12)
+    i = np.arange(1, N + 1)
+    np.testing.assert_allclose(h["what"][:N], (a_star / i + b_star) / y1, rtol=1e-12)
+    for x, mu in ((x1, h["mu1"]), (x2, h["mu2"])):
+        expect = (a_star * (_harmonic(x + w) - _harmonic(x - w - 1)) / (2 * w + 1) + b_star) / y1
+        assert mu == pytest.approx(expect, rel=1e-12)
+    for x, mu in ((x1, h["mu1"]), (x2, h["mu2"])):
+        assert h["a"] / x + h["b"] == pytest.approx(mu, rel=1e-12)
+    # and the fitted curve's tail beyond N is clamp-free: W = E_N + a (H(n) - H(N)) + b (n - N)
+    if h["a"] >= 0 and h["b"] >= 0:
+        W = float(np.sum(h["what"][:N])) + h["a"] * (_harmonic(n) - _harmonic(N)) + h["b"] * (n - N)
+        assert h["W"] == pytest.approx(W, rel=1e-10)
+
+
+def test_window_means_with_custom_sampling_fractions():
+    """Same planted instance through non-default fractions (P:376 lower end 1%, windows at
+    20% / 50% with a 0.5% half-width): the means follow the constants of the ppm rule."""
+    n, a_star, b_star = 5000, 2.0, 0.004
+    idx, q, _ = _planted_harmonic_unit(n, a_star, b_star, seed=3)
+    smp = dict(exact_frac=0.01, p1=0.2, p2=0.5, window_half_frac=0.005)
+    h = O.decode_head(q, idx, 0.9, sampling=smp)
+    assert (h["N"], h["x1"], h["x2"], h["w"]) == (50, 1000, 2500, 25)
+    y1 = a_star + b_star
+    for x, mu in ((h["x1"], h["mu1"]), (h["x2"], h["mu2"])):
+        expect = (a_star * (_harmonic(x + 25) - _harmonic(x - 26)) / 51 + b_star) / y1
+        assert mu == pytest.approx(expect, rel=1e-12)
+
+
 # ----------------------------------------------------------------------------- selection
 def test_selection_monotone_in_p_and_p1_selects_all():
     u = make_unit(4096, 4, seed=2)
