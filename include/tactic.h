@@ -74,7 +74,27 @@ typedef struct {
                                    sampler seeded with seed + (u+1)*0x9E3779B97F4A7C15   */
   uint32_t flags;               /* TACTIC_FLAG_*                                          */
   int32_t num_ctas;             /* attention grid size; 0 = number of SMs                 */
+  /* Alg. 1 sampling fractions (0 = the default in brackets):
+   *   exact_frac        share of the sorted tokens whose weights are exact ("1-2% of
+   *                     total tokens"; reading 10: [0.02])
+   *   p1, p2            window centres as shares of n ("e.g., 10% and 60%";
+   *                     [0.10], [0.60]), 0 < p1 < p2 < 1
+   *   window_half_frac  window half-width as a share of n (reading 8: [0.0025])
+   * Each fraction is quantised to parts per million, f -> round(f * 1e6), and the index
+   * derives (integer arithmetic, identical in the oracle):
+   *   N = ceil(e n / 1e6),  x_k = round_half_up(p_k n / 1e6),  w = max(1, round_half_up(h n / 1e6));
+   * the windows [x_k - w, x_k + w] must not collide with the head, each other or the end,
+   * else every rank is exact (tiny n).  Fixed at build / import; see
+   * tactic_sample_constants.  Out of range: TACTIC_ERR_INVALID_ARGUMENT.               */
+  float exact_frac, p1, p2, window_half_frac;
 } tactic_params_t;
+
+/* The integer constants of Alg. 1's sampling for sequence length n (see tactic_params_t):
+ * exact head N, window centres x1 < x2, half-width w, fallback = 1 when every rank is
+ * exact (windows collide), slots = logits computed per head (N + 2(2w + 1), or n).     */
+typedef struct {
+  int32_t N, x1, x2, w, fallback, slots;
+} tactic_sample_constants_t;
 
 typedef struct {
   int32_t units, batch, num_kv_heads, group_size, seq_len, n_clusters;
@@ -97,8 +117,11 @@ typedef struct {
  *             them once the stream has passed this call.
  *   n_clusters C, 1 <= C <= min(seq_len, TACTIC_MAX_CLUSTERS)   (else INVALID_ARGUMENT)
  *   iters     >= 1
- *   params    nullable (defaults: seed 0, sampler init, no flags)
+ *   params    nullable (defaults: seed 0, sampler init, no flags, default sampling)
  *   out       receives the new index (NULL on failure).
+ * TACTIC_ERR_UNSUPPORTED when the per-unit selection state (G x C order and end ranks,
+ * the sampled-slot summaries) exceeds one CTA's shared memory, e.g. G = 8 with C > ~3000
+ * (tactic_index_set_options checks the windows-exact variant the same way).
  * The assignment GEMM runs on tcgen05 tensor cores (bf16 keys x split-bf16 centroids,
  * fp32 accumulate, fused argmin epilogue).  The call enqueues work only; it allocates
  * device memory (not capturable).                                                     */
@@ -123,6 +146,11 @@ tactic_status_t tactic_index_export(tactic_index_t idx, float* centroids, int32_
                                     double* inertia, int32_t* iters_run, void* stream);
 
 tactic_status_t tactic_index_info(tactic_index_t idx, tactic_index_info_t* info);
+/* Host-only (no device work): the sampling constants for n tokens under `params`
+ * (nullable = defaults), or those an index uses.  INVALID_ARGUMENT on bad fractions or
+ * n < 1.                                                                               */
+tactic_status_t tactic_sample_constants(int32_t n, const tactic_params_t* params, tactic_sample_constants_t* out);
+tactic_status_t tactic_index_sample_constants(tactic_index_t idx, tactic_sample_constants_t* out);
 /* Debug: the %globaltimer / clock stamps the decode kernels leave in the index's timing
  * log (kernel timeline, per-phase stamps of CTA 0 of each kernel; tools/phase_timing.py
  * decodes them), host uint64 [count].  Only for indices created with the environment
@@ -176,7 +204,8 @@ tactic_status_t tactic_decode_profiled(const void* q, tactic_index_t idx, float 
  * merge), over the work lists the last selection on this index left on the device (call
  * tactic_decode / tactic_decode_ex first with the same q; p < 1).  q, out: as in
  * tactic_decode.  Launched without a programmatic dependency, so back-to-back calls on
- * one stream time the kernel's launch duration.  Errors: TACTIC_ERR_INVALID_ARGUMENT. */
+ * one stream time the kernel's launch duration.  Errors: TACTIC_ERR_INVALID_ARGUMENT on
+ * NULL arguments or before the index's first p < 1 selection has been enqueued.        */
 tactic_status_t tactic_decode_attention_only(const void* q, tactic_index_t idx, void* out, void* stream);
 
 /* ---------------------------------------------------------------------------------------

@@ -993,12 +993,8 @@ template <int G, bool DENSE>
 static cudaError_t launch_attn_t(const AttnArgs& a, const CUtensorMap* tmK, const CUtensorMap* tmV,
                                  long long dense_total, int num_ctas, cudaStream_t s, bool pdl) {
   auto kern = attention_kernel<G, DENSE>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ATT_SMEM);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  cudaError_t e = func_smem_optin((const void*)kern, ATT_SMEM);
+  if (e != cudaSuccess) return e;
   CUtensorMap dummy;
   memset(&dummy, 0, sizeof(dummy));
   cudaLaunchConfig_t cfg = {};

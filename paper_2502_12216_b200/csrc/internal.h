@@ -20,9 +20,14 @@ struct SampleConsts {
   bool fallback;
   int slots;  // logits computed per head: N + 2(2w+1), or n in fallback
 };
-SampleConsts sample_consts(int n);
+// n tokens, fractions from params (nullable: defaults); false on out-of-range fractions
+bool sample_consts(int n, const tactic_params_t* params, SampleConsts* out);
 // programmatic dependent launch between the decode kernels (TACTIC_NO_PDL=1 disables)
 bool pdl_enabled();
+// Dynamic shared-memory opt-in of kernel `fn` for at least `bytes` on the CURRENT device
+// (function attributes are per device; cached per (fn, device), thread-safe);
+// nonportable_cluster also allows clusters of more than 8 CTAs.
+cudaError_t func_smem_optin(const void* fn, size_t bytes, bool nonportable_cluster = false);
 
 // Unit-aligned attention split applies when every unit can get >= 2 CTAs; otherwise the
 // attention kernel cuts the global token list (and the fit kernel computes unit_prefix).
@@ -112,6 +117,7 @@ struct tactic_index_s {
   __nv_bfloat16* q_stage = nullptr;  // [units][G][128] (host-buffer decode)
   __nv_bfloat16* o_stage = nullptr;
   long long device_bytes = 0;
+  bool lists_valid = false;      // a p < 1 selection has been enqueued (attention-only needs its lists)
   unsigned long long* tlog = nullptr;  // [units][16][8] phase timestamps (TACTIC_TLOG=1)
 };
 
@@ -185,6 +191,10 @@ cudaError_t launch_sample(const SelArgs& a, cudaStream_t s, bool pdl);
 cudaError_t launch_select(const SelArgs& a, cudaStream_t s, bool pdl);
 cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl);
 int sample_blocks(int slots);
+// dynamic shared memory of the fit kernel (every decode with p < 1) and of the sharded
+// stages' select kernel; checked against the device's opt-in limit at build / import
+size_t fit_smem_bytes(const tactic_index_s* x, bool windows_exact);
+size_t select_smem_bytes(const tactic_index_s* x);
 cudaError_t launch_stage1b(const SelArgs& a, cudaStream_t s);
 // fused S1-S7 (select_fused.cu)
 

@@ -556,13 +556,8 @@ cudaError_t km_assign(const KmArgs& a, int iter, bool simt, cudaStream_t s) {
     km_assign_simt_kernel<<<grid, 128, 0, s>>>(a, iter, a.changed);
     return cudaGetLastError();
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(km_assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)TC_SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = func_smem_optin((const void*)km_assign_tc_kernel, TC_SMEM);
+  if (e != cudaSuccess) return e;
   km_assign_tc_kernel<<<grid_tc, 192, TC_SMEM, s>>>(a, iter, a.changed);
   return cudaGetLastError();
 }

@@ -804,6 +804,7 @@ struct SelectParams {
   unsigned int* unit_cnt; // [1]
   double* cumend;
   double* local_max;
+  int tail_len;           // recent-token tail per unit (counted in unit_prefix, as the fit kernel does)
 };
 
 __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SelectParams P) {
@@ -993,11 +994,11 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SelectParams 
     const int per = (units + nt - 1) / nt;
     const int b0 = tid * per;
     long long loc = 0;
-    for (int v = b0; v < b0 + per && v < units; ++v) loc += __ldcg(P.uprefix + (size_t)v * (C + 1) + C);
+    for (int v = b0; v < b0 + per && v < units; ++v) loc += __ldcg(P.uprefix + (size_t)v * (C + 1) + C) + P.tail_len;
     long long run = block_exclusive_scan<long long>(loc, (long long*)redd, (long long*)nullptr);
     for (int v = b0; v < b0 + per && v < units; ++v) {
       P.unit_prefix[v] = run;
-      run += __ldcg(P.uprefix + (size_t)v * (C + 1) + C);
+      run += __ldcg(P.uprefix + (size_t)v * (C + 1) + C) + P.tail_len;
     }
     if (b0 < units && b0 + per >= units) P.unit_prefix[units] = run;
     if (tid == 0) *P.unit_cnt = 0u;
@@ -1064,13 +1065,9 @@ cudaError_t launch_score_all(const __nv_bfloat16* q, tactic_index_s* x, cudaStre
   return cudaErrorInvalidValue;
 }
 
-static cudaError_t ensure_smem(const void* fn, size_t smem, size_t* done) {
-  if (smem > 40 * 1024 && smem > *done) {  // static smem counts against the 48 KB default too
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    *done = smem;
-  }
-  return cudaSuccess;
+static cudaError_t ensure_smem(const void* fn, size_t smem) {
+  // static smem counts against the 48 KB default too
+  return smem > 40 * 1024 ? func_smem_optin(fn, smem) : cudaSuccess;
 }
 
 int sample_blocks(int slots) { return (slots + SB - 1) / SB; }
@@ -1082,6 +1079,17 @@ cudaError_t launch_sample(const SelArgs& a, cudaStream_t s, bool pdl) {
   auto cfg = make_cfg(dim3(nb, x->G, x->units), dim3(SB), 0, s, pdl, attr);
   return cudaLaunchKernelEx(&cfg, sample_kernel, a.q, (const __nv_bfloat16*)x->Kp, (const int*)x->rowmap, x->n,
                             x->G, x->sc, x->logits, x->summ, nb, x->tlog);
+}
+
+size_t fit_smem_bytes(const tactic_index_s* x, bool windows_exact) {
+  const int nb = sample_blocks(x->sc.slots);
+  return (size_t)x->G * nb * 16 + 16 + (size_t)(x->C + 4) * 4 + (size_t)2 * x->G * x->C * 4 + (size_t)x->C + 64 +
+         (windows_exact ? (size_t)x->G * ((((size_t)2 * (2 * x->sc.w + 1) + 6) & ~(size_t)3) + 4) * 4 + 16 : 0);
+}
+
+size_t select_smem_bytes(const tactic_index_s* x) {
+  const int nex = x->sc.fallback ? x->n : x->sc.N;
+  return (size_t)(nex > 0 ? nex : 1) * 8 + (size_t)x->C * 4 + 16;
 }
 
 cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
@@ -1112,11 +1120,8 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
   P.fixed_budget = x->fixed_budget;
   P.windows_exact = (x->options & 1u) ? 1 : 0;
   cudaLaunchAttribute attr[1];
-  const size_t smem =
-      (size_t)x->G * P.nb * 16 + 16 + (size_t)(x->C + 4) * 4 + (size_t)2 * x->G * x->C * 4 + (size_t)x->C + 64 +
-      (P.windows_exact ? (size_t)x->G * ((((size_t)2 * (2 * x->sc.w + 1) + 6) & ~(size_t)3) + 4) * 4 + 16 : 0);
-  static size_t done = 0;
-  cudaError_t e = ensure_smem((const void*)fit_unit_kernel, smem, &done);
+  const size_t smem = fit_smem_bytes(x, P.windows_exact != 0);
+  cudaError_t e = ensure_smem((const void*)fit_unit_kernel, smem);
   if (e != cudaSuccess) return e;
   auto cfg = make_cfg(dim3(x->units), dim3(FITU_THREADS), smem, s, pdl, attr);
   return cudaLaunchKernelEx(&cfg, fit_unit_kernel, P);
@@ -1124,10 +1129,8 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
 
 cudaError_t launch_select(const SelArgs& a, cudaStream_t s, bool pdl) {
   tactic_index_s* x = a.idx;
-  const int nex = x->sc.fallback ? x->n : x->sc.N;
-  const size_t smem = (size_t)(nex > 0 ? nex : 1) * 8 + (size_t)x->C * 4 + 16;
-  static size_t done = 0;
-  cudaError_t e = ensure_smem((const void*)select_kernel, smem, &done);
+  const size_t smem = select_smem_bytes(x);
+  cudaError_t e = ensure_smem((const void*)select_kernel, smem);
   if (e != cudaSuccess) return e;
   SelectParams P = {};
   P.logits = x->logits;
@@ -1155,6 +1158,7 @@ cudaError_t launch_select(const SelArgs& a, cudaStream_t s, bool pdl) {
   P.unit_cnt = x->counter;
   P.cumend = x->cumend;
   P.local_max = a.local_max;
+  P.tail_len = x->tail_len;
   cudaLaunchAttribute attr[1];
   auto cfg = make_cfg(dim3(x->G, x->units), dim3(SEL_THREADS), smem, s, pdl, attr);
   return cudaLaunchKernelEx(&cfg, select_kernel, P);

@@ -7,6 +7,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -128,6 +130,25 @@ int device_sms() {
 }  // namespace
 
 namespace tactic {
+cudaError_t func_smem_optin(const void* fn, size_t bytes, bool nonportable_cluster) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{fn, dev}];
+  if (have >= bytes && have > 0) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  if (nonportable_cluster) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  have = bytes > 0 ? bytes : 1;
+  return cudaSuccess;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("TACTIC_NO_PDL");
@@ -136,17 +157,30 @@ bool pdl_enabled() {
   return on;
 }
 
-SampleConsts sample_consts(int n) {
+// Readings 8-10 and tactic_params_t: fractions quantised to ppm, then integer rules.
+static long long ppm_of(float f, float dflt) {
+  const double v = (f == 0.0f ? dflt : f);
+  if (!(v > 0.0) || !(v < 1.0)) return -1;
+  return (long long)floor(v * 1e6 + 0.5);
+}
+
+bool sample_consts(int n, const tactic_params_t* params, SampleConsts* out) {
+  const tactic_params_t d = {};
+  const tactic_params_t* P = params ? params : &d;
+  const long long e = ppm_of(P->exact_frac, 0.02f), q1 = ppm_of(P->p1, 0.10f), q2 = ppm_of(P->p2, 0.60f),
+                  h = ppm_of(P->window_half_frac, 0.0025f);
+  if (e < 1 || h < 1 || q1 < 1 || q2 <= q1 || q2 >= 1000000 || n < 1) return false;
   SampleConsts s;
   const long long nn = n;
-  s.N = (int)((2 * nn + 99) / 100);
-  s.x1 = (int)((nn + 5) / 10);
-  s.x2 = (int)((6 * nn + 5) / 10);
-  const long long w = (25 * nn + 5000) / 10000;
+  s.N = (int)((e * nn + 999999) / 1000000);
+  s.x1 = (int)((2 * q1 * nn + 1000000) / 2000000);
+  s.x2 = (int)((2 * q2 * nn + 1000000) / 2000000);
+  const long long w = (2 * h * nn + 1000000) / 2000000;
   s.w = (int)(w > 1 ? w : 1);
   s.fallback = (s.x1 - s.w <= s.N) || (s.x1 + s.w >= s.x2 - s.w) || (s.x2 + s.w > n);
   s.slots = s.fallback ? n : s.N + 2 * (2 * s.w + 1);
-  return s;
+  *out = s;
+  return true;
 }
 }  // namespace tactic
 
@@ -161,12 +195,12 @@ static void free_index(tactic_index_s* x, std::vector<void*>* ptrs) {
 }
 
 // all index allocations are recorded here (keyed by index pointer)
-#include <map>
-#include <mutex>
 static std::mutex g_mu;
 static std::map<tactic_index_s*, std::vector<void*>> g_allocs;
 
-static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_ctas, tactic_index_s** out) {
+static tactic_status_t alloc_index(const Resolved& r, int C, int iters, const tactic_params_t& prm,
+                                   tactic_index_s** out) {
+  const int num_ctas = prm.num_ctas;
   tactic_index_s* x = new tactic_index_s();
   x->B = r.B;
   x->Hkv = r.Hkv;
@@ -178,7 +212,11 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_
   cudaGetDevice(&x->device);
   x->num_sms = device_sms();
   x->num_ctas = num_ctas > 0 ? num_ctas : x->num_sms;
-  x->sc = sample_consts(r.n);
+  if (!sample_consts(r.n, &prm, &x->sc)) {
+    delete x;
+    return fail(TACTIC_ERR_INVALID_ARGUMENT, "sampling fractions out of range (0 < exact_frac, window_half_frac; "
+                "0 < p1 < p2 < 1)");
+  }
   const size_t U = x->units, n = x->n, G = x->G;
   DevAlloc A;
   auto carve = [&]() {
@@ -242,6 +280,9 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_
   cudaMemset(x->order, 0, U * G * C * sizeof(int));  // valid cluster ids before the first decode
 
   cudaMemset(x->ends, 0, U * G * C * sizeof(int));
+  cudaMemset(x->union_list, 0, (U * C + 4) * sizeof(int));   // valid (empty) work lists before
+  cudaMemset(x->union_prefix, 0, (U * (C + 1) + 4) * sizeof(int));  // the first selection
+  cudaMemset(x->unit_prefix, 0, (U + 1) * sizeof(long long));
   std::vector<long long> up(U + 1);
   for (size_t u = 0; u <= U; ++u) up[u] = (long long)u * (long long)n;
   cudaMemcpy(x->all_unit_prefix, up.data(), (U + 1) * sizeof(long long), cudaMemcpyHostToDevice);
@@ -250,6 +291,25 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, int num_
     g_allocs[x] = A.ptrs;
   }
   *out = x;
+  return TACTIC_OK;
+}
+
+static size_t smem_optin_limit() {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 227 * 1024;
+  return (size_t)v;
+}
+
+// the per-unit selection keeps G x C order / end ranks and the per-block sample summaries
+// in one CTA's shared memory (fit kernel); reject sizes that cannot launch
+static tactic_status_t check_select_limits(const tactic_index_s* x, bool windows_exact) {
+  const size_t need = fit_smem_bytes(x, windows_exact), lim = smem_optin_limit();
+  if (need > lim)
+    return fail(TACTIC_ERR_UNSUPPORTED,
+                "selection needs %zu bytes of shared memory per unit (G = %d, C = %d, %d sampled slots%s) > %zu: "
+                "reduce n_clusters or the group size", need, x->G, x->C, x->sc.slots,
+                windows_exact ? ", windows-exact" : "", lim);
   return TACTIC_OK;
 }
 
@@ -284,7 +344,11 @@ static tactic_status_t build_common(const void* K, const void* V, const tactic_k
   tactic_params_t P = {};
   if (params) P = *params;
   tactic_index_s* x = nullptr;
-  if ((st = alloc_index(r, C, iters, P.num_ctas, &x))) return st;
+  if ((st = alloc_index(r, C, iters, P, &x))) return st;
+  if ((st = check_select_limits(x, false))) {
+    tactic_index_destroy(x);
+    return st;
+  }
   const int units = x->units;
   KmArgs a = {};
   a.K = (const __nv_bfloat16*)K;
@@ -498,6 +562,8 @@ tactic_status_t tactic_assign_tokens(tactic_index_t idx, const void* k, int32_t 
 tactic_status_t tactic_index_set_options(tactic_index_t idx, uint32_t options) {
   if (!idx) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL index");
   if (options & ~(uint32_t)TACTIC_OPT_WINDOWS_EXACT) return fail(TACTIC_ERR_INVALID_ARGUMENT, "unknown option bits");
+  tactic_status_t st = check_select_limits(idx, (options & TACTIC_OPT_WINDOWS_EXACT) != 0);
+  if (st) return st;
   idx->options = options;
   return TACTIC_OK;
 }
@@ -515,6 +581,29 @@ tactic_status_t tactic_index_debug_timing(tactic_index_t idx, uint64_t* host, in
   const size_t n = tlog_entries(idx->units);
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(host, idx->tlog, (count < (int32_t)n ? (size_t)count : n) * 8, cudaMemcpyDeviceToHost));
+  return TACTIC_OK;
+}
+
+static void sc_out(const SampleConsts& sc, tactic_sample_constants_t* out) {
+  out->N = sc.N;
+  out->x1 = sc.x1;
+  out->x2 = sc.x2;
+  out->w = sc.w;
+  out->fallback = sc.fallback ? 1 : 0;
+  out->slots = sc.slots;
+}
+
+tactic_status_t tactic_sample_constants(int32_t n, const tactic_params_t* params, tactic_sample_constants_t* out) {
+  if (!out) return fail(TACTIC_ERR_INVALID_ARGUMENT, "out is NULL");
+  SampleConsts sc;
+  if (!sample_consts(n, params, &sc)) return fail(TACTIC_ERR_INVALID_ARGUMENT, "bad n or sampling fractions");
+  sc_out(sc, out);
+  return TACTIC_OK;
+}
+
+tactic_status_t tactic_index_sample_constants(tactic_index_t idx, tactic_sample_constants_t* out) {
+  if (!idx || !out) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  sc_out(idx->sc, out);
   return TACTIC_OK;
 }
 
@@ -586,8 +675,16 @@ static tactic_status_t run_selection(const void* q, tactic_index_t idx, double p
   } else {
     CK(launch_score(sa, s, false));            // S1 only (sharded stage 2)
   }
-  if (mode == 0) CK(launch_fit(sa, s, pdl));     // S5-S7
-  else CK(launch_select(sa, s, pdl));            // sharded stage rules
+  if (mode == 0) {
+    CK(launch_fit(sa, s, pdl));                  // S5-S7
+    idx->lists_valid = true;
+  } else {
+    if (select_smem_bytes(idx) > smem_optin_limit())
+      return fail(TACTIC_ERR_UNSUPPORTED, "sharded selection: exact head of %d ranks exceeds shared memory",
+                  idx->sc.fallback ? idx->n : idx->sc.N);
+    CK(launch_select(sa, s, pdl));               // sharded stage rules
+    if (mode == 1) idx->lists_valid = true;
+  }
   return TACTIC_OK;
 }
 
@@ -639,6 +736,8 @@ tactic_status_t tactic_decode_ex(const void* q, tactic_index_t idx, float p, voi
 
 tactic_status_t tactic_decode_attention_only(const void* q, tactic_index_t idx, void* out, void* stream) {
   if (!q || !idx || !out) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!idx->lists_valid)
+    return fail(TACTIC_ERR_INVALID_ARGUMENT, "no selection has run on this index yet (call tactic_decode with p < 1)");
   return run_attention(q, idx, false, (cudaStream_t)stream, out, nullptr, nullptr, nullptr, true);
 }
 

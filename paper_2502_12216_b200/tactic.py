@@ -39,7 +39,25 @@ class KvDesc(ctypes.Structure):
 
 class Params(ctypes.Structure):
     _fields_ = [("seed", ctypes.c_uint64), ("init_indices", ctypes.c_void_p), ("flags", ctypes.c_uint32),
-                ("num_ctas", ctypes.c_int32)]
+                ("num_ctas", ctypes.c_int32), ("exact_frac", ctypes.c_float), ("p1", ctypes.c_float),
+                ("p2", ctypes.c_float), ("window_half_frac", ctypes.c_float)]
+
+
+class SampleConstants(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int32), ("x1", ctypes.c_int32), ("x2", ctypes.c_int32), ("w", ctypes.c_int32),
+                ("fallback", ctypes.c_int32), ("slots", ctypes.c_int32)]
+
+
+SAMPLING_KEYS = ("exact_frac", "p1", "p2", "window_half_frac")
+
+
+def _params(seed=0, init=None, flags=0, num_ctas=0, sampling=None) -> Params:
+    """tactic_params_t; sampling: optional dict of the Alg. 1 fractions (0 / absent = default)."""
+    sampling = dict(sampling or {})
+    bad = set(sampling) - set(SAMPLING_KEYS)
+    if bad:
+        raise ValueError(f"unknown sampling keys {sorted(bad)}")
+    return Params(seed, init, flags, num_ctas, *[float(sampling.get(k, 0.0)) for k in SAMPLING_KEYS])
 
 
 class IndexInfo(ctypes.Structure):
@@ -82,6 +100,8 @@ _SIGS = {
     "tactic_decode_per_head": [_P, _P, _F, _P, _P],
     "tactic_decode_fixed_budget": [_P, _P, _I, _I, _P, _P, _P],
     "tactic_index_set_options": [_P, ctypes.c_uint32],
+    "tactic_sample_constants": [_I, ctypes.POINTER(Params), ctypes.POINTER(SampleConstants)],
+    "tactic_index_sample_constants": [_P, ctypes.POINTER(SampleConstants)],
 }
 
 
@@ -145,14 +165,17 @@ def device_check() -> int:
     return n.value
 
 
-def sample_constants(n: int) -> dict:
-    """The integer sample constants the library uses (mirrors tactic_api.cu; host logic)."""
-    N = (2 * n + 99) // 100
-    x1 = (n + 5) // 10
-    x2 = (6 * n + 5) // 10
-    w = max(1, (25 * n + 5000) // 10000)
-    fb = (x1 - w <= N) or (x1 + w >= x2 - w) or (x2 + w > n)
-    return {"N": N, "x1": x1, "x2": x2, "w": w, "fallback": fb, "slots": n if fb else N + 2 * (2 * w + 1)}
+def _sc_dict(sc: SampleConstants) -> dict:
+    return {"N": sc.N, "x1": sc.x1, "x2": sc.x2, "w": sc.w, "fallback": bool(sc.fallback), "slots": sc.slots}
+
+
+def sample_constants(n: int, sampling: Optional[dict] = None) -> dict:
+    """tactic_sample_constants: the integer Alg. 1 sampling constants the library derives
+    for n tokens from the sampling fractions (host-only call into the library)."""
+    sc = SampleConstants()
+    p = _params(sampling=sampling)
+    _check(lib().tactic_sample_constants(int(n), ctypes.byref(p), ctypes.byref(sc)))
+    return _sc_dict(sc)
 
 
 class Index:
@@ -182,6 +205,11 @@ class Index:
         except Exception:
             pass
 
+    def sample_constants(self) -> dict:
+        sc = SampleConstants()
+        _check(lib().tactic_index_sample_constants(self.handle, ctypes.byref(sc)))
+        return _sc_dict(sc)
+
     def info(self) -> dict:
         i = IndexInfo()
         _check(lib().tactic_index_info(self.handle, ctypes.byref(i)))
@@ -206,7 +234,7 @@ class Index:
 
 def build_index(K: torch.Tensor, V: torch.Tensor, n_clusters: int, iters: int = 10, *, group_size: int = 4,
                 seed: int = 0, init: Optional[np.ndarray] = None, flags: int = 0, num_ctas: int = 0,
-                stream=None) -> Index:
+                sampling: Optional[dict] = None, stream=None) -> Index:
     """tactic_build_index: k-means (tcgen05 assignment) + cluster-contiguous KV layout."""
     kv = _kv_desc(K, group_size)
     if tuple(V.shape) != tuple(K.shape) or V.stride() != K.stride() or V.dtype != K.dtype:
@@ -216,7 +244,7 @@ def build_index(K: torch.Tensor, V: torch.Tensor, n_clusters: int, iters: int = 
         init_arr = np.ascontiguousarray(init, dtype=np.int32)
         if init_arr.shape != (kv.batch * kv.num_kv_heads, n_clusters):
             raise ValueError("init must be [units, n_clusters]")
-    p = Params(seed, init_arr.ctypes.data if init_arr is not None else None, flags, num_ctas)
+    p = _params(seed, init_arr.ctypes.data if init_arr is not None else None, flags, num_ctas, sampling)
     h = ctypes.c_void_p()
     _check(lib().tactic_build_index(_ptr(K), _ptr(V), ctypes.byref(kv), n_clusters, iters, ctypes.byref(p),
                                     _stream(stream), ctypes.byref(h)))
@@ -224,7 +252,7 @@ def build_index(K: torch.Tensor, V: torch.Tensor, n_clusters: int, iters: int = 
 
 
 def import_index(K: torch.Tensor, V: torch.Tensor, centroids: np.ndarray, assign: np.ndarray, *,
-                 group_size: int = 4, num_ctas: int = 0, stream=None) -> Index:
+                 group_size: int = 4, num_ctas: int = 0, sampling: Optional[dict] = None, stream=None) -> Index:
     """tactic_index_import: index from a given clustering (float32 centroids, int32 assignment)."""
     kv = _kv_desc(K, group_size)
     units = kv.batch * kv.num_kv_heads
@@ -235,7 +263,7 @@ def import_index(K: torch.Tensor, V: torch.Tensor, centroids: np.ndarray, assign
     if asg.shape != (units, kv.seq_len):
         raise ValueError("assign must be [units, n]")
     C = cent.shape[1]
-    p = Params(0, None, 0, num_ctas)
+    p = _params(0, None, 0, num_ctas, sampling)
     h = ctypes.c_void_p()
     _check(lib().tactic_index_import(_ptr(K), _ptr(V), ctypes.byref(kv), C, cent.ctypes.data, asg.ctypes.data,
                                      ctypes.byref(p), _stream(stream), ctypes.byref(h)))
@@ -315,12 +343,20 @@ def dense_decode(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, out: Optiona
                  lse: Optional[torch.Tensor] = None, num_ctas: int = 0, workspace: Optional[torch.Tensor] = None,
                  stream=None) -> torch.Tensor:
     """tactic_dense_decode: the library's own full-attention split-KV baseline."""
+    if q.dtype != torch.bfloat16 or not q.is_cuda or not q.is_contiguous() or q.dim() != 3:
+        raise ValueError("q must be a contiguous CUDA bfloat16 tensor [B, Hq, 128]")
+    if K.dim() != 4 or q.shape[0] != K.shape[0] or q.shape[2] != HEAD_DIM or q.shape[1] % K.shape[1]:
+        raise ValueError("q must be [B, Hkv*G, 128] for K [B, Hkv, n, 128]")
+    if tuple(V.shape) != tuple(K.shape) or V.stride() != K.stride() or V.dtype != K.dtype:
+        raise ValueError("V must match K in shape, strides and dtype")
     G = q.shape[1] // K.shape[1]
     kv = _kv_desc(K, G)
     sz = ctypes.c_size_t()
     _check(lib().tactic_dense_workspace_size(ctypes.byref(kv), num_ctas, ctypes.byref(sz)))
     if workspace is None:
-        key = (q.device.index, sz.value)
+        # the workspace holds self-resetting arrival counters: one per (device, stream)
+        s_ = stream if stream is not None else torch.cuda.current_stream(q.device)
+        key = (q.device.index, s_.cuda_stream, sz.value)
         workspace = _ws_cache.get(key)
         if workspace is None:
             workspace = torch.zeros(sz.value, dtype=torch.uint8, device=q.device)

@@ -65,3 +65,27 @@ def test_kernels_are_sm100a_tensor_core_and_tma():
     for mnem in ("UTCHMMA", "LDTM", "UBLKCP", "UTMALDG", "HMMA.16816.F32.BF16"):
         assert mnem in sass, mnem
     assert "sm_100a" in subprocess.run([exe, "-lelf", lib], capture_output=True, text=True).stdout
+
+
+def test_library_sample_constants_equal_the_oracle_rule(L):
+    """tactic_sample_constants (host logic, no device) against the oracle's ppm rule
+    (readings 8-10) for default and custom fractions over many n, and its
+    argument validation."""
+    import numpy as np
+
+    from oracle import tactic_oracle as O
+    from paper_2502_12216_b200 import tactic
+    rng = np.random.default_rng(5)
+    ns = list(range(1, 3000)) + [int(x) for x in rng.integers(3000, 1 << 20, 2000)]
+    fracs = [None, dict(exact_frac=0.01, p1=0.2, p2=0.5, window_half_frac=0.01),
+             dict(exact_frac=0.015, p1=0.25, p2=0.75, window_half_frac=0.001),
+             dict(exact_frac=0.05, p1=0.1, p2=0.9, window_half_frac=0.0005)]
+    for f in fracs:
+        for n in ns[::3]:
+            got = tactic.sample_constants(n, f)
+            ref = O.sample_constants(n, **(f or {}))
+            assert {k: got[k] for k in ref} == ref, (n, f)
+            assert got["slots"] == (n if ref["fallback"] else ref["N"] + 2 * (2 * ref["w"] + 1))
+    for bad in [dict(p1=0.6, p2=0.1), dict(p2=1.0), dict(exact_frac=-0.1)]:
+        with pytest.raises(tactic.TacticError):
+            tactic.sample_constants(1000, bad)
