@@ -8,11 +8,16 @@ sort, sampled exact scoring, a/x+b fit, estimated-mass selection, GQA union + wo
 split-KV flash-decode, LSE merge) over one C2 layer: Llama-3-8B shape (32 Q / 8 KV
 heads, d=128), 128K context, batch 1, 1024 clusters per KV head, p=0.9, bf16 KV.
 The index (tcgen05 k-means + cluster-contiguous relayout) is built once per layer and
-timed separately ("build").  N>1 (torchrun): each rank runs its own batch-1 C2 layer
-(batch x KV-head sharding, no collective on the data path), scaling "weak"; the
-reported time is the max over ranks divided by N (job-level us per layer-step).
+timed separately ("build").  N GPUs (`--gpus N` re-launches itself under torchrun, one
+rank per GPU): the 8 units (KV heads) of every C2 layer are split into contiguous blocks,
+one per rank (batch x KV-head sharding; no collective on the data
+path), each rank builds and decodes its block, and the reported time is the max over
+ranks of the layer-step time -- the same job on more GPUs ("scaling": "strong").  C3 (batch
+64 x 32K, 512 units) is sharded the same way (512 / N units per GPU) and reported in `c3`;
+C4 (sequence-sharded, one 131072-token shard per GPU) is timed with its three NCCL
+collectives in `c4`.
 
-Layers: the timed steps cycle over LAYERS = 8 distinct synthetic layers (seeds 8 rank + l),
+Layers: the timed steps cycle over LAYERS = 8 distinct synthetic layers (seeds 0..7),
 one index each, as a model's decode does (>= 8 distinct layer caches); the
 selected fraction varies from layer to layer, so the mean is over layers.
 L2: a 256 MiB buffer is written before every timed step as well (the sparse working set
@@ -44,15 +49,22 @@ PAPER_CONTEXT = ("paper (context, not target): up to 7.29x decode-attention and 
 
 
 def _config(args, n_gpus):
-    return {"workload": f"{WORKLOAD}: Llama-3-8B layer (32 Q / 8 KV heads, d=128), 128K context, batch 1 per GPU, "
+    return {"workload": f"{WORKLOAD}: Llama-3-8B layer (32 Q / 8 KV heads, d=128), 128K context, batch 1, "
                         f"1024 clusters/KV head, p={args.p}",
-            "global_batch": n_gpus, "seq_len": CFG["n"], "n_clusters": CFG["C"], "p": args.p,
-            "parallelism": f"batch x KV-head sharded over {n_gpus} GPU(s), no data-path collective",
+            "global_batch": 1, "seq_len": CFG["n"], "n_clusters": CFG["C"], "p": args.p,
+            "parallelism": f"batch x KV-head: the layer's 8 units in contiguous blocks over {n_gpus} GPU(s) "
+                           f"(units per GPU: {[b - a for a, b in (_unit_block(8, n_gpus, r) for r in range(n_gpus))]}), "
+                           "no data-path collective; time = max over ranks",
             "l2": "cold L2 before every timed step: 256 MiB buffer written, then a 256 MiB buffer read (write-back drained); "
                   "within a step each layer reads its own K/V (512 MB per layer > L2)",
             "step": f"one decode step through all {LAYERS} synthetic layers, one CUDA graph, layers serialised "
                     f"(no cross-layer overlap); value = step time / {LAYERS}",
-            "inputs": f"tactic-synth-v1 (synth/), {LAYERS} layers per GPU (seeds {LAYERS} rank + l)"}
+            "inputs": f"tactic-synth-v1 (synth/), {LAYERS} layers (seeds 0..{LAYERS - 1}), unit (b, h) seeded by (seed, b, h)"}
+
+
+def _unit_block(units, world, rank):
+    from paper_2502_12216_b200.sharded import unit_block
+    return unit_block(units, world, rank)
 
 
 def _peaks():
@@ -117,11 +129,10 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ byte model
-def step_bytes(dbg, sizes, G, n, C):
+def step_bytes(dbg, sizes, G, n, C, sc):
     """Algorithmic bytes of one layer-step: fp32 centroids, sampled K rows not re-read by the
-    attention, selected (union) K+V rows, q/out, from the selection the GPU actually made."""
-    from paper_2502_12216_b200.tactic import sample_constants
-    sc = sample_constants(n)
+    attention, selected (union) K+V rows, q/out, from the selection the GPU actually made
+    (sc: the index's sampling constants, tactic_index_sample_constants)."""
     units = sizes.shape[0]
     tot_union, tot_sampled_extra = 0, 0
     for u in range(units):
@@ -159,7 +170,7 @@ def run_reference(args, rank, world):
     from synth import make_unit
     threads = _cpu_threads()
     u = make_unit(CFG["n"], CFG["G"], seed=0, b=0, h=0)
-    idx, _ = O.build_index(u["K"], u["V"], CFG["C"], 1, seed=0, unit=0)   # setup, untimed
+    idx, _ = O.build_index(u["K"], u["V"], CFG["C"], CFG["iters"], seed=0, unit=0)   # setup, untimed
     for _ in range(args.warmup):
         O.decode_unit(u["q"], idx, args.p)
     ts = []
@@ -174,8 +185,8 @@ def run_reference(args, rank, world):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": _config(args, world),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "oracle",
-                             "sample": f"1 of 8 units per step (KV head 0, n=131072, C=1024; index from 1 oracle "
-                                       f"Lloyd iteration, untimed), scaled x8 to a layer-step"},
+                             "sample": f"1 of 8 units per step (KV head 0 of layer 0, n=131072, C=1024; index from "
+                                       f"the oracle's own {CFG['iters']}-iteration k-means, untimed), scaled x8 to a layer-step"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -191,103 +202,284 @@ def _cpu_threads():
     return len(os.sched_getaffinity(0))
 
 
-def cpu_baseline(args, budget_s=12.0):
-    """Time the oracle decode (as it stands) on a bounded sample of the C2 workload."""
+def cpu_baseline(args, K, V, q, cents, assign, budget_s=12.0):
+    """Time the oracle decode (as it stands) on a bounded sample of the C2 workload: unit 0
+    of layer 0 on the SAME clustering the GPU decodes (the GPU's 10-iteration index,
+    exported), so both sides select from one index."""
     from oracle import tactic_oracle as O
-    from synth import make_unit
-    u = make_unit(CFG["n"], CFG["G"], seed=0, b=0, h=0)
-    idx, _ = O.build_index(u["K"], u["V"], CFG["C"], 1, seed=0, unit=0)
-    O.decode_unit(u["q"], idx, args.p)
+    idx = O.make_index(K, V, cents, assign)
+    O.decode_unit(q, idx, args.p)
     ts, t_start = [], time.perf_counter()
     while time.perf_counter() - t_start < budget_s or len(ts) < 3:
         t0 = time.perf_counter()
-        O.decode_unit(u["q"], idx, args.p)
+        O.decode_unit(q, idx, args.p)
         ts.append(time.perf_counter() - t0)
         if len(ts) >= 400:
             break
     val = float(np.mean(ts)) * CFG["B"] * CFG["Hkv"] * 1e6
     return {"value": val, "unit": UNIT, "cores": _cpu_threads(), "kind": "oracle",
-            "sample": f"{len(ts)} oracle decode_unit calls on KV head 0 of C2 (n=131072, C=1024, G=4, p={args.p}; "
-                      f"index from 1 untimed oracle Lloyd iteration), mean x 8 units = one layer-step"}
+            "sample": f"{len(ts)} oracle decode_unit calls on KV head 0 of C2 layer 0 (n=131072, C=1024, G=4, "
+                      f"p={args.p}; the GPU's {CFG['iters']}-iteration clustering, exported), mean x 8 units = one "
+                      "layer-step"}
 
 
 # ------------------------------------------------------------------ GPU arm
 def _unit_bits(job):
     from synth import bf16_bits, make_unit
-    seed, b, h, n, G = job
+    key, j, seed, b, h, n, G, q_seed = job
     u = make_unit(n, G, seed=seed, b=b, h=h)
-    return seed, b, h, bf16_bits(u["K"]), bf16_bits(u["V"]), bf16_bits(u["q"])
+    qb = bf16_bits(u["q"])
+    if q_seed is not None:   # sequence-sharded C4: every shard sees the query of shard 0
+        qb = bf16_bits(make_unit(n, G, seed=q_seed, b=b, h=h)["q"])
+    return key, j, bf16_bits(u["K"]), bf16_bits(u["V"]), qb
 
 
-def make_layers(seeds, dev, B=1, Hkv=None, n=None):
-    """The synthetic layers (one per seed) as bf16 device tensors [B][Hkv][n][128],
-    generated in parallel on the host cores (input generation only; synth/ holds no
-    method arithmetic)."""
+def make_layers(seeds, dev, pairs, n=None, q_seed=None):
+    """One synthetic layer per seed holding the units `pairs` = [(b, h), ...] (this rank's
+    block), as bf16 device tensors K, V [1][len(pairs)][n][128] and q [1][len(pairs) G][128];
+    unit (b, h) of layer `seed` is make_unit(seed, b, h) whichever rank holds it.  Generated
+    in parallel on the host cores (input generation only; synth/ holds no method arithmetic)."""
     import multiprocessing as mp
 
     import torch
-    Hkv = Hkv or CFG["Hkv"]
     n = n or CFG["n"]
     G = CFG["G"]
+    U = len(pairs)
     bf = lambda a: torch.from_numpy(a.view(np.int16)).to(dev).view(torch.bfloat16)  # noqa: E731
-    layers = {sd: {"K": torch.empty((B, Hkv, n, 128), dtype=torch.bfloat16, device=dev),
-                   "V": torch.empty((B, Hkv, n, 128), dtype=torch.bfloat16, device=dev),
-                   "q": torch.empty((B, Hkv * G, 128), dtype=torch.bfloat16, device=dev)} for sd in seeds}
-    jobs = [(sd, b, h, n, G) for sd in seeds for b in range(B) for h in range(Hkv)]
+    layers = {sd: {"K": torch.empty((1, U, n, 128), dtype=torch.bfloat16, device=dev),
+                   "V": torch.empty((1, U, n, 128), dtype=torch.bfloat16, device=dev),
+                   "q": torch.empty((1, U * G, 128), dtype=torch.bfloat16, device=dev), "seed": sd,
+                   "pairs": list(pairs)} for sd in seeds}
+    jobs = [(sd, j, sd, b, h, n, G, q_seed) for sd in seeds for j, (b, h) in enumerate(pairs)]
     workers = max(1, min(len(jobs), len(os.sched_getaffinity(0)) - 1, 32))
     with mp.get_context("fork").Pool(workers) as pool:
-        for sd, b, h, kb, vb, qb in pool.imap_unordered(_unit_bits, jobs, chunksize=4):
+        for sd, j, kb, vb, qb in pool.imap_unordered(_unit_bits, jobs, chunksize=2):
             L = layers[sd]
-            L["K"][b, h] = bf(kb)
-            L["V"][b, h] = bf(vb)
-            L["q"][b, h * G:(h + 1) * G] = bf(qb)
+            L["K"][0, j] = bf(kb)
+            L["V"][0, j] = bf(vb)
+            L["q"][0, j * G:(j + 1) * G] = bf(qb)
     return [layers[sd] for sd in seeds]
 
 
-C3 = dict(B=64, Hkv=8, n=32768, C=256, iters=10)
+C3 = dict(B=64, Hkv=8, n=32768, C=256, iters=10, seed=9000)
+C4 = dict(n_shard=131072, Hkv=8, C=1024, iters=10, seed=7000)
 
 
-def measure_c3(T, dev, p, steps, timed_loop):
-    """BASELINE.json configs[2] on this GPU: Llama-3-8B layer, 32K context, batch 64
-    (512 units, 256 clusters each): decode layer-step vs the own dense decode (the global
-    token split of the attention kernel: more units than half the CTAs)."""
+class Timer:
+    """CUDA-event timing on the launching stream with an L2 flush before every timed
+    replay, barriers around the timed region and the max over ranks."""
+
+    def __init__(self, dev, world):
+        import torch
+        self.world = world
+        self.flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        self.flush_r = torch.ones(32 << 20, dtype=torch.int64, device=dev)
+        self.flush_acc = torch.empty((), dtype=torch.int64, device=dev)
+        self.dev = dev
+
+    def l2_flush(self):
+        # cold L2 before every timed step: write a 256 MiB buffer (> 126 MB L2), then read a
+        # second one so the dirty lines of the write are written back before the step starts
+        import torch
+        self.flush.fill_(1)
+        torch.sum(self.flush_r, dim=0, out=self.flush_acc)
+
+    def loop(self, fns, steps, flush_each=True):
+        import torch
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for i, (a, b) in enumerate(evs):
+            if flush_each:
+                self.l2_flush()
+            a.record()
+            fns[i % len(fns)]()
+            b.record()
+        return evs
+
+    def barrier(self):
+        import torch
+        import torch.distributed as dist
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(self, *vals):
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return vals if len(vals) > 1 else vals[0]
+        t = torch.tensor(list(vals), dtype=torch.float64, device=self.dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out = [float(x) for x in t.tolist()]
+        return out if len(out) > 1 else out[0]
+
+    def timed(self, fns, steps, warmup=3):
+        """mean ms per call over `steps` timed calls; max over ranks"""
+        import torch
+        self.loop(fns, warmup)
+        self.barrier()
+        evs = self.loop(fns, steps)
+        torch.cuda.synchronize()
+        ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+        self.barrier()
+        return self.max_over_ranks(ms)
+
+
+def capture(fn):
     import torch
-    L = make_layers([9000], dev, B=C3["B"], Hkv=C3["Hkv"], n=C3["n"])[0]
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    torch.cuda.synchronize()
+    return g
+
+
+def phase_timeline(T, L, args, tm, reps=20):
+    """In-graph %globaltimer phases of one decode layer-step (S1-S3 score + rank, S4 sample,
+    S5-S7 fit + union work list, S8-S9 attention + merge) on layer L, from an index built
+    with the library's debug timeline (TACTIC_TLOG=1: each decode kernel stamps its first
+    CTA's start and the last CTA's end).  Medians over `reps` cold-L2 replays."""
+    import torch
+    os.environ["TACTIC_TLOG"] = "1"
+    try:
+        idx = T.build_index(L["K"], L["V"], CFG["C"], CFG["iters"], group_size=CFG["G"], seed=L["seed"],
+                            unit_offset=L["u0"])
+    finally:
+        del os.environ["TACTIC_TLOG"]
+    out = torch.empty_like(L["q"])
+    g = capture(lambda: T.decode(L["q"], idx, args.p, out=out))
+    rows = []
+    for _ in range(reps):
+        tm.l2_flush()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        tl = idx.debug_timing().astype(np.int64)[1536:1536 + 20].reshape(5, 4)
+        k_rank, k_sample, k_fit, k_att = 1, 2, 3, 4
+        t0 = tl[k_rank, 0]
+        rows.append([(tl[k_rank, 2] - t0), (tl[k_sample, 2] - tl[k_rank, 2]), (tl[k_fit, 2] - tl[k_sample, 2]),
+                     (tl[k_att, 2] - tl[k_fit, 2]), (tl[k_att, 2] - t0)])
+    med = np.median(np.array(rows, dtype=np.float64), axis=0) / 1e3
+    del g, idx
+    return {"S1_S3_score_rank": med[0], "S4_sample": med[1], "S5_S7_fit_union": med[2],
+            "S8_S9_attention_merge": med[3], "total": med[4],
+            "method": "in-graph %globaltimer (TACTIC_TLOG=1 index of layer 0): score_rank start -> its last CTA "
+                      "end -> sample end -> fit end -> attention end; S9 is fused into the attention kernel; "
+                      f"median of {reps} cold-L2 replays; debug stamps add ~0.5 us"}
+
+
+def measure_c3(T, dev, args, rank, world, tm):
+    """BASELINE.json configs[2]: Llama-3-8B layer, 32K context, batch 64 (512 units, 256
+    clusters each), the 512 units sharded over the ranks in contiguous blocks: decode
+    layer-step vs the own dense decode, max over ranks."""
+    import torch
+    from paper_2502_12216_b200.sharded import block_units, unit_block
+    units = C3["B"] * C3["Hkv"]
+    u0, u1 = unit_block(units, world, rank)
+    L = make_layers([C3["seed"]], dev, block_units(units, C3["Hkv"], world, rank), n=C3["n"])[0]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    idx = T.build_index(L["K"], L["V"], C3["C"], C3["iters"], group_size=CFG["G"], seed=9000)
+    idx = T.build_index(L["K"], L["V"], C3["C"], C3["iters"], group_size=CFG["G"], seed=C3["seed"], unit_offset=u0)
     e1.record()
     torch.cuda.synchronize()
     build_ms = e0.elapsed_time(e1)
     ex = idx.export()
-    units = idx.units
-    sizes = np.stack([np.bincount(ex["assign"][u], minlength=C3["C"]) for u in range(units)])
+    sizes = np.stack([np.bincount(ex["assign"][u], minlength=C3["C"]) for u in range(idx.units)])
     out = torch.empty_like(L["q"])
-    T.decode(L["q"], idx, p, out=out)
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        T.decode(L["q"], idx, p, out=out)
+    g = capture(lambda: T.decode(L["q"], idx, args.p, out=out))
     dout = torch.empty_like(L["q"])
-    T.dense_decode(L["q"], L["K"], L["V"], out=dout)
-    gd = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(gd):
-        T.dense_decode(L["q"], L["K"], L["V"], out=dout)
-    k = max(10, min(steps, 50))
-    timed_loop([g.replay], 3)
-    ev = timed_loop([g.replay], k)
-    torch.cuda.synchronize()
-    us = 1e3 * float(np.mean([a.elapsed_time(b) for a, b in ev]))
-    timed_loop([gd.replay], 3)
-    ev = timed_loop([gd.replay], k)
-    torch.cuda.synchronize()
-    dus = 1e3 * float(np.mean([a.elapsed_time(b) for a, b in ev]))
-    dbg = T.decode_debug(L["q"], idx, p)
-    uf = sum(int(sizes[u][dbg["union_mask"][u].astype(bool)].sum()) for u in range(units)) / (units * C3["n"])
+    gd = capture(lambda: T.dense_decode(L["q"], L["K"], L["V"], out=dout))
+    k = max(10, min(args.steps, 50))
+    us = 1e3 * tm.timed([g.replay], k)
+    dus = 1e3 * tm.timed([gd.replay], k)
+    dbg = T.decode_debug(L["q"], idx, args.p)
+    tok = sum(int(sizes[u][dbg["union_mask"][u].astype(bool)].sum()) for u in range(idx.units))
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([float(tok)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        tok = float(t.item())
+    uf = tok / (units * C3["n"])
     dense_bytes = 2 * units * C3["n"] * 256
-    res = {"workload": "C3: Llama-3-8B layer, 32K context, batch 64 (512 units), 256 clusters/KV head, "
-                       f"p={p}, 1 GPU", "us_per_layer_step": us, "dense_us_per_layer_step": dus,
-           "speedup_vs_dense": dus / us, "union_frac": uf, "dense_gbs": dense_bytes / (dus * 1e-6) / 1e9,
-           "build_ms": build_ms}
+    res = {"workload": f"C3: Llama-3-8B layer, 32K context, batch 64 (512 units), 256 clusters/KV head, p={args.p}; "
+                       f"units sharded over {world} GPU(s) ({u1 - u0} on rank {rank}), time = max over ranks",
+           "us_per_layer_step": us, "dense_us_per_layer_step": dus, "speedup_vs_dense": dus / us,
+           "union_frac": uf, "dense_gbs_job": dense_bytes / (dus * 1e-6) / 1e9, "build_ms": build_ms,
+           "units_per_gpu": u1 - u0, "n_gpus": world,
+           "gpu_launches_per_step": 5}   # score (all heads), rank, sample, fit, attention
+    del L, idx, g, gd
+    torch.cuda.empty_cache()
+    return res
+
+
+def measure_c4(T, dev, args, rank, world, tm):
+    """BASELINE.json configs[3] scaled to the job's GPUs: a context of world x 131072 tokens
+    sequence-sharded one shard per rank (8 KV heads per shard, C = 1024; world = 8 is the 1M
+    configuration).  One decode step = stage1 -> NCCL all-reduce MAX -> stage1b -> NCCL
+    all-reduce SUM -> stage2 -> NCCL all-gather of (o, lse) -> LSE merge (reading 23),
+    timed as one step, plus the compute alone and the three collectives alone."""
+    import torch
+    import torch.distributed as dist
+    G, Hkv, n = CFG["G"], C4["Hkv"], C4["n_shard"]
+    pairs = [(0, h) for h in range(Hkv)]
+    L = make_layers([C4["seed"] + rank], dev, pairs, n=n, q_seed=C4["seed"] if rank else None)[0]
+    idx = T.build_index(L["K"], L["V"], C4["C"], C4["iters"], group_size=G, seed=C4["seed"] + rank)
+    units = Hkv
+    q = L["q"]
+    lm = torch.empty((units, G, 2), dtype=torch.float64, device=dev)
+    ms_ = torch.empty((units, G, 1 + T.SHARD_GRID_T), dtype=torch.float64, device=dev)
+    op = torch.empty((units, G, 128), dtype=torch.float32, device=dev)
+    lp = torch.empty((units, G), dtype=torch.float32, device=dev)
+    o_all = torch.empty((world, units * G, 128), dtype=torch.float32, device=dev)
+    l_all = torch.empty((world, units * G), dtype=torch.float32, device=dev)
+    out = torch.empty((units * G, 128), dtype=torch.bfloat16, device=dev)
+
+    def compute_only():
+        T.decode_stage1(q, idx, lm)
+        T.decode_stage1b(idx, lm, ms_)
+        T.decode_stage2(q, idx, args.p, lm, ms_, op, lp)
+        T.lse_merge(op.view(1, units * G, 128), lp.view(1, units * G), out=out)
+
+    def collectives_only():
+        dist.all_reduce(lm, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ms_, op=dist.ReduceOp.SUM)
+        dist.all_gather_into_tensor(o_all, op.view(units * G, 128))
+        dist.all_gather_into_tensor(l_all, lp.view(units * G))
+
+    def step():
+        T.decode_stage1(q, idx, lm)
+        dist.all_reduce(lm, op=dist.ReduceOp.MAX)
+        T.decode_stage1b(idx, lm, ms_)
+        dist.all_reduce(ms_, op=dist.ReduceOp.SUM)
+        T.decode_stage2(q, idx, args.p, lm, ms_, op, lp)
+        dist.all_gather_into_tensor(o_all, op.view(units * G, 128))
+        dist.all_gather_into_tensor(l_all, lp.view(units * G))
+        T.lse_merge(o_all, l_all, out=out)
+
+    k = max(20, min(args.steps, 100))
+    how = "one CUDA graph per step (NCCL collectives captured)"
+    try:
+        step()
+        tm.barrier()
+        gs = capture(step)
+        step_fn = gs.replay
+    except Exception as e:  # noqa: BLE001  (capture of the collectives unsupported: eager)
+        torch.cuda.synchronize()
+        how = f"eager launches (graph capture failed: {type(e).__name__})"
+        step_fn = step
+    step_us = 1e3 * tm.timed([step_fn], k)
+    gc = capture(compute_only)
+    comp_us = 1e3 * tm.timed([gc.replay], k)
+    coll_us = 1e3 * tm.timed([collectives_only], k)
+    res = {"workload": f"C4: {world} x 131072-token context (1M at 8 GPUs) sequence-sharded, one shard (8 KV heads, "
+                       f"C = 1024) per GPU, p={args.p}; stage1 -> all_reduce MAX -> stage1b -> all_reduce SUM -> "
+                       "stage2 -> all_gather (o, lse) -> LSE merge",
+           "us_per_step": step_us, "compute_only_us": comp_us, "collectives_only_us": coll_us,
+           "timing": how + "; collectives alone: eager NCCL calls on the same buffers", "n_gpus": world,
+           "collective_bytes": {"all_reduce_max": lm.numel() * 8, "all_reduce_sum": ms_.numel() * 8,
+                                "all_gather": (o_all.numel() + l_all.numel()) * 4}}
     del L, idx
     torch.cuda.empty_cache()
     return res
@@ -295,25 +487,30 @@ def measure_c3(T, dev, p, steps, timed_loop):
 
 def run_gpu(args, rank, world, local_rank):
     import torch
-    import torch.distributed as dist
     from paper_2502_12216_b200 import build as B
+    from paper_2502_12216_b200.sharded import block_units, unit_block
     B.build()
     from paper_2502_12216_b200 import tactic as T
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     T.device_check()
     G, n, C = CFG["G"], CFG["n"], CFG["C"]
-    layers = make_layers([LAYERS * rank + l for l in range(LAYERS)], dev)
+    units_job = CFG["B"] * CFG["Hkv"]
+    u0, u1 = unit_block(units_job, world, rank)
+    pairs = block_units(units_job, CFG["Hkv"], world, rank)
+    layers = make_layers(list(range(LAYERS)), dev, pairs)
+    tm = Timer(dev, world)
 
     # ---- index build per layer (tcgen05 k-means + relayout), timed separately
     T.build_index(layers[0]["K"][:, :1, :8192].contiguous(), layers[0]["V"][:, :1, :8192].contiguous(), 64, 2,
                   group_size=G)  # warm
     torch.cuda.synchronize()
     build_ms, iters_run = [], []
-    for li, L in enumerate(layers):
+    for L in layers:
+        L["u0"] = u0
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        L["index"] = T.build_index(L["K"], L["V"], C, CFG["iters"], group_size=G, seed=LAYERS * rank + li)
+        L["index"] = T.build_index(L["K"], L["V"], C, CFG["iters"], group_size=G, seed=L["seed"], unit_offset=u0)
         e1.record()
         torch.cuda.synchronize()
         build_ms.append(e0.elapsed_time(e1))
@@ -321,101 +518,43 @@ def run_gpu(args, rank, world, local_rank):
         iters_run += ex["iters_run"].tolist()
         L["sizes"] = np.stack([np.bincount(ex["assign"][u], minlength=C) for u in range(L["index"].units)])
         L["out"] = torch.empty_like(L["q"])
+        if L["seed"] == 0:
+            L["export"] = ex
     units = layers[0]["index"].units
-    alg_tflop = 2.0 * n * C * 128 * sum(iters_run) / 1e12 / len(layers)   # per layer
+    sc = layers[0]["index"].sample_constants()
+    alg_tflop = 2.0 * n * C * 128 * sum(iters_run) / 1e12 / len(layers)   # per layer (this rank's units)
 
-    # cold L2 before every timed step: write a 256 MiB buffer (> 126 MB L2), then read a
-    # second one so the dirty lines of the write are written back before the step starts
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    flush_r = torch.ones(32 << 20, dtype=torch.int64, device=dev)
-    flush_acc = torch.empty((), dtype=torch.int64, device=dev)
-
-    def l2_flush():
-        flush.fill_(1)
-        torch.sum(flush_r, dim=0, out=flush_acc)
-
-    # ---- one CUDA graph per layer: one decode layer-step
-    for L in layers:
-        T.decode(L["q"], L["index"], args.p, out=L["out"])
-        torch.cuda.synchronize()
-        L["graph"] = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(L["graph"]):
-            T.decode(L["q"], L["index"], args.p, out=L["out"])
-    torch.cuda.synchronize()
-
-    def timed_loop(fns, steps, flush_each=True):
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-        for i, (a, b) in enumerate(evs):
-            if flush_each:
-                l2_flush()
-            a.record()
-            fns[i % len(fns)]()
-            b.record()
-        return evs
+    def model_graph(fn):
+        return capture(lambda: [fn(L) for L in layers])
 
     # ---- one step = one decode step through all LAYERS synthetic layers, captured as ONE
     # CUDA graph (as a serving engine captures its decode step); every layer's decode starts
     # only after the previous layer's has completed (the entry kernel takes no programmatic
     # dependency), each layer reads its own K/V (512 MB per layer > L2) and L2 is flushed
-    # before every step.  value = step time / LAYERS.
-    def model_graph(fn):
-        for L in layers:
-            fn(L)
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            for L in layers:
-                fn(L)
-        torch.cuda.synchronize()
-        return g
-
-    def per_layer_us(evs):
-        return 1e3 * float(np.mean([a.elapsed_time(b) for a, b in evs])) / len(layers)
-
+    # before every step.  value = max over ranks of the step time / LAYERS.
     gmodel = model_graph(lambda L: T.decode(L["q"], L["index"], args.p, out=L["out"]))
-    timed_loop([gmodel.replay], args.warmup)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    tm.loop([gmodel.replay], args.warmup)
+    tm.barrier()
     with ClockSampler(local_rank) as clk:
-        evs = timed_loop([gmodel.replay], args.steps)
+        evs = tm.loop([gmodel.replay], args.steps)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+        tm.barrier()
         # keep the GPU busy a little longer for the clock sampler (not part of the number)
-        timed_loop([gmodel.replay], min(args.steps, 100))
+        tm.loop([gmodel.replay], min(args.steps, 100))
         torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in evs]
-    ms = float(np.mean(step_ms)) / len(layers)   # per layer-step
-    ms_model_step = float(np.mean(step_ms))
+    ms_model_step = tm.max_over_ranks(float(np.mean(step_ms)))
+    ms = ms_model_step / len(layers)   # per layer-step (job: max over ranks)
+    step_p50 = float(np.median(step_ms)) / len(layers)
+    step_p99 = float(np.percentile(step_ms, 99)) / len(layers)
 
-    # the same layer-step as its own graph (one graph launch per layer, as in r01)
-    replays = [L["graph"].replay for L in layers]
-    timed_loop(replays, 2 * LAYERS)
-    torch.cuda.synchronize()
-    iso_ev = timed_loop(replays, max(4 * LAYERS, min(args.steps, 200)))
-    torch.cuda.synchronize()
-    iso_us = 1e3 * float(np.mean([a.elapsed_time(b) for a, b in iso_ev]))
-    if world > 1:
-        t = torch.tensor([ms_model_step], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_model_step = float(t.item())
-        ms = ms_model_step / len(layers)
+    # ---- in-graph phase timeline (S1-S3 / S4 / S5-S7 / S8-S9) of layer 0
+    phases = phase_timeline(T, layers[0], args, tm)
 
-    # ---- per-stage breakdown (selection / attention / merge), events between stages
-    st = []
-    for i in range(max(3 * LAYERS, min(args.steps, 200))):
-        L = layers[i % len(layers)]
-        l2_flush()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        T.decode_profiled(L["q"], L["index"], args.p, ev, out=L["out"])
-        st.append(ev)
-    torch.cuda.synchronize()
-    sel_us = 1e3 * float(np.mean([e[0].elapsed_time(e[1]) for e in st]))
-    att_us = 1e3 * float(np.mean([e[1].elapsed_time(e[2]) for e in st]))
-    mrg_us = 1e3 * float(np.mean([e[2].elapsed_time(e[3]) for e in st]))
+    # ---- the same layer-step as its own graph (one graph launch per layer, as in r01)
+    for L in layers:
+        L["graph"] = capture(lambda L=L: T.decode(L["q"], L["index"], args.p, out=L["out"]))
+    iso_us = 1e3 * tm.timed([L["graph"].replay for L in layers], max(4 * LAYERS, min(args.steps, 200)), 2 * LAYERS)
 
     # ---- the attention kernel's launch duration for the roofline: S8 + S9 alone over each
     # layer's work list (left by the decodes above), the 8 layers' launches back to back in
@@ -423,99 +562,49 @@ def run_gpu(args, rank, world, local_rank):
     for L in layers:
         T.decode(L["q"], L["index"], args.p, out=L["out"])
     gatt = model_graph(lambda L: T.decode_attention_only(L["q"], L["index"], L["out"]))
-    timed_loop([gatt.replay], 3)
-    torch.cuda.synchronize()
-    att_ev = timed_loop([gatt.replay], max(10, min(args.steps, 50)))
-    torch.cuda.synchronize()
-    att_launch_us = per_layer_us(att_ev)
+    att_launch_us = 1e3 * tm.timed([gatt.replay], max(10, min(args.steps, 50))) / len(layers)
 
     # ---- algorithmic bytes from the selections the GPU made (mean over layers)
     bms = []
     for L in layers:
         dbg = T.decode_debug(L["q"], L["index"], args.p)
         assert torch.equal(dbg["out"], L["out"]), "debug decode must reproduce the graph output"
-        bms.append(step_bytes(dbg, L["sizes"], G, n, C))
+        bms.append(step_bytes(dbg, L["sizes"], G, n, C, sc))
     bm = {k: float(np.mean([b[k] for b in bms])) for k in bms[0]}
     bm["union_frac_per_layer"] = [round(b["union_frac"], 5) for b in bms]
 
     # ---- dense baseline (own split-KV flash-decode over the caller's K/V), same layers
-    dgraphs = []
     for L in layers:
         L["dout"] = torch.empty_like(L["q"])
-        T.dense_decode(L["q"], L["K"], L["V"], out=L["dout"])
-        gd = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(gd):
-            T.dense_decode(L["q"], L["K"], L["V"], out=L["dout"])
-        dgraphs.append(gd.replay)
-    timed_loop(dgraphs, 3 * LAYERS)
-    torch.cuda.synchronize()
-    devs = timed_loop(dgraphs, max(2 * LAYERS, min(args.steps, 100)))
-    torch.cuda.synchronize()
-    dense_iso_ms = float(np.mean([a.elapsed_time(b) for a, b in devs]))
+    dgraphs = [capture(lambda L=L: T.dense_decode(L["q"], L["K"], L["V"], out=L["dout"])).replay for L in layers]
+    dense_iso_ms = tm.timed(dgraphs, max(2 * LAYERS, min(args.steps, 100)), 3 * LAYERS)
     gdm = model_graph(lambda L: T.dense_decode(L["q"], L["K"], L["V"], out=L["dout"]))
-    timed_loop([gdm.replay], 3)
-    torch.cuda.synchronize()
-    dev_m = timed_loop([gdm.replay], max(10, min(args.steps, 50)))
-    torch.cuda.synchronize()
-    dense_ms = per_layer_us(dev_m) * 1e-3
-    dense_bytes = 2 * units * n * 128 * 2 + 2 * units * G * 128 * 2
+    dense_ms = tm.timed([gdm.replay], max(10, min(args.steps, 50))) / len(layers)
+    dense_bytes = 2 * units_job * n * 128 * 2 + 2 * units_job * G * 128 * 2
 
-    # ---- e2e through the C ABI with host buffers (H2D q, D2H out inside the timed region)
+    # ---- e2e through the C ABI with host buffers: tactic_decode_host (pinned q in, the
+    # decode, out back, one synchronising call; the library replays its captured graph)
     for L in layers:
         L["q_host"] = L["q"].cpu().pin_memory()
         L["o_host"] = torch.empty_like(L["q_host"]).pin_memory()
         T.decode_host(L["q_host"], L["index"], args.p, L["o_host"])
+        assert torch.equal(L["o_host"], L["out"].cpu()), "host-buffer decode must reproduce the device decode"
     e2e = []
+    tm.barrier()
     for i in range(max(2 * LAYERS, min(args.steps, 200))):
         L = layers[i % len(layers)]
-        l2_flush()
+        tm.l2_flush()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         T.decode_host(L["q_host"], L["index"], args.p, L["o_host"])
         b.record()
         torch.cuda.synchronize()
         e2e.append(a.elapsed_time(b))
-    e2e_ms = float(np.mean(e2e))
-    if world > 1:
-        t = torch.tensor([e2e_ms, dense_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms, dense_ms = float(t[0]), float(t[1])
-    qd = layers[0]["q"]
-    index = layers[0]["index"]
+    e2e_ms = tm.max_over_ranks(float(np.mean(e2e)))
     build_ms = float(np.mean(build_ms))
-    c3 = measure_c3(T, dev, args.p, args.steps, timed_loop) if (args.c3 and world == 1) else None
 
-    # ---- C4 (BASELINE.json configs[3]: 1M tokens sequence-sharded over 8 GPUs): on this
-    # single GPU, one shard's compute per decode step (a C2-shaped shard: 131072 tokens x
-    # 8 KV heads, C = 1024) through the three sharded stages + the final LSE merge, with the
-    # three collectives (MAX all-reduce, SUM all-reduce, all-gather) absent (world size 1)
-    c4 = None
-    if args.c4 and world == 1:
-        L = layers[0]
-        lm = torch.empty((units, G, 2), dtype=torch.float64, device=dev)
-        ms_ = torch.empty((units, G, 1 + T.SHARD_GRID_T), dtype=torch.float64, device=dev)
-        op = torch.empty((units, G, 128), dtype=torch.float32, device=dev)
-        lp = torch.empty((units, G), dtype=torch.float32, device=dev)
-        mo = torch.empty((units * G, 128), dtype=torch.bfloat16, device=dev)
-
-        def shard_step():
-            T.decode_stage1(L["q"], L["index"], lm)
-            T.decode_stage1b(L["index"], lm, ms_)
-            T.decode_stage2(L["q"], L["index"], args.p, lm, ms_, op, lp)
-            T.lse_merge(op.view(1, units * G, 128), lp.view(1, units * G), out=mo)
-
-        shard_step()
-        gs = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(gs):
-            shard_step()
-        timed_loop([gs.replay], 5)
-        torch.cuda.synchronize()
-        ev = timed_loop([gs.replay], max(20, min(args.steps, 100)))
-        torch.cuda.synchronize()
-        c4 = {"workload": "C4 shard: 131072 tokens x 8 KV heads (one of 8 shards of a 1M-token context), C = 1024, "
-                          f"p={args.p}; stage1 + stage1b + stage2 + LSE merge on 1 GPU, collectives not included",
-              "us_per_shard_step": 1e3 * float(np.mean([a.elapsed_time(b) for a, b in ev])),
-              "dense_us_per_shard_step": dense_ms * 1e3}
+    c3 = measure_c3(T, dev, args, rank, world, tm) if args.c3 else None
+    c4 = measure_c4(T, dev, args, rank, world, tm) if args.c4 else None
 
     # ---- Table-1 diagnostics (NEXT 3) over the same layers: Optimal /
     # Cluster-Optimal / Tactic budgets, achieved cumulative score and success rate
@@ -548,35 +637,27 @@ def run_gpu(args, rank, world, local_rank):
             for u in range(units):
                 uni_tok.append(int(L["sizes"][u][dbg["union_mask"][u].astype(bool)].sum()))
                 own_tok.append(sum(int(L["sizes"][u][dbg["order"][u, g][:dbg["J"][u, g]]].sum()) for g in range(G)))
-        timed_loop([gph.replay], 3)
-        torch.cuda.synchronize()
-        ev = timed_loop([gph.replay], max(10, min(args.steps, 50)))
-        torch.cuda.synchronize()
-        ph_us = per_layer_us(ev)
+        ph_us = 1e3 * tm.timed([gph.replay], max(10, min(args.steps, 50))) / len(layers)
         ablation = {"per_head_us_per_layer_step": ph_us, "union_us_per_layer_step": ms * 1e3,
                     "union_speedup": ph_us / (ms * 1e3),
                     "kv_tokens_per_head_loading": float(np.sum(own_tok)) / len(layers),
                     "kv_tokens_union": float(np.sum(uni_tok)) / len(layers),
                     "paper": "union up to 1.65x faster than per-head loading (P:695)"}
 
-    # ---- target-fraction sweep (BASELINE.json configs[4], C5): same layers, graph per (p,
-    # layer), device-timed like the headline, plus the union fraction the GPU selected
+    # ---- target-fraction sweep (BASELINE.json configs[4], C5): same layers, device-timed
+    # like the headline, plus the union fraction the GPU selected
     sweep = []
     if args.sweep and world == 1:
         for p in (0.5, 0.8, 0.9, 0.95, 0.99, 1.0):
             for L in layers:
                 L["o_sw"] = torch.empty_like(L["q"])
             gp = model_graph(lambda L: T.decode(L["q"], L["index"], p, out=L["o_sw"]))
-            timed_loop([gp.replay], 3)
-            torch.cuda.synchronize()
-            ev = timed_loop([gp.replay], max(10, min(args.steps, 50)))
-            torch.cuda.synchronize()
-            us = per_layer_us(ev)
+            us = 1e3 * tm.timed([gp.replay], max(10, min(args.steps, 50))) / len(layers)
             del gp
             uf = []
             for L in layers:
                 if p >= 1.0:
-                    uf.append(float((L["sizes"] > 0).sum() and 1.0))
+                    uf.append(1.0)
                 else:
                     dbg = T.decode_debug(L["q"], L["index"], p)
                     uf.append(sum(int(L["sizes"][u][dbg["union_mask"][u].astype(bool)].sum())
@@ -588,9 +669,9 @@ def run_gpu(args, rank, world, local_rank):
         return
     peaks = _peaks()
     hbm = peaks.get("hbm_gbs", 6650.0)
-    peak_src = "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING)"
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING)"
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    attn_bytes = bm["union_kv"] + bm["q_out"] // 2 + (n_sm + index.units) * G * 129 * 4   # K/V, q, partials
+    attn_bytes = bm["union_kv"] + bm["q_out"] // 2 + (n_sm + units) * G * 129 * 4   # K/V, q, partials
     att_gbs = attn_bytes / (att_launch_us * 1e-6) / 1e9
     traffic = None
     try:
@@ -598,45 +679,79 @@ def run_gpu(args, rank, world, local_rank):
         traffic = tr.get("attention_kernel_sparse_bytes_per_launch")
     except Exception:
         pass
-    value_us = ms * 1e3 / world
+    import torch.cuda.nccl as tnccl
     line = {
-        "metric": METRIC, "value": value_us, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_model_step, "higher_is_better": False, "scaling": "weak",
+        "metric": METRIC, "value": ms * 1e3, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_model_step, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": _config(args, world),
-        # per decode step: score+rank, sample, fit, attention
+        # per decode layer-step: score_rank, sample, fit, attention (p < 1); 1 attention at p >= 1
         "gpu_launches": (1 if args.p >= 1 else 4) * LAYERS * args.steps,
-        "roofline": {"bound": "hbm", "kernel": "attention_kernel<4,false> (S8 sparse split-KV)",
+        "p50_us": step_p50 * 1e3, "p99_us": step_p99 * 1e3,
+        "roofline": {"bound": "hbm", "kernel": "attention_kernel<4,false> (S8 sparse split-KV + fused S9)",
                      "achieved": att_gbs, "peak": hbm, "unit": "GB/s", "frac": att_gbs / hbm,
                      "traffic": traffic, "peak_source": peak_src,
                      "bytes_per_launch": attn_bytes, "us_per_launch": att_launch_us,
                      "timing": "S8+S9 alone, 8 layers' launches back to back in one graph (no PDL), cold L2 "
-                               "per replay, CUDA events; mean per launch",
-                     "us_per_launch_event_bracketed_in_step": att_us},
+                               "per replay, CUDA events; mean per launch (rank 0's units)"},
         "step_roofline": {"bytes_per_step": bm["total"], "achieved_gbs": bm["total"] / (ms * 1e-3) / 1e9,
                           "frac": bm["total"] / (ms * 1e-3) / 1e9 / hbm, "bytes": bm},
-        "stages_us": {"selection_S1_S7": sel_us, "attention_S8": att_us, "merge_S9": mrg_us},
-        "dense": {"us_per_layer_step": dense_ms * 1e3, "gbs": dense_bytes / (dense_ms * 1e-3) / 1e9,
-                  "frac": dense_bytes / (dense_ms * 1e-3) / 1e9 / hbm, "bytes": dense_bytes},
+        "phases_us": phases,
+        "dense": {"us_per_layer_step": dense_ms * 1e3, "gbs_job": dense_bytes / (dense_ms * 1e-3) / 1e9,
+                  "frac": dense_bytes / (dense_ms * 1e-3) / 1e9 / hbm / world, "bytes_job": dense_bytes},
         "speedup_vs_dense": dense_ms / ms,
         "isolated_layer_graph": {"us_per_layer_step": iso_us, "dense_us_per_layer_step": dense_iso_ms * 1e3,
                                  "speedup_vs_dense": dense_iso_ms * 1e3 / iso_us,
                                  "what": "each layer-step as its own CUDA graph, L2 flushed before each (includes one graph launch per layer)"},
         "p_sweep": sweep or None,
         "c3": c3,
-        "c4_shard": c4,
+        "c4": c4,
         "table1": table1,
         "gqa_union_ablation": ablation,
-        "build": {"ms": build_ms, "iters_run": iters_run, "alg_tflop": alg_tflop,
+        "build": {"ms": build_ms, "units_per_gpu": units, "iters_run": iters_run, "alg_tflop": alg_tflop,
                   "alg_tflops": alg_tflop / (build_ms * 1e-3),
                   "exec_tflops_split_bf16": 2 * alg_tflop / (build_ms * 1e-3)},
-        "e2e": {"value": e2e_ms * 1e3 / world, "unit": UNIT, "h2d_bytes_per_step": int(qd.numel() * 2),
-                "d2h_bytes_per_step": int(qd.numel() * 2)},
+        "e2e": {"value": e2e_ms * 1e3, "unit": UNIT, "h2d_bytes_per_step": int(layers[0]["q"].numel() * 2),
+                "d2h_bytes_per_step": int(layers[0]["q"].numel() * 2),
+                "how": "tactic_decode_host per layer-step (pinned q in, decode, out back; the library replays its "
+                       "captured graph), CUDA events around each synchronising call, cold L2; max over ranks"},
+        "nccl": {"backend": "nccl", "world": world, "version": ".".join(map(str, tnccl.version()))
+                 if hasattr(tnccl, "version") else None},
         "clocks": clk.summary(),
         "context": PAPER_CONTEXT,
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args)
+        from synth import make_unit
+        u = make_unit(n, G, seed=0, b=0, h=0)
+        ex = layers[0]["export"]
+        line["cpu_baseline"] = cpu_baseline(args, u["K"], u["V"], u["q"], ex["centroids"][0], ex["assign"][0])
     print(json.dumps(line), flush=True)
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _self_launch(args):
+    """`bench.py --gpus N` outside torchrun: re-run under torch.distributed.run, one rank per
+    GPU of this node; fails loudly when fewer than N GPUs are visible."""
+    import subprocess
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible CUDA devices, found {have}\n")
+        sys.exit(2)
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # communicator lines (NVLS, rings) on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd, env=env))
 
 
 def main():
@@ -650,26 +765,38 @@ def main():
     ap.add_argument("--sweep", type=int, default=1, help="1: add the C5 target-fraction sweep (p_sweep)")
     ap.add_argument("--c3", type=int, default=1, help="1: add the C3 batch-64 32K measurement (configs[2])")
     ap.add_argument("--table1", type=int, default=1, help="1: add the Table-1 diagnostics (budgets, success)")
-    ap.add_argument("--c4", type=int, default=1, help="1: add the C4 per-shard sequence-sharded measurement")
+    ap.add_argument("--c4", type=int, default=1, help="1: add the C4 sequence-sharded step with its collectives")
     ap.add_argument("--ablation", type=int, default=1, help="1: add the GQA union vs per-head loading ablation")
     args = ap.parse_args()
+    if args.warmup < 3:
+        sys.stderr.write("bench.py: --warmup must be >= 3\n")
+        sys.exit(2)
+    in_torchrun = "WORLD_SIZE" in os.environ
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
+    if not in_torchrun and args.gpus > 1:
+        _self_launch(args)
+        return
+    if in_torchrun and world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE\n")
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    # one NCCL process group at every world size (world 1 included): barriers, the
+    # max-over-ranks reduction of the timings, and the C4 step's collectives
+    if in_torchrun:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", local_rank))
     try:
         run_gpu(args, rank, world, local_rank)
     finally:
-        if world > 1:
-            import torch.distributed as dist
-            dist.destroy_process_group()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -87,6 +87,10 @@ typedef struct {
    * else every rank is exact (tiny n).  Fixed at build / import; see
    * tactic_sample_constants.  Out of range: TACTIC_ERR_INVALID_ARGUMENT.               */
   float exact_frac, p1, p2, window_half_frac;
+  /* global number of this index's unit 0 for the init sampler's seeding (default 0): a
+   * rank that holds units [u0, u1) of a batch x KV-head sharded layer passes u0 and draws
+   * the same initial centroids as a single index over all units would. */
+  int32_t unit_offset;
 } tactic_params_t;
 
 /* The integer constants of Alg. 1's sampling for sequence length n (see tactic_params_t):
@@ -179,7 +183,11 @@ tactic_status_t tactic_decode_ex(const void* q, tactic_index_t idx, float p, voi
                                  float* lse, void* stream);
 
 /* Same computation through HOST buffers: q_host bf16 [B][Hq][128] is copied in, out_host
- * bf16 [B][Hq][128] copied back; synchronises the stream (end-to-end user call).      */
+ * bf16 [B][Hq][128] copied back; synchronises the stream (end-to-end user call).  The
+ * copy-in, the decode and the copy-out are captured once as one CUDA graph per (q_host,
+ * out_host, p, tail length, options) and replayed by later calls with the same key (one
+ * launch per call); use page-locked host buffers -- with pageable ones the capture is
+ * refused and the call falls back to stream-ordered copies and launches.             */
 tactic_status_t tactic_decode_host(const void* q_host, tactic_index_t idx, float p,
                                    void* out_host, void* stream);
 

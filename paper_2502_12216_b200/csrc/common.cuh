@@ -266,6 +266,11 @@ __device__ __forceinline__ void st_async_v2u64(uint32_t addr, unsigned long long
                "l"(a), "l"(b), "r"(bar)
                : "memory");
 }
+__device__ __forceinline__ void st_async_u64(uint32_t addr, unsigned long long a, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr), "l"(a),
+               "r"(bar)
+               : "memory");
+}
 __device__ __forceinline__ void st_dsmem_u64(uint32_t addr, unsigned long long v) {
   asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
 }

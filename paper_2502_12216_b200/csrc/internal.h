@@ -118,6 +118,16 @@ struct tactic_index_s {
   __nv_bfloat16* o_stage = nullptr;
   long long device_bytes = 0;
   bool lists_valid = false;      // a p < 1 selection has been enqueued (attention-only needs its lists)
+  // tactic_decode_host: the H2D copy, the decode and the D2H copy captured as one CUDA graph,
+  // re-captured when its key (host buffers, p, tail length, options) changes
+  cudaGraphExec_t hg_exec = nullptr;
+  cudaStream_t hg_stream = nullptr;
+  const void* hg_q = nullptr;
+  void* hg_o = nullptr;
+  float hg_p = 0.f;
+  int hg_tail = -1;
+  uint32_t hg_opts = 0;
+  bool hg_failed = false;        // capture not possible for this key (e.g. pageable host memory)
   unsigned long long* tlog = nullptr;  // [units][16][8] phase timestamps (TACTIC_TLOG=1)
 };
 

@@ -7,12 +7,14 @@
 //       summation order differs from the oracle).  The CTA's centroid slice is index data,
 //       so it is bulk-copied (1-D TMA) into shared memory before the grid-dependency wait.
 //       A warp scores 32 centroids with a shuffle butterfly reduce-scatter.
-//   S2  local bitonic sort of the M (key, id) pairs (register shuffles for partners < 32
-//       apart, double-buffered shared memory above).  Key = the order-preserving bits of
-//       -crit (all 64), compared lexicographically with the cluster id, so the order is
-//       exactly (-crit, id).  The exclusive prefix of the sorted sizes is
-//       scanned, and the sorted run (key, id | size prefix) is pushed into every CTA of the
-//       cluster (DSMEM stores), one cluster barrier.
+//   S2  local bitonic sort of the M keys (register shuffles for partners < 32 apart,
+//       double-buffered shared memory above).  Key = order-preserving bits of -crit with
+//       the low 12 bits replaced by the cluster id, so one 64-bit compare orders by
+//       (-crit, id) (DESIGN reading 24: criticalities that agree in their leading 40
+//       mantissa bits -- 1e-12 relative, far below the fp64 summation-order differences
+//       between any two implementations of q . c -- rank by cluster id).  The
+//       exclusive prefix of the sorted sizes is scanned, and the sorted run (keys, size
+//       prefix) is pushed into every CTA of the cluster (DSMEM stores), one cluster barrier.
 //       The global rank of a cluster is its local position plus its lower bound in the
 //       other R-1 runs; its end rank e_r is its own inclusive prefix plus the other runs'
 //       prefixes at those bounds -- no scatter and no second barrier.
@@ -42,32 +44,25 @@ struct SRParams {
   unsigned long long* tlog;
 };
 
-__device__ __forceinline__ unsigned long long crit_key(double crit) {
+__device__ __forceinline__ unsigned long long crit_key(double crit, int id) {
   if (crit == 0.0) crit = 0.0;  // -0 == +0
   const unsigned long long b = (unsigned long long)__double_as_longlong(-crit);
-  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // ascending = descending crit
-}
-// (key, id) < (key', id') lexicographically; padding entries are (~0, INT_MAX)
-__device__ __forceinline__ bool kid_less(unsigned long long k, int i, unsigned long long k2, int i2) {
-  return k < k2 || (k == k2 && i < i2);
+  const unsigned long long k = (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // ascending = descending crit
+  return (k & ~0xFFFull) | (unsigned long long)id;
 }
 
-// one entry of a pushed run: sorted key, cluster id (high 32 bits of `pi`) and exclusive
-// size prefix (low 32 bits); entry M: (~0, INT_MAX | total)
+// one entry of a pushed run: sorted key and exclusive size prefix (entry M: ~0, total)
 struct __align__(16) RunEnt {
   unsigned long long key;
-  unsigned long long pi;
+  unsigned long long pre;
 };
-__device__ __forceinline__ int run_id(const RunEnt& e) { return (int)(e.pi >> 32); }
-__device__ __forceinline__ int run_pre(const RunEnt& e) { return (int)(uint32_t)e.pi; }
 
 // PS (prescored): S1 ran in score_kernel (select.cu: one read of a unit's centroids for all
 // G heads, the same products and butterfly tree: bit-identical crit); this kernel loads crit and holds no centroid slice, so more
 // clusters fit per SM.  Used when the launch spans several waves (batch 64, C3).
 template <int M, int R, bool PS>
 constexpr size_t sr_smem() {
-  return (PS ? 0 : (size_t)M * 512) + (size_t)R * (M + 1) * sizeof(RunEnt) + 2 * (size_t)M * 8 + 2 * (size_t)M * 4 +
-         2 * (size_t)M * 4 + 64;
+  return (PS ? 0 : (size_t)M * 512) + (size_t)R * (M + 1) * sizeof(RunEnt) + 2 * (size_t)M * 8 + 2 * (size_t)M * 4 + 64;
 }
 
 template <int M, int R, bool PS>
@@ -79,9 +74,8 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
   extern __shared__ __align__(128) uint8_t sm[];
   float* s_cent = (float*)sm;                                // [M][128] (not PS)
   RunEnt* runs = (RunEnt*)(sm + (PS ? 0 : M * 512));          // [R][M+1]
-  unsigned long long* bk = (unsigned long long*)(runs + R * (M + 1));  // [2][M] keys
-  int* bi = (int*)(bk + 2 * M);                               // [2][M] ids
-  int* s_size = bi + 2 * M;                                   // [M]
+  unsigned long long* bk = (unsigned long long*)(runs + R * (M + 1));  // [2][M]
+  int* s_size = (int*)(bk + 2 * M);                           // [M]
   int* s_row = s_size + M;                                    // [M]
   __shared__ uint64_t bar, rbar;
   __shared__ int red[NW];
@@ -167,39 +161,30 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
   }
   pstamp(1);
 
-  // ---- S2: local bitonic sort (ascending (key, id) = descending crit, then id)
-  unsigned long long x = valid ? crit_key(crit) : ~0ull;
-  int xid = valid ? j : INT_MAX;
+  // ---- S2: local bitonic sort (ascending packed keys = descending crit, then id)
+  unsigned long long x = valid ? crit_key(crit, j) : ~0ull;
   int buf = 0;
 #pragma unroll
   for (int k = 2; k <= M; k <<= 1) {
 #pragma unroll
     for (int d = k >> 1; d > 0; d >>= 1) {
       unsigned long long o;
-      int oid;
       if (d < 32) {
         o = __shfl_xor_sync(0xffffffffu, x, d);
-        oid = __shfl_xor_sync(0xffffffffu, xid, d);
       } else {
         bk[buf * M + tid] = x;
-        bi[buf * M + tid] = xid;
         __syncthreads();
         o = bk[buf * M + (tid ^ d)];
-        oid = bi[buf * M + (tid ^ d)];
         buf ^= 1;
       }
       const bool take_min = ((tid & d) == 0) == ((tid & k) == 0);
-      const bool o_less = kid_less(o, oid, x, xid);
-      if (take_min == o_less) {
-        x = o;
-        xid = oid;
-      }
+      x = take_min ? (o < x ? o : x) : (o > x ? o : x);
     }
   }
   pstamp(2);
   // exclusive prefix of the sorted sizes
-  const bool real = xid != INT_MAX;
-  const int id = real ? xid : 0;
+  const bool real = x != ~0ull;
+  const int id = real ? (int)(x & 0xFFFull) : 0;
   const int size = real ? s_size[id - c * M] : 0;
   int incl = size;
 #pragma unroll
@@ -222,11 +207,8 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
 #pragma unroll
   for (int cc = 0; cc < R; ++cc) {
     const uint32_t rb = dsmem_addr(&rbar, (uint32_t)cc);
-    st_async_v2u64(dsmem_addr(runs + c * (M + 1) + tid, (uint32_t)cc), x,
-                   ((unsigned long long)(uint32_t)xid << 32) | (uint32_t)pre, rb);
-    if (tid == M - 1)
-      st_async_v2u64(dsmem_addr(runs + c * (M + 1) + M, (uint32_t)cc), ~0ull,
-                     ((unsigned long long)(uint32_t)INT_MAX << 32) | (uint32_t)tot, rb);
+    st_async_v2u64(dsmem_addr(runs + c * (M + 1) + tid, (uint32_t)cc), x, (unsigned long long)pre, rb);
+    if (tid == M - 1) st_async_v2u64(dsmem_addr(runs + c * (M + 1) + M, (uint32_t)cc), ~0ull, (unsigned long long)tot, rb);
   }
   const size_t ug = (size_t)u * P.G + g;
   if (!PS && valid) P.crit[ug * C + j] = crit;
@@ -244,18 +226,15 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
     for (int len = M; len > 1;) {
       const int half = len >> 1;
 #pragma unroll
-      for (int cc = 0; cc < R; ++cc) {
-        const RunEnt e = runs[cc * (M + 1) + base[cc] + half - 1];
-        base[cc] = kid_less(e.key, run_id(e), x, xid) ? base[cc] + half : base[cc];
-      }
+      for (int cc = 0; cc < R; ++cc)
+        base[cc] = runs[cc * (M + 1) + base[cc] + half - 1].key < x ? base[cc] + half : base[cc];
       len -= half;
     }
 #pragma unroll
     for (int cc = 0; cc < R; ++cc) {
-      const RunEnt e = runs[cc * (M + 1) + base[cc]];
-      const int lb = base[cc] + (kid_less(e.key, run_id(e), x, xid) ? 1 : 0);
+      const int lb = base[cc] + (runs[cc * (M + 1) + base[cc]].key < x ? 1 : 0);
       r += lb;
-      end += run_pre(runs[cc * (M + 1) + lb]);
+      end += (int)runs[cc * (M + 1) + lb].pre;
     }
   }
   pstamp(5);

@@ -189,6 +189,8 @@ struct tactic_index_priv {
 };
 
 static void free_index(tactic_index_s* x, std::vector<void*>* ptrs) {
+  if (x->hg_exec) cudaGraphExecDestroy(x->hg_exec);
+  if (x->hg_stream) cudaStreamDestroy(x->hg_stream);
   if (ptrs)
     for (void* p : *ptrs) cudaFree(p);
   delete x;
@@ -339,6 +341,7 @@ static tactic_status_t build_common(const void* K, const void* V, const tactic_k
   if (C < 1 || C > r.n) return fail(TACTIC_ERR_INVALID_ARGUMENT, "n_clusters must be in [1, seq_len] (got %d)", C);
   if (C > TACTIC_MAX_CLUSTERS) return fail(TACTIC_ERR_UNSUPPORTED, "n_clusters %d > TACTIC_MAX_CLUSTERS", C);
   if (iters < 1) return fail(TACTIC_ERR_INVALID_ARGUMENT, "iters must be >= 1");
+  if (params && params->unit_offset < 0) return fail(TACTIC_ERR_INVALID_ARGUMENT, "unit_offset < 0");
   if ((uintptr_t)K % 16 || (uintptr_t)V % 16) return fail(TACTIC_ERR_SHAPE, "K and V must be 16-byte aligned");
   if ((st = check_device())) return st;
   tactic_params_t P = {};
@@ -435,7 +438,7 @@ static tactic_status_t build_common(const void* K, const void* V, const tactic_k
           init[(size_t)u * C + j] = t;
         }
       } else {
-        sample_init(r.n, C, P.seed, u, &init[(size_t)u * C]);
+        sample_init(r.n, C, P.seed, P.unit_offset + u, &init[(size_t)u * C]);
       }
     }
     CKB(cudaMemcpyAsync(d_init, init.data(), init.size() * 4, cudaMemcpyHostToDevice, s));
@@ -760,14 +763,53 @@ tactic_status_t tactic_decode(const void* q, tactic_index_t idx, float p, void* 
   return tactic_decode_ex(q, idx, p, out, nullptr, stream);
 }
 
-tactic_status_t tactic_decode_host(const void* q_host, tactic_index_t idx, float p, void* out_host, void* stream) {
-  if (!q_host || !idx || !out_host) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
-  cudaStream_t s = (cudaStream_t)stream;
+// H2D q -> decode -> D2H out, enqueued on s (the body of the host-buffer call)
+static tactic_status_t decode_host_body(const void* q_host, tactic_index_t idx, float p, void* out_host,
+                                        cudaStream_t s) {
   const size_t bytes = (size_t)idx->units * idx->G * 128 * 2;
   CK(cudaMemcpyAsync(idx->q_stage, q_host, bytes, cudaMemcpyHostToDevice, s));
-  tactic_status_t st = tactic_decode_ex(idx->q_stage, idx, p, idx->o_stage, nullptr, stream);
+  tactic_status_t st = tactic_decode_ex(idx->q_stage, idx, p, idx->o_stage, nullptr, s);
   if (st) return st;
   CK(cudaMemcpyAsync(out_host, idx->o_stage, bytes, cudaMemcpyDeviceToHost, s));
+  return TACTIC_OK;
+}
+
+tactic_status_t tactic_decode_host(const void* q_host, tactic_index_t idx, float p, void* out_host, void* stream) {
+  if (!q_host || !idx || !out_host) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  tactic_status_t st = check_p(p);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool same = idx->hg_q == q_host && idx->hg_o == out_host && idx->hg_p == p && idx->hg_tail == idx->tail_len &&
+                    idx->hg_opts == idx->options;
+  if (!same) {  // (re)capture the whole call as one graph: one launch per call afterwards
+    if (idx->hg_exec) cudaGraphExecDestroy(idx->hg_exec);
+    idx->hg_exec = nullptr;
+    idx->hg_q = q_host;
+    idx->hg_o = out_host;
+    idx->hg_p = p;
+    idx->hg_tail = idx->tail_len;
+    idx->hg_opts = idx->options;
+    idx->hg_failed = false;
+    if (!idx->hg_stream) CK(cudaStreamCreateWithFlags(&idx->hg_stream, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(idx->hg_stream, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      st = decode_host_body(q_host, idx, p, out_host, idx->hg_stream);
+      e = cudaStreamEndCapture(idx->hg_stream, &g);
+      if (st == TACTIC_OK && e == cudaSuccess && g) e = cudaGraphInstantiate(&idx->hg_exec, g, 0);
+      if (g) cudaGraphDestroy(g);
+    }
+    if (st != TACTIC_OK || e != cudaSuccess || !idx->hg_exec) {  // e.g. pageable host buffers
+      cudaGetLastError();
+      idx->hg_exec = nullptr;
+      idx->hg_failed = true;
+    }
+  }
+  if (idx->hg_exec) {
+    CK(cudaGraphLaunch(idx->hg_exec, s));
+  } else if ((st = decode_host_body(q_host, idx, p, out_host, s))) {
+    return st;
+  }
   CK(cudaStreamSynchronize(s));
   return TACTIC_OK;
 }

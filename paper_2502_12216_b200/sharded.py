@@ -18,10 +18,28 @@ the libtactic stage entry points.
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import Callable, Optional
+from typing import Callable, List, Optional, Tuple
 
 import torch
 import torch.distributed as dist
+
+
+def unit_block(units: int, world: int, rank: int) -> Tuple[int, int]:
+    """Batch x KV-head mode (the paper's sub-requests, across GPUs):
+    rank `rank` of `world` owns the contiguous unit range [start, stop) of the units
+    u = b * Hkv + h (batch-major); the first units % world ranks take one extra unit.
+    No collective touches the data path: each rank builds and decodes its own units."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("need 0 <= rank < world")
+    base, extra = divmod(units, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def block_units(units: int, Hkv: int, world: int, rank: int) -> List[Tuple[int, int]]:
+    """The (b, h) pairs of rank's unit block."""
+    start, stop = unit_block(units, world, rank)
+    return [divmod(u, Hkv) for u in range(start, stop)]
 
 
 @dataclass

@@ -40,7 +40,7 @@ class KvDesc(ctypes.Structure):
 class Params(ctypes.Structure):
     _fields_ = [("seed", ctypes.c_uint64), ("init_indices", ctypes.c_void_p), ("flags", ctypes.c_uint32),
                 ("num_ctas", ctypes.c_int32), ("exact_frac", ctypes.c_float), ("p1", ctypes.c_float),
-                ("p2", ctypes.c_float), ("window_half_frac", ctypes.c_float)]
+                ("p2", ctypes.c_float), ("window_half_frac", ctypes.c_float), ("unit_offset", ctypes.c_int32)]
 
 
 class SampleConstants(ctypes.Structure):
@@ -51,13 +51,14 @@ class SampleConstants(ctypes.Structure):
 SAMPLING_KEYS = ("exact_frac", "p1", "p2", "window_half_frac")
 
 
-def _params(seed=0, init=None, flags=0, num_ctas=0, sampling=None) -> Params:
+def _params(seed=0, init=None, flags=0, num_ctas=0, sampling=None, unit_offset=0) -> Params:
     """tactic_params_t; sampling: optional dict of the Alg. 1 fractions (0 / absent = default)."""
     sampling = dict(sampling or {})
     bad = set(sampling) - set(SAMPLING_KEYS)
     if bad:
         raise ValueError(f"unknown sampling keys {sorted(bad)}")
-    return Params(seed, init, flags, num_ctas, *[float(sampling.get(k, 0.0)) for k in SAMPLING_KEYS])
+    return Params(seed, init, flags, num_ctas, *[float(sampling.get(k, 0.0)) for k in SAMPLING_KEYS],
+                  int(unit_offset))
 
 
 class IndexInfo(ctypes.Structure):
@@ -234,7 +235,7 @@ class Index:
 
 def build_index(K: torch.Tensor, V: torch.Tensor, n_clusters: int, iters: int = 10, *, group_size: int = 4,
                 seed: int = 0, init: Optional[np.ndarray] = None, flags: int = 0, num_ctas: int = 0,
-                sampling: Optional[dict] = None, stream=None) -> Index:
+                sampling: Optional[dict] = None, unit_offset: int = 0, stream=None) -> Index:
     """tactic_build_index: k-means (tcgen05 assignment) + cluster-contiguous KV layout."""
     kv = _kv_desc(K, group_size)
     if tuple(V.shape) != tuple(K.shape) or V.stride() != K.stride() or V.dtype != K.dtype:
@@ -244,7 +245,7 @@ def build_index(K: torch.Tensor, V: torch.Tensor, n_clusters: int, iters: int = 
         init_arr = np.ascontiguousarray(init, dtype=np.int32)
         if init_arr.shape != (kv.batch * kv.num_kv_heads, n_clusters):
             raise ValueError("init must be [units, n_clusters]")
-    p = _params(seed, init_arr.ctypes.data if init_arr is not None else None, flags, num_ctas, sampling)
+    p = _params(seed, init_arr.ctypes.data if init_arr is not None else None, flags, num_ctas, sampling, unit_offset)
     h = ctypes.c_void_p()
     _check(lib().tactic_build_index(_ptr(K), _ptr(V), ctypes.byref(kv), n_clusters, iters, ctypes.byref(p),
                                     _stream(stream), ctypes.byref(h)))

@@ -125,3 +125,55 @@ def test_max_over_ranks_timing_reduction():
     for pr in procs:
         pr.join(timeout=60)
     assert vals == [2.5, 2.5]
+
+
+def _block_worker(rank, port, units, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        from paper_2502_12216_b200.sharded import block_units, unit_block
+        lo, hi = unit_block(units, 2, rank)
+        t = torch.tensor([lo, hi], dtype=torch.int64)
+        got = [torch.zeros(2, dtype=torch.int64) for _ in range(2)]
+        dist.all_gather(got, t)
+        # every rank's step time, then the job time = max over ranks (bench.py)
+        tm = torch.tensor([float(hi - lo)], dtype=torch.float64)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        out_q.put((rank, [g.tolist() for g in got], float(tm), block_units(units, 8, 2, rank)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("units", [8, 512, 7, 1])
+def test_unit_partition_world2_gloo(units):
+    """bench.py's batch x KV-head sharding: the two ranks' unit blocks are
+    contiguous, disjoint and cover [0, units) batch-major; balanced to within one unit."""
+    ctx = mp.get_context("spawn")
+    q_ = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_block_worker, args=(r, port, units, q_)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict((r, (b, t, bu)) for r, b, t, bu in (q_.get(timeout=120) for _ in range(2)))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    blocks = res[0][0]
+    assert blocks == res[1][0]
+    assert blocks[0][0] == 0 and blocks[0][1] == blocks[1][0] and blocks[1][1] == units
+    sizes = [hi - lo for lo, hi in blocks]
+    assert max(sizes) - min(sizes) <= 1
+    assert res[0][1] == res[1][1] == float(max(sizes))
+    pairs = res[0][2] + res[1][2]
+    assert pairs == [divmod(u, 8) for u in range(units)]
+
+
+def test_unit_block_all_worlds():
+    from paper_2502_12216_b200.sharded import unit_block
+    for units in (1, 7, 8, 512):
+        for world in (1, 2, 3, 4, 8):
+            blocks = [unit_block(units, world, r) for r in range(world)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == units
+            assert all(blocks[i][1] == blocks[i + 1][0] for i in range(world - 1))
+            assert max(b - a for a, b in blocks) - min(b - a for a, b in blocks) <= 1
