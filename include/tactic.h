@@ -103,8 +103,9 @@ typedef struct {
 typedef struct {
   int32_t units, batch, num_kv_heads, group_size, seq_len, n_clusters;
   int32_t iters_requested;
-  int32_t select_cluster_size;  /* always 0 (the retired single-kernel selection); kept for
-                                   ABI stability                                         */
+  int32_t select_cluster_size;  /* CTAs per thread-block cluster of the one-launch decode
+                                   (TACTIC_OPT_CLUSTER_DECODE, see tactic_decode); 0 = this
+                                   index decodes through the multi-kernel chain          */
   int64_t device_bytes;         /* bytes the index holds on the device                   */
 } tactic_index_info_t;
 
@@ -174,6 +175,14 @@ void tactic_index_destroy(tactic_index_t idx);
  *  every cluster, reading 15),  S7 union over the G heads turned into a balanced
  *  token work list over all units (sub-requests),  S8 split-KV flash-decode
  *  of every head over the union (reading 17),  S9 log-sum-exp merge.
+ * Execution: a chain of kernels (score/rank, sample, fit, attention; the later ones
+ * overlap their prologues with programmatic dependent launch).  With
+ * TACTIC_OPT_CLUSTER_DECODE (and G in {1,2,4,8}, C <= 2048, C x G <= 4096, default
+ * selection rules) S1-S9 of every unit run in ONE launch instead, one thread-block
+ * cluster of ceil(C / M) CTAs per unit (M = 64 or 128 clusters per CTA) exchanging
+ * through distributed shared memory.  Both compute the same selection (parity-tested
+ * against each other and the oracle); the selection outputs of tactic_decode_debug are
+ * written by either.
  *   q    device bf16 [B][Hq][128]          p   0 < p <= 1  (else INVALID_ARGUMENT)
  *   out  device bf16 [B][Hq][128]          lse nullable device float32 [B][Hq] (natural log)
  */
@@ -309,6 +318,11 @@ tactic_status_t tactic_decode_fixed_budget(const void* q, tactic_index_t idx, in
  *     W (exact values take precedence over the fit, as for ranks <= N); the default is
  *     reading 11 (only ranks <= N exact).  0 restores the default.                     */
 #define TACTIC_OPT_WINDOWS_EXACT 1u
+/*   TACTIC_OPT_CLUSTER_DECODE  decode S1-S9 in one launch of per-unit thread-block
+ *     clusters when the index qualifies (see tactic_decode).  Off by default: one unit's
+ *     cluster streams at most ~60 GB/s per SM, so with few units (batch 1) the
+ *     HBM-bound phases cannot spread over the whole chip.               */
+#define TACTIC_OPT_CLUSTER_DECODE 2u
 tactic_status_t tactic_index_set_options(tactic_index_t idx, uint32_t options);
 
 /* ---------------------------------------------------------------------------------------

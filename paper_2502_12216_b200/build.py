@@ -20,8 +20,8 @@ LIB = os.path.join(LIBDIR, "libtactic.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["tactic_api.cu", "attention.cu", "select.cu", "rank_cluster.cu", "kmeans.cu",
-           "tail.cu", "diag.cu"]
-HEADERS = ["common.cuh", "internal.h"]
+           "tail.cu", "diag.cu", "decode_fused.cu"]
+HEADERS = ["common.cuh", "internal.h", "fitmath.cuh"]
 
 
 def _newest(paths):

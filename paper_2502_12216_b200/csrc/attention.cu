@@ -89,29 +89,6 @@ __device__ __forceinline__ int pieces_of_unit(long long us, long long ue, long l
   return cnt;
 }
 
-// Warp-cooperative search (all 32 lanes call it): largest index i in [0, count) with
-// arr[i] <= key, for a non-decreasing arr with arr[0] <= key.  One coalesced probe of
-// 32 entries per round: 2 round trips for count <= 1024 instead of a 10-step chain.
-template <typename T>
-__device__ __forceinline__ int warp_floor_search(const T* arr, int count, T key) {
-  const int lane = threadIdx.x & 31;
-  int base = 0, len = count;
-  while (len > 32) {
-    const int stride = (len + 31) >> 5;
-    const int idx = base + lane * stride;
-    const bool ok = idx < base + len && arr[idx] <= key;
-    const unsigned bal = __ballot_sync(0xffffffffu, ok);
-    const int h = 31 - __clz(bal);
-    const int nb = base + h * stride;
-    const int end = base + len;
-    base = nb;
-    len = (nb + stride < end ? nb + stride : end) - nb;
-  }
-  const bool ok = lane < len && arr[base + lane] <= key;
-  const unsigned bal = __ballot_sync(0xffffffffu, ok);
-  return base + (31 - __clz(bal));
-}
-
 // warp_floor_search over arr[i] + i x (arr non-decreasing, x >= 0)
 __device__ __forceinline__ int warp_floor_search_off(const long long* arr, int count, long long key, long long x) {
   const int lane = threadIdx.x & 31;

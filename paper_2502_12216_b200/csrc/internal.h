@@ -117,6 +117,7 @@ struct tactic_index_s {
   __nv_bfloat16* q_stage = nullptr;  // [units][G][128] (host-buffer decode)
   __nv_bfloat16* o_stage = nullptr;
   long long device_bytes = 0;
+  int fz_checked_m = 0;           // one-launch decode: 0 unchecked, -1 no cluster shape fits, else M
   bool lists_valid = false;      // a p < 1 selection has been enqueued (attention-only needs its lists)
   // tactic_decode_host: the H2D copy, the decode and the D2H copy captured as one CUDA graph,
   // re-captured when its key (host buffers, p, tail length, options) changes
@@ -206,7 +207,41 @@ int sample_blocks(int slots);
 size_t fit_smem_bytes(const tactic_index_s* x, bool windows_exact);
 size_t select_smem_bytes(const tactic_index_s* x);
 cudaError_t launch_stage1b(const SelArgs& a, cudaStream_t s);
-// fused S1-S7 (select_fused.cu)
+// ---- the whole decode step in one cluster launch (decode_fused.cu)
+struct FusedArgs {
+  const __nv_bfloat16* q;          // [units][G][128]
+  const float* cent;               // [units][C][128]
+  const int* offsets;              // [units][C+1]
+  const __nv_bfloat16* Kp;         // [units][n][128] cluster-contiguous, rows swizzled
+  const __nv_bfloat16* Vp;
+  const __nv_bfloat16* Kt;         // recent-token tail [units][tail_cap][128] (nullable)
+  const __nv_bfloat16* Vt;
+  int n, C, units, tail_len, tail_cap;
+  SampleConsts sc;
+  float p;                         // target fraction, < 1
+  int fixed_budget;                // > 0: Quest-like token budget per head (NEXT 4)
+  // selection outputs (the multi-kernel path's layout)
+  double* crit;                    // [units][G][C]
+  int* order;                      // [units][G][C]
+  int* ends;                       // [units][G][C]
+  float* logits;                   // [units][G][slots]
+  double* fit;                     // [units][G][6]
+  int* J;                          // [units][G]
+  uint8_t* umask;                  // [units][C]
+  int* ulist;                      // [units][C]
+  int* uprefix;                    // [units][C+1]
+  long long* unit_prefix;          // nullable [units+1] (global attention split consumers)
+  unsigned int* unit_cnt;          // arrival counter for unit_prefix (zero between calls)
+  __nv_bfloat16* out;              // nullable [units][G][128]
+  float* out_f32;                  // nullable
+  float* lse;                      // nullable [units][G]
+  unsigned long long* tlog;        // nullable debug stamps
+  int dbg_stop;                    // debug: leave after this phase (0 = run to the end)
+};
+// M clusters per CTA (64 or 128), R = ceil(C / M) CTAs per cluster (<= 16)
+cudaError_t launch_decode_fused(const FusedArgs& a, int G, int M, int R, cudaStream_t s);
+int fused_max_active_clusters(int G, int M, int R);
+size_t fused_smem_bytes(int M);
 
 // ---- k-means / layout (kmeans.cu)
 struct KmArgs {

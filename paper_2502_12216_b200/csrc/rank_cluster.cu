@@ -28,6 +28,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "fitmath.cuh"
 
 namespace tactic {
 
@@ -43,13 +44,6 @@ struct SRParams {
   int* rowmap;              // [units][G][slots]
   unsigned long long* tlog;
 };
-
-__device__ __forceinline__ unsigned long long crit_key(double crit, int id) {
-  if (crit == 0.0) crit = 0.0;  // -0 == +0
-  const unsigned long long b = (unsigned long long)__double_as_longlong(-crit);
-  const unsigned long long k = (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // ascending = descending crit
-  return (k & ~0xFFFull) | (unsigned long long)id;
-}
 
 // one entry of a pushed run: sorted key and exclusive size prefix (entry M: ~0, total)
 struct __align__(16) RunEnt {
@@ -110,7 +104,7 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
         bulk_g2s((uint8_t*)s_cent + o, src + o, b, &bar);
       }
     }
-    mbar_arrive_expect_tx(&rbar, (uint32_t)(R * (M + 1) * sizeof(RunEnt)));
+    if (R > 1) mbar_arrive_expect_tx(&rbar, (uint32_t)(R * (M + 1) * sizeof(RunEnt)));
   }
   {
     const int* off = P.offsets + (size_t)u * (C + 1);
@@ -204,16 +198,23 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
   const int pre = wbase + incl - size;  // exclusive
   // push the sorted run into every CTA of the cluster (st.async, completes on their rbar)
   cluster_wait();
+  if constexpr (R == 1) {  // a one-CTA cluster: plain stores (st.async needs a peer CTA)
+    runs[tid] = RunEnt{x, (unsigned long long)pre};
+    if (tid == M - 1) runs[M] = RunEnt{~0ull, (unsigned long long)tot};
+  } else {
 #pragma unroll
-  for (int cc = 0; cc < R; ++cc) {
-    const uint32_t rb = dsmem_addr(&rbar, (uint32_t)cc);
-    st_async_v2u64(dsmem_addr(runs + c * (M + 1) + tid, (uint32_t)cc), x, (unsigned long long)pre, rb);
-    if (tid == M - 1) st_async_v2u64(dsmem_addr(runs + c * (M + 1) + M, (uint32_t)cc), ~0ull, (unsigned long long)tot, rb);
+    for (int cc = 0; cc < R; ++cc) {
+      const uint32_t rb = dsmem_addr(&rbar, (uint32_t)cc);
+      st_async_v2u64(dsmem_addr(runs + c * (M + 1) + tid, (uint32_t)cc), x, (unsigned long long)pre, rb);
+      if (tid == M - 1)
+        st_async_v2u64(dsmem_addr(runs + c * (M + 1) + M, (uint32_t)cc), ~0ull, (unsigned long long)tot, rb);
+    }
   }
   const size_t ug = (size_t)u * P.G + g;
   if (!PS && valid) P.crit[ug * C + j] = crit;
   pstamp(3);
-  mbar_wait(&rbar, 0);
+  if constexpr (R == 1) __syncthreads();
+  else mbar_wait(&rbar, 0);
   pstamp(4);
 
   // ---- global rank and end rank: lower bounds in all R runs (own run: the own position)

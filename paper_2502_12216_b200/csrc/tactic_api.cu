@@ -132,20 +132,23 @@ int device_sms() {
 namespace tactic {
 cudaError_t func_smem_optin(const void* fn, size_t bytes, bool nonportable_cluster) {
   static std::mutex mu;
-  static std::map<std::pair<const void*, int>, size_t> done;
+  static std::map<std::pair<const void*, int>, std::pair<size_t, bool>> done;  // (bytes, non-portable)
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> lk(mu);
-  size_t& have = done[{fn, dev}];
-  if (have >= bytes && have > 0) return cudaSuccess;
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e != cudaSuccess) return e;
-  if (nonportable_cluster) {
+  auto& have = done[{fn, dev}];
+  if (have.first >= bytes && have.first > 0 && (have.second || !nonportable_cluster)) return cudaSuccess;
+  if (have.first < bytes || have.first == 0) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    have.first = bytes > 0 ? bytes : 1;
+  }
+  if (nonportable_cluster && !have.second) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
+    have.second = true;
   }
-  have = bytes > 0 ? bytes : 1;
   return cudaSuccess;
 }
 
@@ -471,6 +474,8 @@ static tactic_status_t build_common(const void* K, const void* V, const tactic_k
 }
 
 extern "C" {
+static bool fused_plan(tactic_index_t idx, int* M, int* R);
+
 
 tactic_status_t tactic_build_index(const void* K, const void* V, const tactic_kv_desc_t* kv, int32_t n_clusters,
                                    int32_t iters, const tactic_params_t* params, void* stream,
@@ -564,7 +569,8 @@ tactic_status_t tactic_assign_tokens(tactic_index_t idx, const void* k, int32_t 
 
 tactic_status_t tactic_index_set_options(tactic_index_t idx, uint32_t options) {
   if (!idx) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL index");
-  if (options & ~(uint32_t)TACTIC_OPT_WINDOWS_EXACT) return fail(TACTIC_ERR_INVALID_ARGUMENT, "unknown option bits");
+  if (options & ~(uint32_t)(TACTIC_OPT_WINDOWS_EXACT | TACTIC_OPT_CLUSTER_DECODE))
+    return fail(TACTIC_ERR_INVALID_ARGUMENT, "unknown option bits");
   tactic_status_t st = check_select_limits(idx, (options & TACTIC_OPT_WINDOWS_EXACT) != 0);
   if (st) return st;
   idx->options = options;
@@ -620,7 +626,8 @@ tactic_status_t tactic_index_info(tactic_index_t idx, tactic_index_info_t* info)
   info->n_clusters = idx->C;
   info->iters_requested = idx->iters_req;
   info->device_bytes = idx->device_bytes;
-  info->select_cluster_size = 0;  // (the fused single-kernel selection was retired in round 1)
+  int fm = 0, fr = 0;
+  info->select_cluster_size = fused_plan(idx, &fm, &fr) ? fr : 0;
   return TACTIC_OK;
 }
 
@@ -658,6 +665,86 @@ tactic_status_t tactic_index_export(tactic_index_t idx, float* centroids, int32_
 }
 
 // ------------------------------------------------------------------------ decode
+// One-launch decode (decode_fused.cu, TACTIC_OPT_CLUSTER_DECODE): M clusters per CTA and
+// R CTAs per unit cluster, or false when the index decodes through the multi-kernel chain.
+// TACTIC_FUSED_M=128 prefers 128 clusters per CTA (measurement aid).
+static bool fused_plan(tactic_index_t idx, int* M, int* R) {
+  static const int env_m = [] { const char* e = getenv("TACTIC_FUSED_M"); return e ? atoi(e) : 0; }();
+  if (!(idx->options & TACTIC_OPT_CLUSTER_DECODE) || (idx->options & TACTIC_OPT_WINDOWS_EXACT)) return false;
+  const int G = idx->G, C = idx->C;
+  if (!(G == 1 || G == 2 || G == 4 || G == 8) || C > 2048 || (long long)C * G > 4096 || idx->n >= (1 << 24))
+    return false;
+  static const bool verbose = [] { const char* e = getenv("TACTIC_VERBOSE"); return e && e[0] == '1'; }();
+  if (idx->fz_checked_m == 0) {
+    // first decode: the smallest M whose clusters all fit in one wave (every unit resident
+    // at once), else the M that keeps the most SMs busy per wave
+    idx->fz_checked_m = -1;
+    long long best = 0;
+    for (int m : {64, 128}) {
+      if ((m == 64 && (C > 1024 || env_m == 128)) || C > 16 * m) continue;
+      const int r = (C + m - 1) / m;
+      // stage region (decode_fused.cu): R run blocks + R candidate blocks + >= 2 sample stages
+      const size_t rblk = ((size_t)G * (m + 1) * 12 + 15) & ~(size_t)15;
+      const size_t cblk = (16 + (size_t)m * (3 + G) * 4 + 15) & ~(size_t)15;
+      if (r * (rblk + cblk) > 128 * 1024 || 128 * 1024 - r * cblk < 2 * 16384) continue;
+      const int nc = fused_max_active_clusters(G, m, r);
+      if (verbose) fprintf(stderr, "[tactic] one-launch decode G=%d M=%d R=%d: %d clusters resident\n", G, m, r, nc);
+      if (nc >= idx->units) {
+        idx->fz_checked_m = m;
+        break;
+      }
+      if (nc >= 1 && (long long)nc * r > best) {
+        best = (long long)nc * r;
+        idx->fz_checked_m = m;
+      }
+    }
+  }
+  if (idx->fz_checked_m <= 0) return false;
+  *M = idx->fz_checked_m;
+  *R = (C + *M - 1) / *M;
+  return true;
+}
+
+static tactic_status_t run_fused(const void* q, tactic_index_t idx, float p, int M, int R, cudaStream_t s,
+                                 void* out, float* out_f32, float* lse) {
+  FusedArgs a = {};
+  a.q = (const __nv_bfloat16*)q;
+  a.cent = idx->cent;
+  a.offsets = idx->offsets;
+  a.Kp = idx->Kp;
+  a.Vp = idx->Vp;
+  a.Kt = idx->Kt;
+  a.Vt = idx->Vt;
+  a.n = idx->n;
+  a.C = idx->C;
+  a.units = idx->units;
+  a.tail_len = idx->tail_len;
+  a.tail_cap = idx->tail_cap;
+  a.sc = idx->sc;
+  a.p = p;
+  a.fixed_budget = idx->fixed_budget;
+  a.crit = idx->crit;
+  a.order = idx->order;
+  a.ends = idx->ends;
+  a.logits = idx->logits;
+  a.fit = idx->fit;
+  a.J = idx->J;
+  a.umask = idx->umask;
+  a.ulist = idx->union_list;
+  a.uprefix = idx->union_prefix;
+  a.unit_prefix = unit_split_ok(idx->units, idx->num_ctas) ? nullptr : idx->unit_prefix;
+  a.unit_cnt = idx->counter;
+  a.out = (__nv_bfloat16*)out;
+  a.out_f32 = out_f32;
+  a.lse = lse;
+  a.tlog = idx->tlog;
+  static const int dbg_stop = [] { const char* e = getenv("TACTIC_FUSED_STOP"); return e ? atoi(e) : 0; }();
+  a.dbg_stop = dbg_stop;
+  CK(launch_decode_fused(a, idx->G, M, R, s));
+  idx->lists_valid = true;
+  return TACTIC_OK;
+}
+
 static tactic_status_t run_selection(const void* q, tactic_index_t idx, double p, int mode, cudaStream_t s,
                                      const double* gmax, const double* gmass, double* local_max) {
   SelArgs sa = {};
@@ -733,6 +820,8 @@ tactic_status_t tactic_decode_ex(const void* q, tactic_index_t idx, float p, voi
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
   if (p >= 1.0f) return run_attention(q, idx, true, s, out, nullptr, lse, nullptr, true);  // reading 15
+  int M = 0, R = 0;
+  if (fused_plan(idx, &M, &R)) return run_fused(q, idx, p, M, R, s, out, nullptr, lse);
   if ((st = run_selection(q, idx, (double)p, 0, s, nullptr, nullptr, nullptr))) return st;
   return run_attention(q, idx, false, s, out, nullptr, lse);
 }
@@ -820,8 +909,13 @@ tactic_status_t tactic_decode_debug(const void* q, tactic_index_t idx, float p, 
   tactic_status_t st = check_p(p);
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  if ((st = run_selection(q, idx, (double)p, 0, s, nullptr, nullptr, nullptr))) return st;
-  if ((st = run_attention(q, idx, false, s, out, nullptr, lse))) return st;
+  int M = 0, R = 0;
+  if (p < 1.0f && fused_plan(idx, &M, &R)) {
+    if ((st = run_fused(q, idx, p, M, R, s, out, nullptr, lse))) return st;
+  } else {
+    if ((st = run_selection(q, idx, (double)p, 0, s, nullptr, nullptr, nullptr))) return st;
+    if ((st = run_attention(q, idx, false, s, out, nullptr, lse))) return st;
+  }
   const size_t U = idx->units, G = idx->G, C = idx->C;
   if (order) CK(cudaMemcpyAsync(order, idx->order, U * G * C * 4, cudaMemcpyDeviceToHost, s));
   if (J) CK(cudaMemcpyAsync(J, idx->J, U * G * 4, cudaMemcpyDeviceToHost, s));

@@ -100,12 +100,15 @@ def _check_unit_selection(res, u, G, heads_o, p, C):
     return True
 
 
+@pytest.mark.parametrize("path", ["fused", "multi"])
 @pytest.mark.parametrize("n,C,seed", [(4096, 64, 0), (4096, 64, 1), (32768, 256, 2), (5000, 77, 3)])
-def test_import_decode_selection_and_output(T, n, C, seed):
+def test_import_decode_selection_and_output(T, n, C, seed, path):
     G = 4
     K, V, q = _layer(1, 2, G, n, seed)
     cents, asg, idxs = oracle_layer_clustering(K, V, C, 10, seed)
     index = _import(T, K, V, cents, asg, G)
+    T.set_options(index, T.OPT_CLUSTER_DECODE if path == "fused" else 0)
+    assert (index.info()["select_cluster_size"] > 0) == (path == "fused")
     qd = dev_bf16(q)
     for p in [0.5, 0.8, 0.9, 0.95, 0.99]:
         res = T.decode_debug(qd, index, p)
@@ -138,12 +141,14 @@ def test_import_decode_p1_equals_full_attention(T):
         assert_output_close(out[0, u * G:(u + 1) * G], o, "p=1")
 
 
+@pytest.mark.parametrize("path", ["fused", "multi"])
 @pytest.mark.parametrize("G", [1, 2, 8])
-def test_group_sizes(T, G):
+def test_group_sizes(T, G, path):
     n, C = 4096, 64
     K, V, q = _layer(1, 1, G, n, 10 + G)
     cents, asg, idxs = oracle_layer_clustering(K, V, C, 10, G)
     index = _import(T, K, V, cents, asg, G)
+    T.set_options(index, T.OPT_CLUSTER_DECODE if path == "fused" else 0)
     res = T.decode_debug(dev_bf16(q), index, 0.9)
     ro = O.decode_unit(q[0], idxs[0], 0.9)
     _check_unit_selection(res, 0, G, ro["heads"], 0.9, C)
@@ -152,13 +157,16 @@ def test_group_sizes(T, G):
     assert_output_close(res["out"].float().cpu().numpy()[0], o, f"G={G}")
 
 
-def test_edge_cases_tiny_fallback_singletons_empty_clusters(T):
+@pytest.mark.parametrize("path", ["fused", "multi"])
+def test_edge_cases_tiny_fallback_singletons_empty_clusters(T, path):
+    opt = T.OPT_CLUSTER_DECODE if path == "fused" else 0
     G = 4
     # tiny n -> exact fallback (O6)
     u = make_unit(12, G, seed=1)
     K, V, q = u["K"][None, None], u["V"][None, None], u["q"][None]
     cents, asg, idxs = oracle_layer_clustering(K, V, 3, 10, 1)
     index = _import(T, K, V, cents, asg, G)
+    T.set_options(index, opt)
     for p in [0.5, 0.9]:
         res = T.decode_debug(dev_bf16(q), index, p)
         ro = O.decode_unit(q[0], idxs[0], p)
@@ -169,6 +177,7 @@ def test_edge_cases_tiny_fallback_singletons_empty_clusters(T):
     K, V, q = u["K"][None, None], u["V"][None, None], u["q"][None]
     idx = O.make_index(u["K"], u["V"], u["K"], np.arange(256))
     index = _import(T, K, V, u["K"][None], np.arange(256, dtype=np.int32)[None], G)
+    T.set_options(index, opt)
     res = T.decode_debug(dev_bf16(q), index, 0.8)
     ro = O.decode_unit(q[0], idx, 0.8)
     _check_unit_selection(res, 0, G, ro["heads"], 0.8, 256)
@@ -184,11 +193,13 @@ def test_edge_cases_tiny_fallback_singletons_empty_clusters(T):
     cents[[5, 17, 40]] = 1e3  # high criticality but empty: must never be selected
     idx = O.make_index(u["K"], u["V"], cents, asg)
     index = _import(T, K, V, cents[None], asg.astype(np.int32)[None], G)
+    T.set_options(index, opt)
     res = T.decode_debug(dev_bf16(q), index, 0.9)
     ro = O.decode_unit(q[0], idx, 0.9)
     _check_unit_selection(res, 0, G, ro["heads"], 0.9, 51)
     assert not res["union_mask"][0][[5, 17, 40]].any()
     index1 = _import(T, K, V, u["K"][:1][None], np.zeros((1, 3000), dtype=np.int32), G)
+    T.set_options(index1, opt)
     out1 = T.decode(dev_bf16(q), index1, 0.5).float().cpu().numpy()
     o, _ = O.full_attention(q[0], u["K"], u["V"])
     assert_output_close(out1[0], o, "C=1")
@@ -636,17 +647,24 @@ def test_per_head_loading_with_tail(T):
 
 
 def test_attention_only_reproduces_decode(T):
-    """tactic_decode_attention_only (the bench's roofline timing) reruns S8 + S9 over the
-    work lists of the last selection: bit-identical output, also when called repeatedly."""
+    """tactic_decode_attention_only reruns S8 + S9 (the multi-kernel attention kernel) over
+    the work lists of the last selection: bit-identical to the multi-kernel decode, also
+    when called repeatedly; the one-launch decode writes the same lists (its own token
+    split, so equal within rounding)."""
     B, H, G, n, C = 1, 2, 4, 8192, 64
     K, V, q = _layer(B, H, G, n, 321)
     cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, B)
     index = _import(T, K, V, cents, asg, G)
     qd = dev_bf16(q)
-    ref = T.decode(qd, index, 0.9)
-    out = torch.empty_like(ref)
-    for _ in range(3):
-        out.zero_()
-        T.decode_attention_only(qd, index, out)
-        torch.cuda.synchronize()
-        assert torch.equal(out, ref)
+    for opt in (0, T.OPT_CLUSTER_DECODE):
+        T.set_options(index, opt)
+        ref = T.decode(qd, index, 0.9)
+        out = torch.empty_like(ref)
+        for _ in range(3):
+            out.zero_()
+            T.decode_attention_only(qd, index, out)
+            torch.cuda.synchronize()
+            if not opt:
+                assert torch.equal(out, ref)
+            else:
+                assert_output_close(out.float().cpu().numpy(), ref.float().cpu().numpy(), "attention-only")
