@@ -76,6 +76,10 @@ for it in range(4):
         names = ["head0 last chunk", "staged", "fitted", "marked", "unit0 compact start", "unit0 compact end"]
         print("  sample_fit (us from first start): " + "  ".join(f"{nm} {(fs[i] - z) / 1e3:6.2f}" for i, nm in enumerate(names)
                                                               if fs[i] > 0))
+        ds = full[270:274]
+        if ds[0] > 0:
+            print("  fit unit 0 descriptors (us from first start): " + "  ".join(
+                f"{nm} {(x - z) / 1e3:.2f}" for nm, x in zip(["arrived", "all arrived", "totals", "written"], ds)))
         hs = full[1700:1705]
         if hs[0] > 0:
             print("  fit warp 0 (us after summaries staged): " + "  ".join(
