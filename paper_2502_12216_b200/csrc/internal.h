@@ -100,11 +100,8 @@ struct tactic_index_s {
   int* head_cnt2 = nullptr;      // [units*G] attention arrival counters of the ablation
   int fixed_budget = 0;          // > 0 during tactic_decode_fixed_budget (NEXT 4 baseline)
   uint32_t options = 0;          // TACTIC_OPT_* (tactic_index_set_options)
-  uint8_t* mask_acc = nullptr;   // [units][C] union accumulator (zero between calls)
-  unsigned int* head_cnt = nullptr;  // [units] selection arrival counters
   float* logits = nullptr;       // [units][G][slots]
   double* fit = nullptr;         // [units][G][6]
-  double* cumend = nullptr;      // [units][G][C] (sharded stage 1)
   int* J = nullptr;              // [units][G]
   uint8_t* umask = nullptr;      // [units][C]
   int* union_list = nullptr;     // [units][C] first layout row of each union segment
@@ -113,7 +110,7 @@ struct tactic_index_s {
   unsigned int* counter = nullptr;   // last-block counter (self-resetting)
   float* part_o = nullptr;       // [num_ctas + units][G][128]
   float* part_lse = nullptr;     // [num_ctas + units][G]
-  double* stage = nullptr;       // sharded mode scratch [units][G][2]
+  double* stage = nullptr;       // sharded stage 1 -> 1b: [units][G][2] (E_N, 0)
   __nv_bfloat16* q_stage = nullptr;  // [units][G][128] (host-buffer decode)
   __nv_bfloat16* o_stage = nullptr;
   long long device_bytes = 0;
@@ -187,7 +184,7 @@ struct SelArgs {
   const __nv_bfloat16* q;
   tactic_index_s* idx;
   double p;
-  int mode;                        // 0 = normal, 1 = sharded stage-2 (grid threshold)
+  int mode;                        // 0 = Alg. 1, 1 = sharded stage 2 (theta*), 2 = sharded stage 1
   const double* gmax;              // [units][G][2] (stage 2 / 1b)
   const double* gmass;             // [units][G][1+T]
   double* mass_out;                // stage 1b
@@ -199,13 +196,12 @@ cudaError_t launch_score_all(const __nv_bfloat16* q, tactic_index_s* x, cudaStre
 // S1 + S2 + S3 (rank_cluster.cu): crit, order, ends, sampled-slot row map
 cudaError_t launch_score_rank(const __nv_bfloat16* q, tactic_index_s* x, cudaStream_t s, bool pdl);
 cudaError_t launch_sample(const SelArgs& a, cudaStream_t s, bool pdl);
-cudaError_t launch_select(const SelArgs& a, cudaStream_t s, bool pdl);
 cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl);
 int sample_blocks(int slots);
 // dynamic shared memory of the fit kernel (every decode with p < 1) and of the sharded
 // stages' select kernel; checked against the device's opt-in limit at build / import
 size_t fit_smem_bytes(const tactic_index_s* x, bool windows_exact);
-size_t select_smem_bytes(const tactic_index_s* x);
+size_t stage1b_smem_bytes(const tactic_index_s* x);
 cudaError_t launch_stage1b(const SelArgs& a, cudaStream_t s);
 // ---- the whole decode step in one cluster launch (decode_fused.cu)
 struct FusedArgs {

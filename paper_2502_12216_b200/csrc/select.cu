@@ -1,25 +1,24 @@
-// select.cu -- decode-time selection S1-S7 (§4.3-§4.6, App. B Alg. 1).
+// select.cu -- decode-time selection S1, S4-S7 (§4.3-§4.6, App. B Alg. 1).
 //
-//  score_kernel   S1  crit[u][g][j] = q_g . c_j in float64 (products of a
-//                     bf16 query and a float32 centroid are exact in fp64, so only the
-//                     summation order differs from the oracle).  A warp scores 32/G
-//                     centroids for all G heads and reduce-scatters the 32 partial sums
-//                     with a shuffle butterfly (31 exchanges instead of 5 per value).
-//  (S1 + S2 + S3 of the normal path run in rank_cluster.cu: one cluster kernel that
-//   scores, sorts and writes order / end ranks / the sampled-slot row map; score_kernel
-//   here serves the sharded stage 2, which needs crit only)
-//  sample_kernel  S4  exact logits q.k/sqrt(d) of the sampled ranks: the first N ranks
-//                     and two windows of 2w+1 ranks around x1, x2 (Alg. 1 l.4,
-//                     readings 8-11); 16 rows in flight per warp.
-//  select_kernel  S4-S6 per (unit, head): shift m, exact head weights + prefix, window
-//                     means, two-point fit y = a/x + b, estimated total W,
-//                     minimal k with cum(k) >= p W (Alg. 1 l.10) at cluster
-//                     granularity (reading 14); marks the selected clusters.
-//                 S7  the last head of a unit to finish compacts the GQA union
-//                     into the attention work list; the last unit to finish writes the
-//                     global token prefix over units (sub-requests).
-// The clamp-aware tail sum  sum_{i=N+1}^{k} max(0, a/i + b)  uses harmonic numbers
-// from the asymptotic digamma series (exact sums below 20) instead of a table.
+//  score_kernel    S1  crit[u][g][j] = q_g . c_j in float64 (products of a
+//                      bf16 query and a float32 centroid are exact in fp64, so only the
+//                      summation order differs from the oracle).  A warp scores 32/G
+//                      centroids for all G heads and reduce-scatters the 32 partial sums
+//                      with a shuffle butterfly (31 exchanges instead of 5 per value).
+//                      Used before score_rank_kernel when the clusters span several waves.
+//  (S1 + S2 + S3 run in rank_cluster.cu: scores, sorted order, end ranks, row map)
+//  sample_kernel   S4  exact logits q.k/sqrt(d) of the sampled ranks: the first N ranks
+//                      and two windows of 2w+1 ranks around x1, x2 (Alg. 1 l.4,
+//                      readings 8-11), with per-block summaries for the fit.
+//  fit_unit_kernel S5-S7 per unit (one warp per head): shift m, E_N, window means,
+//                      two-point fit y = a/x + b, W, minimal k with
+//                      cum(k) >= p W (Alg. 1 l.10) at cluster granularity (reading
+//                      14), the GQA union compacted into the attention work list.
+//                      Sequence-sharded mode (reading 23): stage 1 = the fit only, stage 2
+//                      = the shared threshold theta* selects a rank prefix per head.
+//  stage1b_kernel  sharded stage 1b: the shard's mass above every grid point.
+// The clamp-aware tail sum  sum_{i=N+1}^{k} max(0, a/i + b)  uses harmonic numbers from
+// the asymptotic digamma series (fitmath.cuh) instead of a table.
 #include <cuda_bf16.h>
 #include <float.h>
 #include <limits.h>
@@ -29,83 +28,6 @@
 #include "fitmath.cuh"
 
 namespace tactic {
-
-constexpr int SEL_THREADS = 512;
-constexpr int RANK_THREADS = 512;
-
-// ------------------------------------------------------------------ helpers
-__device__ double harmonic(long long k) {
-  if (k <= 0) return 0.0;
-  if (k < 20) {
-    double s = 0.0;
-    for (long long i = k; i >= 1; --i) s += 1.0 / (double)i;
-    return s;
-  }
-  const double x = (double)k, x2 = 1.0 / (x * x);
-  return log(x) + 0.57721566490153286061 + 0.5 / x -
-         x2 * (1.0 / 12.0 - x2 * (1.0 / 120.0 - x2 * (1.0 / 252.0 - x2 * (1.0 / 240.0 - x2 * (1.0 / 132.0)))));
-}
-
-// sum_{i=N+1}^{k} max(0, a/i + b)
-__device__ double tail_mass(double a, double b, long long N, long long k) {
-  if (k <= N) return 0.0;
-  if (a >= 0.0 && b >= 0.0) return a * (harmonic(k) - harmonic(N)) + b * (double)(k - N);
-  if (a <= 0.0 && b <= 0.0) return 0.0;
-  if (a > 0.0) {  // b < 0: positive while i < a/(-b)
-    const double t = a / (-b);
-    long long top = t >= 9.0e15 ? k : (long long)floor(t);
-    if (top > k) top = k;
-    while (top < k && a / (double)(top + 1) + b > 0.0) ++top;
-    while (top > N && !(a / (double)top + b > 0.0)) --top;
-    if (top <= N) return 0.0;
-    return a * (harmonic(top) - harmonic(N)) + b * (double)(top - N);
-  }
-  // a < 0, b > 0: positive once i > (-a)/b
-  const double t = (-a) / b;
-  long long lo = t >= 9.0e15 ? k + 1 : (long long)floor(t) + 1;
-  if (lo < N + 1) lo = N + 1;
-  while (lo > N + 1 && a / (double)(lo - 1) + b > 0.0) --lo;
-  while (lo <= k && !(a / (double)lo + b > 0.0)) ++lo;
-  if (lo > k) return 0.0;
-  return a * (harmonic(k) - harmonic(lo - 1)) + b * (double)(k - lo + 1);
-}
-
-template <typename T> __device__ __forceinline__ T lowest();
-template <> __device__ __forceinline__ float lowest<float>() { return -INFINITY; }
-template <> __device__ __forceinline__ double lowest<double>() { return -INFINITY; }
-template <> __device__ __forceinline__ int lowest<int>() { return INT_MIN; }
-template <typename T> __device__ __forceinline__ T highest();
-template <> __device__ __forceinline__ double highest<double>() { return INFINITY; }
-
-enum { RED_SUM = 0, RED_MAX = 1, RED_MIN = 2 };
-
-template <typename T, int OP>
-__device__ __forceinline__ T red_op(T a, T b) {
-  if (OP == RED_SUM) return a + b;
-  if (OP == RED_MAX) return a > b ? a : b;
-  return a < b ? a : b;
-}
-
-template <typename T, int OP>
-__device__ T block_reduce(T v, T* red) {
-  const T ident = OP == RED_SUM ? (T)0 : (OP == RED_MAX ? lowest<T>() : highest<T>());
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = red_op<T, OP>(v, __shfl_xor_sync(0xffffffffu, v, o));
-  __syncthreads();
-  if (lane == 0) red[w] = v;
-  __syncthreads();
-  if (w == 0) {
-    v = lane < nw ? red[lane] : ident;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = red_op<T, OP>(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) red[0] = v;
-  }
-  __syncthreads();
-  T r = red[0];
-  __syncthreads();
-  return r;
-}
 
 // exclusive scan of per-thread totals across the block; returns this thread's offset
 template <typename T>
@@ -135,29 +57,6 @@ __device__ T block_exclusive_scan(T v, T* red, T* total) {
   T r = red[w] + inc - v;
   __syncthreads();
   return r;
-}
-
-// smallest k in [lo, hi] with pred(k) true; pred(hi) must hold; pred monotone.
-template <typename Pred>
-__device__ long long block_lower_bound(long long lo, long long hi, Pred pred, long long* sh) {
-  while (lo < hi) {
-    const long long cnt = hi - lo + 1;
-    const long long step = (cnt + blockDim.x - 1) / blockDim.x;
-    const long long k = lo + (long long)threadIdx.x * step;
-    if (threadIdx.x == 0) sh[0] = LLONG_MAX;
-    __syncthreads();
-    if (k <= hi && pred(k)) atomicMin((unsigned long long*)sh, (unsigned long long)threadIdx.x);
-    __syncthreads();
-    const long long t = sh[0];
-    __syncthreads();
-    if (t == LLONG_MAX) return hi;  // unreachable when pred(hi) holds (kept for safety)
-    const long long nhi = lo + t * step;
-    const long long nlo = t > 0 ? lo + (t - 1) * step + 1 : lo;
-    lo = nlo;
-    hi = nhi < hi ? nhi : hi;
-    if (step == 1) return hi;
-  }
-  return lo;
 }
 
 // ------------------------------------------------------------------ S1
@@ -358,6 +257,15 @@ struct FitParams {
   int tail_len;              // recent-token tail per unit (counted in unit_prefix)
   int fixed_budget;          // > 0: Quest-like fixed token budget per head (NEXT 4 baseline)
   int windows_exact;         // SPEC variant: window ranks keep their exact weights
+  // sequence-sharded mode (reading 23): 0 = Alg. 1 selection; 2 = stage 1 (fit only:
+  // local shift m, theta_max, E_N, W; no selection); 1 = stage 2 (the shared threshold
+  // theta* from the all-reduced mass vector selects a rank prefix per head)
+  int shard_mode;
+  const double* crit;        // [units][G][C] (stage 1's criticalities)
+  const double* gmax;        // stage 2: [units][G][2] global (m, theta_max)
+  const double* gmass;       // stage 2: [units][G][1 + T] global (W, M(theta_t))
+  double* local_max;         // stage 1: [units][G][2] local (m, theta_max)
+  double* en_out;            // stage 1: [units][G][2] (E_N, 0) for stage 1b
 };
 
 // ------------------------------------------------------------------ S5-S7, one CTA per unit
@@ -476,8 +384,9 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
     stamp(1);
     if (tid == 0) tl_mark(P.tlog, 3, 1, u == 0);
     // stage the sample kernel's summaries (one round trip; + the window logits of every
-    // head for the windows-exact variant, from the 16-byte aligned slot at or below N)
-    if (tid == 0) {
+    // head for the windows-exact variant, from the 16-byte aligned slot at or below N);
+    // sharded stage 2 needs none (its rule reads the mass vector)
+    if (tid == 0 && P.shard_mode != 1) {
       const uint32_t bs = (uint32_t)G * nb * 16;
       uint32_t lb = 0;
       if (s_wx)
@@ -494,12 +403,43 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
                    (uint32_t)((((st - al) + 2 * W1s) * 4 + 15) & ~(size_t)15), &sbar);
         }
     }
-    mbar_wait(&sbar, 0);
+    if (P.shard_mode != 1) mbar_wait(&sbar, 0);
     __syncthreads();
     stamp(2);
     if (stamp_on && tid == 0) P.tlog[1709] = clock64();
   }
-  if (warp < G) {
+  if (warp < G && P.shard_mode == 1) {
+    // sharded stage 2 (reading 23): theta* = the largest grid point theta_t whose
+    // all-reduced mass reaches p W (none: every cluster); the head selects the rank prefix
+    // of clusters with crit / sqrt(d) >= theta* (the order is by descending crit)
+    const int g = warp;
+    const double* gm = P.gmass + (ub + g) * (1 + TACTIC_SHARD_GRID_T);
+    const double thmax = P.gmax[(ub + g) * 2 + 1], Wt = gm[0];
+    int tmin = TACTIC_SHARD_GRID_T + 1;
+    if (P.p < 1.0)
+      for (int t0 = 1; t0 <= TACTIC_SHARD_GRID_T; t0 += 32) {
+        const unsigned hit = __ballot_sync(0xffffffffu, t0 + lane <= TACTIC_SHARD_GRID_T && gm[t0 + lane] >= P.p * Wt);
+        if (hit) {
+          tmin = t0 + __ffs(hit) - 1;
+          break;
+        }
+      }
+    const double thstar = tmin <= TACTIC_SHARD_GRID_T ? thmax - (double)tmin * TACTIC_SHARD_GRID_STEP : -INFINITY;
+    const double* cr = P.crit + (ub + g) * C;
+    const int* ord = s_ord + (size_t)g * C;
+    const double isd = 1.0 / sqrt(128.0);
+    const int J = warp_count_false(C, [&](int r) { return cr[ord[r]] * isd < thstar; });
+    if (lane == 0) {
+      P.J[ub + g] = J;
+      double* f = P.fit + (ub + g) * 6;
+      f[0] = thstar; f[1] = Wt; f[2] = P.gmax[(ub + g) * 2]; f[3] = thmax; f[4] = 0; f[5] = 0;
+    }
+    __syncwarp();
+    for (int r = lane; r < J; r += 32) {
+      const int cid = ord[r];
+      if (s_off[cid + 1] > s_off[cid]) mask[cid] = 1;
+    }
+  } else if (warp < G) {
     const int g = warp;
     const float* sg = sm + (size_t)g * nb * 4;
     // common shift m = max of the block maxima (reading 13), then the three region sums
@@ -558,94 +498,109 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
       W = windows_cum(EN, tail, xw, sc, n);
     }
     wstamp(1);
-    int J = C;  // p >= 1: every cluster (reading 15)
-    if (P.fixed_budget > 0) {
-      // Quest-like baseline: clusters in criticality order until the head
-      // holds fixed_budget tokens (rounded up to the cluster end, as reading 14)
-      const int* eg = s_end + (size_t)g * C;
-      J = 1 + warp_count_false(C - 1, [&](int r) { return eg[r] >= P.fixed_budget; });
-    } else if (P.p < 1.0) {
-      const float target = (float)P.p * W;
-      const int* eg = s_end + (size_t)g * C;
-      if (EN >= target) {
-        // the crossing lies inside the exact head (slots 0..nex-1 = ranks 1..nex): the
-        // block of SB slots that crosses, then the slot inside it (one global round trip)
-        const int nex = sc.fallback ? n : sc.N;
-        const int nbh = (nex + SB - 1) / SB;
-        float carry = 0.f, before = 0.f;
-        int bs = nbh - 1;
-        for (int b0 = 0; b0 < nbh; b0 += 32) {
-          const int bb = b0 + lane;
-          const float vo = bb < nbh ? sg[bb * 4 + 1] * __expf(sg[bb * 4] - m) : 0.f;
-          float v = vo;
-#pragma unroll
+    if (P.shard_mode == 2) {  // sharded stage 1: the local fit only (stage 1b uses it)
+      if (lane == 0) {
+        double* f = P.fit + (ub + g) * 6;
+        f[0] = a; f[1] = b; f[2] = m; f[3] = W; f[4] = mu1; f[5] = mu2;
+        P.en_out[(ub + g) * 2] = EN;
+        P.en_out[(ub + g) * 2 + 1] = 0.0;
+        P.local_max[(ub + g) * 2] = m;
+        P.local_max[(ub + g) * 2 + 1] = P.crit[(ub + g) * C + s_ord[(size_t)g * C]] / sqrt(128.0);
+      }
+    } else {  // the selection (stage 1 selects nothing)
+      int J = C;  // p >= 1: every cluster (reading 15)
+      if (P.fixed_budget > 0) {
+        // Quest-like baseline: clusters in criticality order until the head
+        // holds fixed_budget tokens (rounded up to the cluster end, as reading 14)
+        const int* eg = s_end + (size_t)g * C;
+        J = 1 + warp_count_false(C - 1, [&](int r) { return eg[r] >= P.fixed_budget; });
+      } else if (P.p < 1.0) {
+        const float target = (float)P.p * W;
+        const int* eg = s_end + (size_t)g * C;
+        if (EN >= target) {
+          // the crossing lies inside the exact head (slots 0..nex-1 = ranks 1..nex): the
+          // block of SB slots that crosses, then the slot inside it (one global round trip)
+          const int nex = sc.fallback ? n : sc.N;
+          const int nbh = (nex + SB - 1) / SB;
+          float carry = 0.f, before = 0.f;
+          int bs = nbh - 1;
+          for (int b0 = 0; b0 < nbh; b0 += 32) {
+            const int bb = b0 + lane;
+            const float vo = bb < nbh ? sg[bb * 4 + 1] * __expf(sg[bb * 4] - m) : 0.f;
+            float v = vo;
+  #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const float x = __shfl_up_sync(0xffffffffu, v, o);
+              if (lane >= o) v += x;
+            }
+            const unsigned hit = __ballot_sync(0xffffffffu, bb < nbh && carry + v >= target);
+            if (hit) {
+              const int hl = __ffs(hit) - 1;
+              bs = b0 + hl;
+              before = carry + __shfl_sync(0xffffffffu, v, hl) - __shfl_sync(0xffffffffu, vo, hl);
+              break;
+            }
+            carry += __shfl_sync(0xffffffffu, v, 31);
+            before = carry;
+          }
+          const int s0 = bs * SB, s1 = min(nex, s0 + SB);
+          constexpr int PER = SB / 32;  // consecutive slots per lane
+          float w[PER];
+  #pragma unroll
+          for (int k = 0; k < PER; ++k) {
+            const int s = s0 + PER * lane + k;
+            w[k] = s < s1 ? __expf(__ldcg(P.logits + (ub + g) * sc.slots + s) - m) : 0.f;
+          }
+  #pragma unroll
+          for (int k = 1; k < PER; ++k) w[k] += w[k - 1];
+          float v = w[PER - 1];
+  #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             const float x = __shfl_up_sync(0xffffffffu, v, o);
             if (lane >= o) v += x;
           }
-          const unsigned hit = __ballot_sync(0xffffffffu, bb < nbh && carry + v >= target);
-          if (hit) {
-            const int hl = __ffs(hit) - 1;
-            bs = b0 + hl;
-            before = carry + __shfl_sync(0xffffffffu, v, hl) - __shfl_sync(0xffffffffu, vo, hl);
-            break;
-          }
-          carry += __shfl_sync(0xffffffffu, v, 31);
-          before = carry;
+          const float excl = before + v - w[PER - 1];
+          int kl = PER;
+  #pragma unroll
+          for (int k = PER - 1; k >= 0; --k)
+            if (s0 + PER * lane + k < s1 && excl + w[k] >= target) kl = k;
+          const unsigned hit = __ballot_sync(0xffffffffu, kl < PER);
+          const int hl = hit ? __ffs(hit) - 1 : 31;
+          const int kls = __shfl_sync(0xffffffffu, kl, hl);
+          // k* = the 1-based rank of the crossing slot (rounding guard: the block's last slot)
+          const int kstar = hit ? s0 + PER * hl + kls + 1 : s1;
+          J = 1 + warp_count_false(C - 1, [&](int r) { return eg[r] >= kstar; });
+        } else {
+          // past the head: cum(e_r) = EN + tail(e_r) at the cluster ends; the first cluster
+          // whose end reaches the target (ends are non-decreasing in rank)
+          const int r = xw ? warp_count_false(C, [&](int r) { return eg[r] > sc.N && windows_cum(EN, tail, xw, sc, eg[r]) >= target; })
+                           : warp_count_false(C, [&](int r) { return eg[r] > sc.N && EN + tail(eg[r]) >= target; });
+          J = r < C ? r + 1 : C;
         }
-        const int s0 = bs * SB, s1 = min(nex, s0 + SB);
-        constexpr int PER = SB / 32;  // consecutive slots per lane
-        float w[PER];
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-          const int s = s0 + PER * lane + k;
-          w[k] = s < s1 ? __expf(__ldcg(P.logits + (ub + g) * sc.slots + s) - m) : 0.f;
-        }
-#pragma unroll
-        for (int k = 1; k < PER; ++k) w[k] += w[k - 1];
-        float v = w[PER - 1];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const float x = __shfl_up_sync(0xffffffffu, v, o);
-          if (lane >= o) v += x;
-        }
-        const float excl = before + v - w[PER - 1];
-        int kl = PER;
-#pragma unroll
-        for (int k = PER - 1; k >= 0; --k)
-          if (s0 + PER * lane + k < s1 && excl + w[k] >= target) kl = k;
-        const unsigned hit = __ballot_sync(0xffffffffu, kl < PER);
-        const int hl = hit ? __ffs(hit) - 1 : 31;
-        const int kls = __shfl_sync(0xffffffffu, kl, hl);
-        // k* = the 1-based rank of the crossing slot (rounding guard: the block's last slot)
-        const int kstar = hit ? s0 + PER * hl + kls + 1 : s1;
-        J = 1 + warp_count_false(C - 1, [&](int r) { return eg[r] >= kstar; });
-      } else {
-        // past the head: cum(e_r) = EN + tail(e_r) at the cluster ends; the first cluster
-        // whose end reaches the target (ends are non-decreasing in rank)
-        const int r = xw ? warp_count_false(C, [&](int r) { return eg[r] > sc.N && windows_cum(EN, tail, xw, sc, eg[r]) >= target; })
-                         : warp_count_false(C, [&](int r) { return eg[r] > sc.N && EN + tail(eg[r]) >= target; });
-        J = r < C ? r + 1 : C;
       }
-    }
-    wstamp(3);
-    if (lane == 0) {
-      s_J[g] = J;
-      P.J[ub + g] = J;
-      double* f = P.fit + (ub + g) * 6;
-      f[0] = a; f[1] = b; f[2] = m; f[3] = W; f[4] = mu1; f[5] = mu2;
-    }
-    // mark this head's selected non-empty clusters (the OR over heads is the GQA union)
-    const int* ord = s_ord + (size_t)g * C;
-    __syncwarp();
-    for (int r = lane; r < J; r += 32) {
-      const int cid = ord[r];
-      if (s_off[cid + 1] > s_off[cid]) mask[cid] = 1;
+      wstamp(3);
+      if (lane == 0) {
+        s_J[g] = J;
+        P.J[ub + g] = J;
+        double* f = P.fit + (ub + g) * 6;
+        f[0] = a; f[1] = b; f[2] = m; f[3] = W; f[4] = mu1; f[5] = mu2;
+      }
+      // mark this head's selected non-empty clusters (the OR over heads is the GQA union)
+      const int* ord = s_ord + (size_t)g * C;
+      __syncwarp();
+      for (int r = lane; r < J; r += 32) {
+        const int cid = ord[r];
+        if (s_off[cid + 1] > s_off[cid]) mask[cid] = 1;
+      }
     }
     wstamp(4);
   }
   __syncthreads();
   stamp(3);
+  if (P.shard_mode == 2) {
+    pdl_launch_dependents();
+    return;
+  }
   // ---- S7: compact the union (cluster-id order) into the work list.  Thread t owns a
   // contiguous cluster chunk; one packed (tokens << 20 | clusters) block scan places it.
   {
@@ -726,260 +681,95 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
   if (tid == 0) tl_mark(P.tlog, 3, 2, u == 0);
 }
 
-// ------------------------------------------------------------------ S4-S7
-// mode 0: Alg. 1 selection; mode 1: sharded stage 2 (grid threshold); mode 2: sharded
-// stage 1 (fit only: local (m, theta_max) and cumulative mass at cluster ends).
-struct SelectParams {
-  const float* logits;
-  const int* order;
-  const int* ends;
-  const int* offsets;
-  const double* crit;
-  int n, C, G, units;
-  SampleConsts sc;
-  double p;
-  int mode;
-  const double* gmax;
-  const double* gmass;
-  double* fit;
-  int* J;
-  uint8_t* mask_acc;      // [units][C] union accumulator, all-zero between calls
-  uint8_t* umask;         // [units][C] debug copy of the union
-  int* ulist;             // [units][C] segment row starts
-  int* uprefix;           // [units][C+1]
-  long long* unit_prefix; // [units+1]
-  unsigned int* head_cnt; // [units]
-  unsigned int* unit_cnt; // [1]
-  double* cumend;
-  double* local_max;
-  int tail_len;           // recent-token tail per unit (counted in unit_prefix, as the fit kernel does)
-};
-
-__global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SelectParams P) {
-  extern __shared__ uint8_t smraw[];
-  const int C = P.C, G = P.G, n = P.n;
-  const SampleConsts sc = P.sc;
-  const int nex = sc.fallback ? n : sc.N;
-  double* epref = (double*)smraw;                       // [max(nex, 1)]
-  int* s_ends = (int*)(epref + (nex > 0 ? nex : 1));     // [C]
-  __shared__ double redd[32];
-  __shared__ float redf[32];
-  __shared__ int redi[32];
-  __shared__ long long sh_k;
-  __shared__ bool s_last;
-  __shared__ int s_totc, s_tott;
-  pdl_wait();
-  const int g = blockIdx.x, u = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
-  const size_t ug = (size_t)u * G + g;
-  const int* off = P.offsets + (size_t)u * (C + 1);
-  const int* ord = P.order + ug * C;
-  uint8_t* macc = P.mask_acc + (size_t)u * C;
-
-  if (P.mode == 1) {
-    // ---- sharded stage 2: theta* from the all-reduced mass vector
-    const double* gm = P.gmass + ug * (1 + TACTIC_SHARD_GRID_T);
-    const double thmax = P.gmax[ug * 2 + 1];
-    const double Wt = gm[0];
-    double thstar = -INFINITY;
-    if (P.p < 1.0) {
-      int tmin = INT_MAX;
-      for (int t = 1 + tid; t <= TACTIC_SHARD_GRID_T; t += nt)
-        if (gm[t] >= P.p * Wt) tmin = min(tmin, t);
-      tmin = -block_reduce<int, RED_MAX>(-tmin, redi);
-      if (tmin <= TACTIC_SHARD_GRID_T) thstar = thmax - (double)tmin * TACTIC_SHARD_GRID_STEP;
-    }
-    const double* cr = P.crit + ug * C;
-    const double isd = 1.0 / sqrt(128.0);
-    int cnt = 0;
-    for (int j = tid; j < C; j += nt) {
-      if ((off[j + 1] > off[j]) && (cr[j] * isd >= thstar)) {
-        macc[j] = 1;
-        ++cnt;
-      }
-    }
-    cnt = block_reduce<int, RED_SUM>(cnt, redi);
-    if (tid == 0) {
-      P.J[ug] = cnt;
-      double* f = P.fit + ug * 6;
-      f[0] = thstar; f[1] = Wt; f[2] = P.gmax[ug * 2]; f[3] = thmax; f[4] = 0; f[5] = 0;
-    }
-  } else {
-    for (int r = tid; r < C; r += nt) s_ends[r] = P.ends[ug * C + r];
-    const float* L = P.logits + ug * sc.slots;
-    // shift m = max sampled logit (reading 13)
-    float mf = -INFINITY;
-    for (int i = tid; i < sc.slots; i += nt) mf = fmaxf(mf, L[i]);
-    mf = block_reduce<float, RED_MAX>(mf, redf);
-    const double m = (double)mf;
-    // exact head weights e_i = exp(l_i - m), i <= nex, and their inclusive prefix
-    const int per = (nex + nt - 1) / nt;
-    const int b0 = tid * per;
-    double loc = 0.0;
-    for (int i = b0; i < b0 + per && i < nex; ++i) loc += exp((double)L[i] - m);
-    double run = block_exclusive_scan<double>(loc, redd, (double*)nullptr);
-    for (int i = b0; i < b0 + per && i < nex; ++i) {
-      run += exp((double)L[i] - m);
-      epref[i] = run;
-    }
-    __syncthreads();
-    const double EN = epref[nex - 1];
-    double a = 0.0, b = 0.0, mu1 = 0.0, mu2 = 0.0, W;
-    if (sc.fallback) {
-      W = EN;
-    } else {
-      const int W1 = 2 * sc.w + 1;
-      double s1 = 0.0, s2 = 0.0;
-      for (int i = tid; i < W1; i += nt) {
-        s1 += exp((double)L[sc.N + i] - m);
-        s2 += exp((double)L[sc.N + W1 + i] - m);
-      }
-      s1 = block_reduce<double, RED_SUM>(s1, redd);
-      s2 = block_reduce<double, RED_SUM>(s2, redd);
-      mu1 = s1 / (double)W1;
-      mu2 = s2 / (double)W1;
-      const double x1 = (double)sc.x1, x2 = (double)sc.x2;
-      a = (mu1 - mu2) * x1 * x2 / (x2 - x1);  // O8 / Alg. 1 l.4
-      b = mu1 - a / x1;
-      W = EN + tail_mass(a, b, sc.N, n);
-    }
-    if (tid == 0) {
-      double* f = P.fit + ug * 6;
-      f[0] = a; f[1] = b; f[2] = m; f[3] = W; f[4] = mu1; f[5] = mu2;
-    }
-    if (P.mode == 2) {
-      // sharded stage 1: cumulative estimated mass at every cluster end (local frame)
-      double* ce = P.cumend + ug * C;
-      for (int r = tid; r < C; r += nt) {
-        const long long e = s_ends[r];
-        double v;
-        if (e <= 0) v = 0.0;
-        else if (e <= nex) v = epref[e - 1];
-        else v = EN + tail_mass(a, b, sc.N, e);
-        ce[r] = v;
-      }
-      if (tid == 0) {
-        P.local_max[ug * 2] = m;
-        P.local_max[ug * 2 + 1] = P.crit[ug * C + ord[0]] / sqrt(128.0);
-      }
-      return;
-    }
-    long long kstar = (long long)n + 1;  // p >= 1: every rank (reading 15)
-    if (P.p < 1.0) {
-      const double target = P.p * W;
-      if (EN >= target) {
-        kstar = 1 + block_lower_bound(0, nex - 1, [&](long long i) { return epref[i] >= target; }, &sh_k);
-      } else {
-        const double aa = a, bb = b, en_ = EN;
-        const long long NN = sc.N;
-        kstar = block_lower_bound(NN + 1, n, [&](long long k) { return en_ + tail_mass(aa, bb, NN, k) >= target; },
-                                  &sh_k);
-      }
-    }
-    // J = #{r : s_r < k*}, s_r = e_{r-1}; mark the selected non-empty clusters
-    int cnt = 0;
-    for (int r = tid; r < C; r += nt) {
-      const long long sr = r ? s_ends[r - 1] : 0;
-      if (sr < kstar) {
-        ++cnt;
-        const int cid = ord[r];
-        if (off[cid + 1] > off[cid]) macc[cid] = 1;
-      }
-    }
-    cnt = block_reduce<int, RED_SUM>(cnt, redi);
-    if (tid == 0) P.J[ug] = cnt;
-  }
-
-  // ---- S7: the last head of the unit compacts the union (cluster-id order)
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(&P.head_cnt[u], 1u);
-    s_last = (prev == (unsigned)G - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  {
-    const int per = (C + nt - 1) / nt;
-    const int b0 = tid * per;
-    int lc = 0, lt = 0;
-    for (int j = b0; j < b0 + per && j < C; ++j)
-      if (__ldcg(macc + j)) { ++lc; lt += off[j + 1] - off[j]; }
-    int cbase = block_exclusive_scan<int>(lc, redi, &s_totc);
-    int tbase = block_exclusive_scan<int>(lt, redi, &s_tott);
-    int* ul = P.ulist + (size_t)u * C;
-    int* up = P.uprefix + (size_t)u * (C + 1);
-    uint8_t* um = P.umask + (size_t)u * C;
-    for (int j = b0; j < b0 + per && j < C; ++j) {
-      const uint8_t mk = __ldcg(macc + j);
-      um[j] = mk;
-      macc[j] = 0;  // reset the accumulator for the next call
-      if (mk) {
-        ul[cbase] = off[j];  // work-list segment = first layout row of the cluster
-        up[cbase] = tbase;
-        ++cbase;
-        tbase += off[j + 1] - off[j];
-      }
-    }
-    const int ucount = s_totc, tot = s_tott;
-    for (int k = ucount + tid; k <= C; k += nt) {
-      up[k] = tot;
-      if (k < C) ul[k] = 0;
-    }
-  }
-  if (tid == 0) P.head_cnt[u] = 0;
-  // ---- global token prefix over units: done by the last unit to finish
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(P.unit_cnt, 1u);
-    s_last = (prev == (unsigned)P.units - 1);
-  }
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    const int units = P.units;
-    const int per = (units + nt - 1) / nt;
-    const int b0 = tid * per;
-    long long loc = 0;
-    for (int v = b0; v < b0 + per && v < units; ++v) loc += __ldcg(P.uprefix + (size_t)v * (C + 1) + C) + P.tail_len;
-    long long run = block_exclusive_scan<long long>(loc, (long long*)redd, (long long*)nullptr);
-    for (int v = b0; v < b0 + per && v < units; ++v) {
-      P.unit_prefix[v] = run;
-      run += __ldcg(P.uprefix + (size_t)v * (C + 1) + C) + P.tail_len;
-    }
-    if (b0 < units && b0 + per >= units) P.unit_prefix[units] = run;
-    if (tid == 0) *P.unit_cnt = 0u;
-  }
-  pdl_launch_dependents();
-}
-
 // ------------------------------------------------------------------ sharded stage 1b
-__global__ void stage1b_kernel(const double* __restrict__ crit, const int* __restrict__ order,
-                               const double* __restrict__ cumend, const double* __restrict__ fit,
-                               const double* __restrict__ gmax, int C, int G, double* __restrict__ mass) {
+// One CTA per (unit, head) (reading 23): the shard's estimated mass of the clusters above
+// every grid point theta_t = theta_max - t / 16 (t = 1..T) of the GLOBAL frame, re-expressed
+// with the global shift: M_s(theta_t) = cum(e_{r_t}) exp(m_s - m) where r_t = #clusters
+// with crit / sqrt(d) >= theta_t (a rank prefix) and cum(e) = the exact prefix for e <= N,
+// E_N + tail(e) beyond (the stage-1 fit).  The criticalities in rank order, the end ranks
+// and the exact head prefix are staged in shared memory once (three round trips), so each
+// grid point is a binary search in shared memory.
+constexpr int S1B_THREADS = 256;
+__global__ void __launch_bounds__(S1B_THREADS) stage1b_kernel(const double* __restrict__ crit,
+                                                              const int* __restrict__ order,
+                                                              const int* __restrict__ ends,
+                                                              const float* __restrict__ logits,
+                                                              const double* __restrict__ fit,
+                                                              const double* __restrict__ en,
+                                                              const double* __restrict__ gmax, int C, int n,
+                                                              SampleConsts sc, double* __restrict__ mass) {
+  extern __shared__ __align__(16) uint8_t s1b[];
+  __shared__ float red[S1B_THREADS / 32];
   const size_t ug = blockIdx.x;
-  const double* cr = crit + ug * C;
-  const int* ord = order + ug * C;
-  const double* ce = cumend + ug * C;
+  const int tid = threadIdx.x;
+  double* th = (double*)s1b;             // [C] theta in rank order
+  int* se = (int*)(th + C);              // [C] end ranks
+  const int nex = sc.fallback ? n : sc.N;
+  float* hp = (float*)(se + C);          // [nex] inclusive exact-head prefix (local frame)
   const double ms = fit[ug * 6 + 2], Ws = fit[ug * 6 + 3];
+  const float a = (float)fit[ug * 6 + 0], b = (float)fit[ug * 6 + 1];
+  const float EN = (float)en[ug * 2];
   const double mg = gmax[ug * 2], thmax = gmax[ug * 2 + 1];
   const double f = exp(ms - mg);
   const double isd = 1.0 / sqrt(128.0);
+#pragma unroll 4
+  for (int r = tid; r < C; r += S1B_THREADS) {
+    th[r] = crit[ug * C + __ldcg(order + ug * C + r)] * isd;
+    se[r] = __ldcg(ends + ug * C + r);
+  }
+  // exact head weights exp(l - m_s) of ranks 1..nex: coalesced loads into shared memory,
+  // then the inclusive prefix over contiguous per-thread chunks
+  const float* lg = logits + ug * sc.slots;
+  const float msf = (float)ms;
+#pragma unroll 4
+  for (int k = tid; k < nex; k += S1B_THREADS) hp[k] = __expf(__ldcg(lg + k) - msf);
+  __syncthreads();
+  const int per = (nex + S1B_THREADS - 1) / S1B_THREADS, k0 = tid * per, k1 = min(nex, k0 + per);
+  float loc = 0.f;
+  for (int k = k0; k < k1; ++k) loc += hp[k];
+  float inc = loc;
+  const int lane = tid & 31, w = tid >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float x = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += x;
+  }
+  if (lane == 31) red[w] = inc;
+  __syncthreads();
+  float run = inc - loc;
+  for (int i = 0; i < w; ++i) run += red[i];
+  for (int k = k0; k < k1; ++k) {
+    run += hp[k];
+    hp[k] = run;
+  }
+  __syncthreads();
+  TailF tail = {0.f, 0.f, 1, 0};
+  if (!sc.fallback) tail = make_tail_f(a, b, sc.N, n);
   double* out = mass + ug * (1 + TACTIC_SHARD_GRID_T);
-  for (int t = threadIdx.x; t <= TACTIC_SHARD_GRID_T; t += blockDim.x) {
+  for (int t = tid; t <= TACTIC_SHARD_GRID_T; t += S1B_THREADS) {
     if (t == 0) {
       out[0] = Ws * f;
       continue;
     }
-    const double th = thmax - (double)t * TACTIC_SHARD_GRID_STEP;
-    int lo = 0, hi = C;  // number of clusters (a prefix of the order) with theta >= th
+    const double tht = thmax - (double)t * TACTIC_SHARD_GRID_STEP;
+    int lo = 0, hi = C;  // r_t: clusters (a prefix of the order) with theta >= tht
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (cr[ord[mid]] * isd >= th) lo = mid + 1; else hi = mid;
+      if (th[mid] >= tht) lo = mid + 1;
+      else hi = mid;
     }
-    out[t] = lo > 0 ? ce[lo - 1] * f : 0.0;
+    double cum = 0.0;
+    if (lo > 0) {
+      const int e = se[lo - 1];
+      cum = e <= 0 ? 0.0 : (e <= nex ? (double)hp[e - 1] : (double)(EN + tail(e)));
+    }
+    out[t] = cum * f;
   }
+}
+
+size_t stage1b_smem_bytes(const tactic_index_s* x) {
+  const int nex = x->sc.fallback ? x->n : x->sc.N;
+  return (size_t)x->C * 12 + (size_t)(nex > 0 ? nex : 1) * 4 + 16;
 }
 
 // ------------------------------------------------------------------ launchers
@@ -1035,11 +825,6 @@ size_t fit_smem_bytes(const tactic_index_s* x, bool windows_exact) {
          (windows_exact ? (size_t)x->G * ((((size_t)2 * (2 * x->sc.w + 1) + 6) & ~(size_t)3) + 4) * 4 + 16 : 0);
 }
 
-size_t select_smem_bytes(const tactic_index_s* x) {
-  const int nex = x->sc.fallback ? x->n : x->sc.N;
-  return (size_t)(nex > 0 ? nex : 1) * 8 + (size_t)x->C * 4 + 16;
-}
-
 cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
   tactic_index_s* x = a.idx;
   FitParams P = {};
@@ -1067,6 +852,12 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
   P.tail_len = x->tail_len;
   P.fixed_budget = x->fixed_budget;
   P.windows_exact = (x->options & 1u) ? 1 : 0;
+  P.shard_mode = a.mode;  // 0 Alg. 1, 1 sharded stage 2, 2 sharded stage 1
+  P.crit = x->crit;
+  P.gmax = a.gmax;
+  P.gmass = a.gmass;
+  P.local_max = a.local_max;
+  P.en_out = x->stage;
   cudaLaunchAttribute attr[1];
   const size_t smem = fit_smem_bytes(x, P.windows_exact != 0);
   cudaError_t e = ensure_smem((const void*)fit_unit_kernel, smem);
@@ -1075,47 +866,13 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
   return cudaLaunchKernelEx(&cfg, fit_unit_kernel, P);
 }
 
-cudaError_t launch_select(const SelArgs& a, cudaStream_t s, bool pdl) {
-  tactic_index_s* x = a.idx;
-  const size_t smem = select_smem_bytes(x);
-  cudaError_t e = ensure_smem((const void*)select_kernel, smem);
-  if (e != cudaSuccess) return e;
-  SelectParams P = {};
-  P.logits = x->logits;
-  P.order = x->order;
-  P.ends = x->ends;
-  P.offsets = x->offsets;
-  P.crit = x->crit;
-  P.n = x->n;
-  P.C = x->C;
-  P.G = x->G;
-  P.units = x->units;
-  P.sc = x->sc;
-  P.p = a.p;
-  P.mode = a.mode;
-  P.gmax = a.gmax;
-  P.gmass = a.gmass;
-  P.fit = x->fit;
-  P.J = x->J;
-  P.mask_acc = x->mask_acc;
-  P.umask = x->umask;
-  P.ulist = x->union_list;
-  P.uprefix = x->union_prefix;
-  P.unit_prefix = x->unit_prefix;
-  P.head_cnt = x->head_cnt;
-  P.unit_cnt = x->counter;
-  P.cumend = x->cumend;
-  P.local_max = a.local_max;
-  P.tail_len = x->tail_len;
-  cudaLaunchAttribute attr[1];
-  auto cfg = make_cfg(dim3(x->G, x->units), dim3(SEL_THREADS), smem, s, pdl, attr);
-  return cudaLaunchKernelEx(&cfg, select_kernel, P);
-}
-
 cudaError_t launch_stage1b(const SelArgs& a, cudaStream_t s) {
   tactic_index_s* x = a.idx;
-  stage1b_kernel<<<x->units * x->G, 256, 0, s>>>(x->crit, x->order, x->cumend, x->fit, a.gmax, x->C, x->G,
-                                                  a.mass_out);
+  const size_t smem = stage1b_smem_bytes(x);
+  cudaError_t e = ensure_smem((const void*)stage1b_kernel, smem);
+  if (e != cudaSuccess) return e;
+  stage1b_kernel<<<x->units * x->G, S1B_THREADS, smem, s>>>(x->crit, x->order, x->ends, x->logits, x->fit, x->stage,
+                                                             a.gmax, x->C, x->n, x->sc, a.mass_out);
   return cudaGetLastError();
 }
 

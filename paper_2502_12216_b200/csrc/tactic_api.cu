@@ -240,7 +240,6 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, const ta
     x->ends = A.get<int>(U * G * C);
     x->logits = A.get<float>(U * G * (size_t)x->sc.slots);
     x->fit = A.get<double>(U * G * 6);
-    x->cumend = A.get<double>(U * G * C);
     x->J = A.get<int>(U * G);
     x->umask = A.get<uint8_t>(U * C);
     x->union_list = A.get<int>(U * C + 4);          // +4: 16-byte bulk reads of the whole list
@@ -258,8 +257,6 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, const ta
     x->head_cnt2 = A.get<int>(U * G);
     x->rowmap = A.get<int>(U * G * (size_t)x->sc.slots);
     x->summ = A.get<float>(U * G * (size_t)sample_blocks(x->sc.slots) * 4);
-    x->mask_acc = A.get<uint8_t>(U * C);
-    x->head_cnt = A.get<unsigned int>(U);
   };
   carve();
   if (A.reserve()) carve();
@@ -280,8 +277,6 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, const ta
   cudaMemset(x->counter, 0, sizeof(unsigned int));
   cudaMemset(x->unit_cnt, 0, U * sizeof(int));
   cudaMemset(x->head_cnt2, 0, U * G * sizeof(int));
-  cudaMemset(x->mask_acc, 0, U * C);
-  cudaMemset(x->head_cnt, 0, U * sizeof(unsigned int));
   cudaMemset(x->order, 0, U * G * C * sizeof(int));  // valid cluster ids before the first decode
 
   cudaMemset(x->ends, 0, U * G * C * sizeof(int));
@@ -759,22 +754,11 @@ static tactic_status_t run_selection(const void* q, tactic_index_t idx, double p
   // a caller's preceding kernel produces q.  The later kernels overlap their prologues
   // with the previous kernel's tail through programmatic dependent launch.
   const bool pdl = true;
-  if (mode != 1) {
-    CK(launch_score_rank(sa.q, idx, s, false));  // S1, S2, S3 (+ sampled-slot row map)
-    CK(launch_sample(sa, s, pdl));             // S4 (+ per-block fit summaries)
-  } else {
-    CK(launch_score(sa, s, false));            // S1 only (sharded stage 2)
-  }
-  if (mode == 0) {
-    CK(launch_fit(sa, s, pdl));                  // S5-S7
-    idx->lists_valid = true;
-  } else {
-    if (select_smem_bytes(idx) > smem_optin_limit())
-      return fail(TACTIC_ERR_UNSUPPORTED, "sharded selection: exact head of %d ranks exceeds shared memory",
-                  idx->sc.fallback ? idx->n : idx->sc.N);
-    CK(launch_select(sa, s, pdl));               // sharded stage rules
-    if (mode == 1) idx->lists_valid = true;
-  }
+  CK(launch_score_rank(sa.q, idx, s, false));    // S1, S2, S3 (+ sampled-slot row map)
+  CK(launch_sample(sa, s, pdl));                 // S4 (+ per-block fit summaries)
+  // mode 0: Alg. 1 selection; mode 2: sharded stage 1 (the fit only, same kernel)
+  CK(launch_fit(sa, s, pdl));                    // S5-S7
+  if (mode == 0) idx->lists_valid = true;
   return TACTIC_OK;
 }
 
@@ -1090,6 +1074,9 @@ tactic_status_t tactic_decode_stage1(const void* q, tactic_index_t idx, double* 
 
 tactic_status_t tactic_decode_stage1b(tactic_index_t idx, const double* global_max, double* mass, void* stream) {
   if (!idx || !global_max || !mass) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (stage1b_smem_bytes(idx) > smem_optin_limit())
+    return fail(TACTIC_ERR_UNSUPPORTED, "sharded stage 1b: exact head of %d ranks exceeds shared memory",
+                idx->sc.fallback ? idx->n : idx->sc.N);
   SelArgs sa = {};
   sa.idx = idx;
   sa.gmax = global_max;
@@ -1112,7 +1099,9 @@ tactic_status_t tactic_decode_stage2(const void* q, tactic_index_t idx, float p,
   sa.mode = 1;
   sa.gmax = global_max;
   sa.gmass = global_mass;
-  CK(launch_select(sa, s, true));
+  // stage 2 reuses stage 1's criticalities and order (the same q on the same index)
+  CK(launch_fit(sa, s, false));                  // theta* rule + union (fit kernel, mode 1)
+  idx->lists_valid = true;
   return run_attention(q, idx, false, s, nullptr, o_part, lse_part);
 }
 

@@ -27,7 +27,7 @@ from paper_2502_12216_b200 import tactic as T  # noqa: E402
 if args.c3:
     import bench  # noqa: E402
     G, n, C = 4, 32768, 256
-    L = bench.make_layers([9000], torch.device("cuda", 0), B=64, Hkv=8, n=n)[0]
+    L = bench.make_layers([9000], torch.device("cuda", 0), [(b, h) for b in range(64) for h in range(8)], n=n)[0]
     Kd, Vd, qd = L["K"], L["V"], L["q"]
     idx = T.build_index(Kd, Vd, C, 10, group_size=G, seed=9000)
 else:

@@ -13,7 +13,7 @@ import bench  # noqa: E402
 from paper_2502_12216_b200 import tactic as T  # noqa: E402
 
 dev = torch.device("cuda", 0)
-L = bench.make_layers([0], dev)[0]
+L = bench.make_layers([0], dev, [(0, h) for h in range(8)])[0]
 idx = T.build_index(L["K"], L["V"], 1024, 4, group_size=4)
 torch.cuda.synchronize()
 print("ok", idx.info()["units"])

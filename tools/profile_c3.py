@@ -14,7 +14,7 @@ import bench  # noqa: E402
 from paper_2502_12216_b200 import tactic as T  # noqa: E402
 
 dev = torch.device("cuda", 0)
-L = bench.make_layers([9000], dev, B=64, Hkv=8, n=32768)[0]
+L = bench.make_layers([9000], dev, [(b, h) for b in range(64) for h in range(8)], n=32768)[0]
 idx = T.build_index(L["K"], L["V"], 256, 10, group_size=4, seed=9000)
 out = torch.empty_like(L["q"])
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)

@@ -130,7 +130,7 @@ if __name__ == "__main__":
     ap.add_argument("--p", type=float, nargs="+", default=[0.5, 0.9])
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
-    for L in bench.make_layers(list(range(a.layers)), dev):
+    for L in bench.make_layers(list(range(a.layers)), dev, [(0, h) for h in range(8)]):
         idx = T.build_index(L["K"], L["V"], 1024, 10, group_size=4)
         ex = idx.export()
         sizes = np.stack([np.bincount(ex["assign"][u], minlength=1024) for u in range(idx.units)])
