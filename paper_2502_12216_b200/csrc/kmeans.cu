@@ -515,13 +515,29 @@ __global__ void km_inertia_kernel(const KmArgs a, double* __restrict__ part) {
   if (j >= a.C) return;
   const int* off = a.offsets + (size_t)u * (a.C + 1);
   const float4 c = *reinterpret_cast<const float4*>(a.cent + ((size_t)u * a.C + j) * 128 + lane * 4);
+  // the cluster's member rows in order, 8 rows' loads in flight per warp (a lone dependent
+  // walk ran at ~0.3 TB/s); per-row sums added in row order, so the result is deterministic
   double s = 0.0;
-  for (int r = off[j]; r < off[j + 1]; ++r) {
-    // dims 4*lane..4*lane+3 live in logical chunk lane/2, half lane%2
-    const __nv_bfloat16* k = a.Kp + ((size_t)u * a.n + r) * 128 + swz_chunk(lane >> 1, r) * 8 + (lane & 1) * 4;
-    const double d0 = (double)__bfloat162float(k[0]) - c.x, d1 = (double)__bfloat162float(k[1]) - c.y;
-    const double d2 = (double)__bfloat162float(k[2]) - c.z, d3 = (double)__bfloat162float(k[3]) - c.w;
-    s += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+  const int r0 = off[j], r1 = off[j + 1];
+  for (int rb = r0; rb < r1; rb += 8) {
+    uint2 raw[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = rb + i;
+      // dims 4*lane..4*lane+3 live in logical chunk lane/2, half lane%2
+      raw[i] = r < r1 ? *reinterpret_cast<const uint2*>(a.Kp + ((size_t)u * a.n + r) * 128 +
+                                                        swz_chunk(lane >> 1, r) * 8 + (lane & 1) * 4)
+                      : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (rb + i >= r1) break;
+      const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&raw[i]);
+      const float2 x0 = __bfloat1622float2(k2[0]), x1 = __bfloat1622float2(k2[1]);
+      const double d0 = (double)x0.x - c.x, d1 = (double)x0.y - c.y;
+      const double d2 = (double)x1.x - c.z, d3 = (double)x1.y - c.w;
+      s += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+    }
   }
   s = warp_sum_d(s);
   if (lane == 0) part[(size_t)u * a.C + j] = s;

@@ -15,5 +15,6 @@ from paper_2502_12216_b200 import tactic as T  # noqa: E402
 dev = torch.device("cuda", 0)
 L = bench.make_layers([0], dev, [(0, h) for h in range(8)])[0]
 idx = T.build_index(L["K"], L["V"], 1024, 4, group_size=4)
+ex = idx.export()  # (runs the inertia kernel)
 torch.cuda.synchronize()
 print("ok", idx.info()["units"])
