@@ -651,3 +651,23 @@ def test_windows_exact_variant_weights_and_total():
     assert b["W"] - a["W"] == pytest.approx(float(b["what"][win].sum() - a["what"][win].sum()), rel=1e-9, abs=1e-12)
     Js = [O.decode_head(q, idx, p, windows_exact=True)["J"] for p in (0.5, 0.8, 0.9, 0.95, 0.99)]
     assert Js == sorted(Js)
+
+
+# ---------------------------------------------------------------------------- frozen input recipe
+def test_recipe_regression_pins():
+    """The frozen recipe (tactic-synth-v1) and the oracle's selection on it:
+    per-head selected clusters and tokens and the GQA union at C1 and one 32K unit must stay
+    exactly those recorded in tests/golden/recipe_regression.json (written by
+    tools/make_recipe_golden.py, which calls only oracle/ and synth/) -- a change to the
+    generator or to the oracle's arithmetic shows up here first."""
+    import json
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import make_recipe_golden as M
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "recipe_regression.json")))
+    assert gold["recipe"] == "tactic-synth-v1"
+    for g in gold["cases"]:
+        got = M.compute(g["case"])
+        assert got["inertia"] == pytest.approx(g["inertia"], rel=1e-12)
+        assert got["p"] == g["p"], g["case"]["name"]
