@@ -287,13 +287,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < ATT_STAGES; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], ATT_CWARPS);
+      mbar_init(&empty[i], ATT_CWARPS * 32);  // every consumer lane releases its own reads
     }
     mbar_init(mbar, 1);
     mbar_init(mbar + 1, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&ep_full[i], ATT_CWARPS);
-      mbar_init(&ep_empty[i], 1);
+      mbar_init(&ep_full[i], ATT_CWARPS * 32);  // every writer lane publishes its own stores
+      mbar_init(&ep_empty[i], 32);
     }
     fence_barrier_init();
   }
@@ -612,8 +612,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             make_float4(of.x * il, of.y * il, of.z * il, of.w * il);
         if (lane == 0) a.part_lse[slot * G + g] = none ? -INFINITY : (mf + log2f(lf)) * 0.6931471805599453f;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ep_empty[b]);
+      mbar_arrive(&ep_empty[b]);
       // arrival: __syncwarp orders the lanes' partial stores before lane 0's gpu-scope
       // release; the last arrival acquires, and __syncwarp passes that on to the lanes
       const long long us = DENSE ? (long long)u * a.n : vpre(u);
@@ -724,8 +723,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         mma_bf16_16816(o[mt], af, b0, b1);
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
+    mbar_arrive(&empty[stage]);
     if (++stage == nst) { stage = 0; phase ^= 1; }
 
     if (md.flags & FLAG_LAST) {
@@ -760,8 +758,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       }
       if (!unit_mode) {
         if (ct == 0) ep_meta[ep_b] = md.unit;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ep_full[ep_b]);
+        mbar_arrive(&ep_full[ep_b]);
         ++ep_n;
       }
      if (unit_mode) {
@@ -923,8 +920,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     const int b = ep_n & 1;
     mbar_wait(&ep_empty[b], (uint32_t)(((ep_n >> 1) & 1) ^ 1));
     if (ct == 0) ep_meta[b] = -1;
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&ep_full[b]);
+    mbar_arrive(&ep_full[b]);
   }
   if (ct == 0) stamp(34);
   if (a.tlog && ct == 0 && 2 * cta + 1 < 512) {

@@ -225,12 +225,12 @@ __global__ void __launch_bounds__(FZ_THREADS, 1) decode_fused_kernel(const Fused
   // ------------------------------------------------------------------ prologue
   if (tid == 0) {
     for (int i = 0; i < FZ_SST; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], FZ_CW);
+      mbar_init(&s_full[i], 32);          // every producer lane publishes its slot metadata
+      mbar_init(&s_empty[i], FZ_CW * 32);  // every consumer lane releases its own reads
     }
     for (int i = 0; i < FZ_AST; ++i) {
       mbar_init(&s_afull[i], 1);
-      mbar_init(&s_aempty[i], FZ_CW);
+      mbar_init(&s_aempty[i], FZ_CW * 32);
     }
     mbar_init(&s_cbar, 1);
     mbar_init(&s_rbar, 1);
@@ -528,11 +528,12 @@ __global__ void __launch_bounds__(FZ_THREADS, 1) decode_fused_kernel(const Fused
           }
         }
       }
-      __syncwarp();
       if (lane == 0) {
         s_meta[stage].mask = mask;
         s_meta[stage].flags = 0;
         mbar_arrive_expect_tx(&s_full[stage], bytes);
+      } else {
+        mbar_arrive(&s_full[stage]);
       }
       if (nst_dbg++ == 0) stamp(10);
       if (++stage == NSS) {
@@ -544,8 +545,8 @@ __global__ void __launch_bounds__(FZ_THREADS, 1) decode_fused_kernel(const Fused
     if (lane == 0) {
       s_meta[stage].mask = 0;
       s_meta[stage].flags = FZ_END;
-      mbar_arrive(&s_full[stage]);
     }
+    mbar_arrive(&s_full[stage]);
     if (stamp_on) a.tlog[3011] = (unsigned long long)nst_dbg;
   } else if (warp <= FZ_CW) {
     // consumers: 16 slots each; S^T(16 rows x 8 heads) = K q^T on mma.sync
@@ -610,8 +611,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1) decode_fused_kernel(const Fused
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[stage]);
+      mbar_arrive(&s_empty[stage]);
       if (++stage == NSS) {
         stage = 0;
         ph ^= 1;
@@ -1007,8 +1007,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1) decode_fused_kernel(const Fused
           mma_bf16_16816(o[mt], af, b0, b1);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_aempty[stage]);
+      mbar_arrive(&s_aempty[stage]);
       if (++stage == FZ_AST) {
         stage = 0;
         ph ^= 1;

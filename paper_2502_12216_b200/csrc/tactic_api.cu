@@ -963,11 +963,15 @@ tactic_status_t tactic_decode_fixed_budget(const void* q, tactic_index_t idx, in
   tactic_status_t st;
   if (per_head && (st = per_head_checks(idx))) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  idx->fixed_budget = budget;  // read by the fit kernel's launcher only
-  st = run_selection(q, idx, 0.5, 0, s, nullptr, nullptr, nullptr);
+  int M = 0, R = 0;
+  idx->fixed_budget = budget;  // read by the fit kernel's / cluster decode's launcher only
+  const bool fused = !per_head && fused_plan(idx, &M, &R);
+  st = fused ? run_fused(q, idx, 0.5f, M, R, s, out, nullptr, nullptr)
+             : run_selection(q, idx, 0.5, 0, s, nullptr, nullptr, nullptr);
   idx->fixed_budget = 0;
   if (st) return st;
-  if (per_head) {
+  if (fused) {
+  } else if (per_head) {
     if ((st = per_head_attention(q, idx, out, s))) return st;
   } else if ((st = run_attention(q, idx, false, s, out, nullptr, nullptr))) {
     return st;

@@ -424,15 +424,17 @@ def _tail_tokens(units, t, seed):
     return kt, vt
 
 
+@pytest.mark.parametrize("path", ["multi", "fused"])
 @pytest.mark.parametrize("B,H,n,C", [(1, 2, 4096, 64),     # unit-aligned split
                                      (12, 8, 2048, 32)])   # global token split (96 units)
-def test_tail_append_decode_parity(T, B, H, n, C):
+def test_tail_append_decode_parity(T, B, H, n, C, path):
     """Appended tokens (two appends) are attended in full after the selected clusters;
     the selection itself is unchanged (it ranks the clustered tokens only)."""
     G = 4
     K, V, q = _layer(B, H, G, n, 700 + B)
     cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, B)
     index = _import(T, K, V, cents, asg, G)
+    T.set_options(index, T.OPT_CLUSTER_DECODE if path == "fused" else 0)
     units = B * H
     kt1, vt1 = _tail_tokens(units, 21, 1)
     kt2, vt2 = _tail_tokens(units, 44, 2)
@@ -565,11 +567,13 @@ def test_per_head_loading_matches_oracle_own_set_attention(T):
 
 
 # ----------------------------------------------------------------------------- NEXT 4: fixed-budget baseline
-def test_fixed_budget_selection_and_output(T):
+@pytest.mark.parametrize("path", ["multi", "fused"])
+def test_fixed_budget_selection_and_output(T, path):
     G, n, C = 4, 8192, 128
     K, V, q = _layer(1, 2, G, n, 51)
     cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, 51)
     index = _import(T, K, V, cents, asg, G)
+    T.set_options(index, T.OPT_CLUSTER_DECODE if path == "fused" else 0)
     qd = dev_bf16(q)
     for budget in (100, 700):
         out, J = T.decode_fixed_budget(qd, index, budget)
