@@ -280,10 +280,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) tl_mark(a.tlog, 4, 0, blockIdx.x == 0);
-  // zero the stage buffers once: never-written slots must hold finite values (0 * NaN)
+  // zero the V halves of the stages once: a never-written V slot meets P = 0, and 0 * NaN
+  // would poison O (a never-written K slot only feeds a logit that the mask replaces)
   const int nst = (!DENSE && a.unit_split != 0) ? ATT_LIST_STAGES : ATT_STAGES;  // stages in use
-  for (int i = threadIdx.x; i < nst * ATT_STAGE_BYTES / 16; i += ATT_THREADS)
-    reinterpret_cast<uint4*>(stages)[i] = make_uint4(0, 0, 0, 0);
+  constexpr int HALF16 = ATT_STAGE_BYTES / 32;  // 16-byte words per K or V half
+  for (int i = threadIdx.x; i < nst * HALF16; i += ATT_THREADS)
+    reinterpret_cast<uint4*>(stages + (i / HALF16) * ATT_STAGE_BYTES + ATT_STAGE_BYTES / 2)[i % HALF16] =
+        make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     for (int i = 0; i < ATT_STAGES; ++i) {
       mbar_init(&full[i], 1);
