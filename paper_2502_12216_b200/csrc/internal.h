@@ -259,11 +259,13 @@ struct KmArgs {
   uint8_t* bimg;                   // [units][Cpad/128][64 KB]
   float* cnorm;                    // [units][Cpad]
   int* blk_counts;                 // [units][nblk][C]
+  int* col_tot;                    // [units][C] cluster sizes (km_scan -> km_scatter)
   int* changed;                    // [units]
   int* converged;                  // [units]
 };
 cudaError_t km_init_centroids(const KmArgs& a, const int* init_dev, cudaStream_t s);
-cudaError_t km_assign(const KmArgs& a, int iter, bool simt, cudaStream_t s);
+// tmK: 4-D map of the caller's K ([B][Hkv][n][128], box 64 dims x 128 rows, SWIZZLE_128B)
+cudaError_t km_assign(const KmArgs& a, const CUtensorMap* tmK, int iter, bool simt, cudaStream_t s);
 cudaError_t km_count_scan_scatter(const KmArgs& a, int iter, cudaStream_t s);
 cudaError_t km_update(const KmArgs& a, int iter, cudaStream_t s);
 cudaError_t km_finalize(const KmArgs& a, cudaStream_t s);

@@ -326,6 +326,37 @@ static tactic_status_t check_device() {
   return TACTIC_OK;
 }
 
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t get_encode() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled_t)p;
+  }
+  return fn;
+}
+
+static tactic_status_t make_kv_map(CUtensorMap* m, const void* base, const Resolved& r, int box_rows) {
+  PFN_encodeTiled_t enc = get_encode();
+  if (!enc) return fail(TACTIC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {128, (cuuint64_t)r.n, (cuuint64_t)r.Hkv, (cuuint64_t)r.B};
+  cuuint64_t strides[3] = {(cuuint64_t)r.sn * 2, (cuuint64_t)r.sh * 2, (cuuint64_t)r.sb * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_rows, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult cr = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(TACTIC_ERR_SHAPE, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  return TACTIC_OK;
+}
+
+
 // Build / import share everything after the centroids are known.
 static tactic_status_t build_common(const void* K, const void* V, const tactic_kv_desc_t* kv, int32_t C,
                                     int32_t iters, const tactic_params_t* params, cudaStream_t s,
@@ -385,7 +416,8 @@ static tactic_status_t build_common(const void* K, const void* V, const tactic_k
   const bool build = host_cent == nullptr;
   if ((e = cudaMallocAsync((void**)&a.bimg, (size_t)units * a.Cpad / 128 * 65536, s))) return bail(cuda_fail(e, "scratch"));
   if ((e = cudaMallocAsync((void**)&a.cnorm, (size_t)units * a.Cpad * 4, s))) return bail(cuda_fail(e, "scratch"));
-  if ((e = cudaMallocAsync((void**)&a.blk_counts, (size_t)units * a.nblk * C * 4, s))) return bail(cuda_fail(e, "scratch"));
+  if ((e = cudaMallocAsync((void**)&a.blk_counts, (size_t)units * (a.nblk + 1) * C * 4, s))) return bail(cuda_fail(e, "scratch"));
+  a.col_tot = a.blk_counts + (size_t)units * a.nblk * C;
   if ((e = cudaMallocAsync((void**)&a.changed, (size_t)(iters + 2) * units * 4, s))) return bail(cuda_fail(e, "scratch"));
   if ((e = cudaMallocAsync((void**)&a.converged, (size_t)units * 4, s))) return bail(cuda_fail(e, "scratch"));
   if ((e = cudaMallocAsync((void**)&d_init, (size_t)units * C * 4, s))) return bail(cuda_fail(e, "scratch"));
@@ -424,6 +456,12 @@ static tactic_status_t build_common(const void* K, const void* V, const tactic_k
     }
   }
   if (build) {
+    CUtensorMap tmK;  // the assignment GEMM's A tiles (128 keys) straight from the caller's K
+    if ((st = make_kv_map(&tmK, K, r, 128))) {
+      free_scratch();
+      cudaStreamSynchronize(s);
+      return bail(st);
+    }
     std::vector<int> init((size_t)units * C);
     for (int u = 0; u < units; ++u) {
       if (P.init_indices) {
@@ -444,7 +482,7 @@ static tactic_status_t build_common(const void* K, const void* V, const tactic_k
     CKB(km_init_centroids(a, d_init, s));
     const bool simt = (P.flags & TACTIC_FLAG_KMEANS_SIMT) != 0;
     for (int it = 1; it <= iters; ++it) {
-      CKB(km_assign(a, it, simt, s));
+      CKB(km_assign(a, &tmK, it, simt, s));
       CKB(km_count_scan_scatter(a, it, s));
       CKB(km_update(a, it, s));
     }
@@ -995,36 +1033,6 @@ tactic_status_t tactic_dense_workspace_size(const tactic_kv_desc_t* kv, int32_t 
   return TACTIC_OK;
 }
 
-typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static PFN_encodeTiled_t get_encode() {
-  static PFN_encodeTiled_t fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = (PFN_encodeTiled_t)p;
-  }
-  return fn;
-}
-
-static tactic_status_t make_kv_map(CUtensorMap* m, const void* base, const Resolved& r) {
-  PFN_encodeTiled_t enc = get_encode();
-  if (!enc) return fail(TACTIC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[4] = {128, (cuuint64_t)r.n, (cuuint64_t)r.Hkv, (cuuint64_t)r.B};
-  cuuint64_t strides[3] = {(cuuint64_t)r.sn * 2, (cuuint64_t)r.sh * 2, (cuuint64_t)r.sb * 2};
-  cuuint32_t box[4] = {64, 64, 1, 1};
-  cuuint32_t es[4] = {1, 1, 1, 1};
-  CUresult cr = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return fail(TACTIC_ERR_SHAPE, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
-  return TACTIC_OK;
-}
-
 tactic_status_t tactic_dense_decode(const void* q, const void* K, const void* V, const tactic_kv_desc_t* kv,
                                     void* out, float* lse, void* workspace, size_t workspace_bytes,
                                     int32_t num_ctas, void* stream) {
@@ -1039,8 +1047,8 @@ tactic_status_t tactic_dense_decode(const void* q, const void* K, const void* V,
   if (workspace_bytes < need) return fail(TACTIC_ERR_INVALID_ARGUMENT, "workspace too small (%zu < %zu)", workspace_bytes, need);
   if ((uintptr_t)K % 16 || (uintptr_t)V % 16) return fail(TACTIC_ERR_SHAPE, "K and V must be 16-byte aligned");
   CUtensorMap mk, mv;
-  if ((st = make_kv_map(&mk, K, r))) return st;
-  if ((st = make_kv_map(&mv, V, r))) return st;
+  if ((st = make_kv_map(&mk, K, r, 64))) return st;
+  if ((st = make_kv_map(&mv, V, r, 64))) return st;
   const size_t units = (size_t)r.B * r.Hkv;
   const size_t slots = (size_t)P + units;
   float* part_o = (float*)workspace;
