@@ -107,6 +107,11 @@ typedef struct {
                                    (TACTIC_OPT_CLUSTER_DECODE, see tactic_decode); 0 = this
                                    index decodes through the multi-kernel chain          */
   int64_t device_bytes;         /* bytes the index holds on the device                   */
+  float build_gpu_ms;           /* device time of the build's kernels (first k-means launch
+                                   to the end of the layout), from CUDA events the library
+                                   records on the build stream -- host work (allocation,
+                                   launch) excluded; waits for the build to finish; -1 if
+                                   unavailable                                           */
 } tactic_index_info_t;
 
 /* ---------------------------------------------------------------------------------------

@@ -114,6 +114,7 @@ struct tactic_index_s {
   __nv_bfloat16* q_stage = nullptr;  // [units][G][128] (host-buffer decode)
   __nv_bfloat16* o_stage = nullptr;
   long long device_bytes = 0;
+  cudaEvent_t ev_build[2] = {nullptr, nullptr};  // around the build's kernels (info.build_gpu_ms)
   int fz_checked_m = 0;           // one-launch decode: 0 unchecked, -1 no cluster shape fits, else M
   bool lists_valid = false;      // a p < 1 selection has been enqueued (attention-only needs its lists)
   // tactic_decode_host: the H2D copy, the decode and the D2H copy captured as one CUDA graph,

@@ -220,19 +220,24 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t acc = tt & 1;
         mbar_wait(&tfull[acc], (tt >> 1) & 1);
         tc_fence_after();
-        // the tile's 128 columns in one TMEM round trip (4 loads, one wait); the accumulator
-        // is handed back to the MMA issuer before the argmin, so the epilogue's arithmetic
-        // overlaps the next MMAs into this buffer
+        // the tile's 128 columns in two TMEM round trips: columns 64..127 load while the
+        // argmin runs over 0..63, and the accumulator goes back to the MMA issuer as soon as
+        // the second load has landed (before the rest of the argmin)
         uint32_t v[4][32];
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch)
-          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * (128 * TC_KA) + at * 128 + ch * 32, v[ch]);
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * (128 * TC_KA) + at * 128;
+        tmem_ld32(taddr, v[0]);
+        tmem_ld32(taddr + 32, v[1]);
         tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        tmem_ld32(taddr + 64, v[2]);
+        tmem_ld32(taddr + 96, v[3]);
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
+          if (ch == 2) {
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
           const int jb = t * 128 + ch * 32;
           float cv[32];
 #pragma unroll

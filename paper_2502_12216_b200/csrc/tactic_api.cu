@@ -192,6 +192,8 @@ struct tactic_index_priv {
 };
 
 static void free_index(tactic_index_s* x, std::vector<void*>* ptrs) {
+  for (cudaEvent_t e : x->ev_build)
+    if (e) cudaEventDestroy(e);
   if (x->hg_exec) cudaGraphExecDestroy(x->hg_exec);
   if (x->hg_stream) cudaStreamDestroy(x->hg_stream);
   if (ptrs)
@@ -422,6 +424,11 @@ static tactic_status_t build_common(const void* K, const void* V, const tactic_k
   if ((e = cudaMallocAsync((void**)&a.converged, (size_t)units * 4, s))) return bail(cuda_fail(e, "scratch"));
   if ((e = cudaMallocAsync((void**)&d_init, (size_t)units * C * 4, s))) return bail(cuda_fail(e, "scratch"));
   if ((e = cudaMallocAsync((void**)&d_flag, 4, s))) return bail(cuda_fail(e, "scratch"));
+  if (cudaEventCreate(&x->ev_build[0]) != cudaSuccess || cudaEventCreate(&x->ev_build[1]) != cudaSuccess) {
+    cudaGetLastError();  // timing only: the build goes on without it
+    for (cudaEvent_t& ev : x->ev_build)
+      if (ev) { cudaEventDestroy(ev); ev = nullptr; }
+  }
   cudaMemsetAsync(a.changed, 0, (size_t)(iters + 2) * units * 4, s);
   cudaMemsetAsync(a.converged, 0, (size_t)units * 4, s);
   cudaMemsetAsync(d_flag, 0, 4, s);
@@ -479,6 +486,7 @@ static tactic_status_t build_common(const void* K, const void* V, const tactic_k
     }
     CKB(cudaMemcpyAsync(d_init, init.data(), init.size() * 4, cudaMemcpyHostToDevice, s));
     CKB(cudaStreamSynchronize(s));  // pageable staging buffer goes out of scope
+    if (x->ev_build[0]) CKB(cudaEventRecord(x->ev_build[0], s));
     CKB(km_init_centroids(a, d_init, s));
     const bool simt = (P.flags & TACTIC_FLAG_KMEANS_SIMT) != 0;
     for (int it = 1; it <= iters; ++it) {
@@ -494,11 +502,13 @@ static tactic_status_t build_common(const void* K, const void* V, const tactic_k
       }
     CKB(cudaMemcpyAsync(x->cent, host_cent, (size_t)units * C * 128 * 4, cudaMemcpyHostToDevice, s));
     CKB(cudaMemcpyAsync(x->assign, host_assign, (size_t)units * r.n * 4, cudaMemcpyHostToDevice, s));
+    if (x->ev_build[0]) CKB(cudaEventRecord(x->ev_build[0], s));
     CKB(km_count_scan_scatter(a, 1, s));
     x->iters_req = 0;
     a.iters_req = 0;
   }
   CKB(km_finalize(a, s));
+  if (x->ev_build[1]) CKB(cudaEventRecord(x->ev_build[1], s));
   free_scratch();
   if (!build) CKB(cudaStreamSynchronize(s));
 #undef CKB
@@ -661,6 +671,12 @@ tactic_status_t tactic_index_info(tactic_index_t idx, tactic_index_info_t* info)
   info->device_bytes = idx->device_bytes;
   int fm = 0, fr = 0;
   info->select_cluster_size = fused_plan(idx, &fm, &fr) ? fr : 0;
+  info->build_gpu_ms = -1.f;
+  float ms = 0.f;
+  if (idx->ev_build[0] && idx->ev_build[1] && cudaEventSynchronize(idx->ev_build[1]) == cudaSuccess &&
+      cudaEventElapsedTime(&ms, idx->ev_build[0], idx->ev_build[1]) == cudaSuccess)
+    info->build_gpu_ms = ms;
+  cudaGetLastError();
   return TACTIC_OK;
 }
 

@@ -65,7 +65,7 @@ class IndexInfo(ctypes.Structure):
     _fields_ = [("units", ctypes.c_int32), ("batch", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
                 ("group_size", ctypes.c_int32), ("seq_len", ctypes.c_int32), ("n_clusters", ctypes.c_int32),
                 ("iters_requested", ctypes.c_int32), ("select_cluster_size", ctypes.c_int32),
-                ("device_bytes", ctypes.c_int64)]
+                ("device_bytes", ctypes.c_int64), ("build_gpu_ms", ctypes.c_float)]
 
 
 _lib = None

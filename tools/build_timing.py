@@ -38,7 +38,8 @@ for L in layers:
     t1 = time.perf_counter()
     torch.cuda.synchronize()
     t2 = time.perf_counter()
-    nbytes = idx.info()["device_bytes"]
+    info = idx.info()
+    nbytes = info["device_bytes"]
     malloc_ms = float("nan")
     if rt is not None:
         p = ctypes.c_void_p()
@@ -47,7 +48,7 @@ for L in layers:
         m1 = time.perf_counter()
         rt.cudaFree(p)
         malloc_ms = (m1 - m0) * 1e3
-    print(f"seed {L['seed']}: events {e0.elapsed_time(e1):.3f} ms, host call {1e3 * (t1 - t0):.3f} ms, "
+    print(f"seed {L['seed']}: events {e0.elapsed_time(e1):.3f} ms, kernels {info['build_gpu_ms']:.3f} ms, host call {1e3 * (t1 - t0):.3f} ms, "
           f"call+sync {1e3 * (t2 - t0):.3f} ms, arena {nbytes / 2**20:.0f} MiB cudaMalloc {malloc_ms:.3f} ms, "
           f"iters {np.asarray(idx.export()['iters_run']).tolist()}")
     del idx

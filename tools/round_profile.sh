@@ -17,3 +17,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none \
   -k regex:"score_kernel|score_rank|sample_kernel|fit_unit|attention_kernel" --csv \
   --log-file gpurun_out/c3_launches_$R.csv python tools/profile_c3.py > gpurun_out/c3_launches_$R.log 2>&1
 echo "c3 launch list rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:km_ --csv \
+  --log-file gpurun_out/km_launches_$R.csv python tools/build_timing.py --layers 8 > gpurun_out/km_launches_$R.log 2>&1
+echo "build launch list rc=$?"
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:km_assign_tc -s 3 -c 1 \
+  -o gpurun_out/km_$R -f python tools/profile_build.py > gpurun_out/km_$R.log 2>&1
+echo "k-means capture rc=$?"

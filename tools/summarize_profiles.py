@@ -5,7 +5,9 @@
 Reads  gpurun_out/bench_<R>.json          (one bench.py JSON line)
        gpurun_out/launches_<R>.csv        (ncu --metrics gpu__time_duration.sum launch list of bench.py)
        gpurun_out/full_<R>.ncu-rep        (ncu --set full of tools/profile_decode.py: one decode + one dense)
-Writes profiles/<R>_bench.json, profiles/<R>_launches.txt, profiles/<R>_ncu_full.txt,
+       gpurun_out/km_<R>.ncu-rep          (ncu --set full of one tcgen05 k-means assignment launch)
+       gpurun_out/km_launches_<R>.csv     (launch list of tools/build_timing.py: 8 C2 layer builds)
+Writes profiles/<R>_bench.json, profiles/<R>_launches.txt, profiles/<R>_ncu_full.txt, profiles/<R>_km_build.txt,
        profiles/ncu_traffic.json (dram bytes per launch of the sparse attention kernel, read by bench.py)
 """
 import collections
@@ -122,6 +124,38 @@ if os.path.exists(fp):
     if traffic:
         traffic["source"] = f"profiles/{R}_ncu_full.txt (dram__bytes_read.sum + dram__bytes_write.sum)"
         json.dump(traffic, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
+# ---- index build: tcgen05 assignment capture + the build's launch list
+kp, klp = os.path.join(OUT, f"km_{R}.ncu-rep"), os.path.join(OUT, f"km_launches_{R}.csv")
+if os.path.exists(kp) or os.path.exists(klp):
+    with open(os.path.join(PROF, f"{R}_km_build.txt"), "w") as f:
+        f.write(f"# C2 index build (8 units x 131072 keys, C = 1024, 10 Lloyd iterations) ({R}).\n")
+        if os.path.exists(klp):
+            rows = list(csv.reader(open(klp)))
+            hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+            h = rows[hi]
+            ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+            agg = collections.defaultdict(list)
+            for r in rows[hi + 1:]:
+                if len(r) > vi:
+                    agg[r[ki]].append(float(r[vi].replace(",", "")) / 1000.0)
+            f.write("# ncu --metrics gpu__time_duration.sum --clock-control none launch list of "
+                    "`python tools/build_timing.py --layers 8` (cold, serialised; the first build is a warm-up "
+                    "of 8192 keys):\n")
+            f.write(f"{'launches':>8} {'mean us':>9}  kernel\n")
+            for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
+                f.write(f"{len(v):8d} {sum(v) / len(v):9.2f}  {k[:100]}\n")
+        if os.path.exists(kp):
+            raw = subprocess.run(["ncu", "-i", kp, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+            rr = list(csv.reader(io.StringIO(raw)))
+            h, units = rr[0], rr[1]
+            f.write("\n# ncu --set full --clock-control none of one km_assign_tc_kernel launch "
+                    "(tools/profile_build.py, 4th assignment):\n")
+            for m in ("gpu__time_duration.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+                      "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
+                      "l1tex__m_xbar2l1tex_read_bytes.sum.per_second", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+                      "dram__bytes_read.sum", "launch__grid_size", "launch__block_size", "launch__registers_per_thread"):
+                if m in h:
+                    f.write(f"  {m:70s} {rr[2][h.index(m)]:>12s} {units[h.index(m)]}\n")
 # ---- C3 launch list (tools/profile_c3.py: 3 decodes + 1 dense decode, batch 64 x 32K)
 cp = os.path.join(OUT, f"c3_launches_{R}.csv")
 if os.path.exists(cp):
