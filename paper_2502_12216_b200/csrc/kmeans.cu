@@ -576,22 +576,21 @@ __global__ void km_all_list_kernel(const KmArgs a, int iters) {
 }
 
 // sum over cluster j's rows of |k - c_j|^2 in fp64, read from the cluster-contiguous
-// layout (one warp per cluster, member order): deterministic per-cluster partials.
-__global__ void km_inertia_kernel(const KmArgs a, double* __restrict__ part) {
-  const int u = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (j >= a.C) return;
+// layout.  One CTA per cluster: warp w takes rows r0 + w, r0 + w + 8, ... (8 rows' loads in
+// flight), the 8 warp partials are added in warp order -- deterministic, and the largest
+// cluster no longer sets the kernel time on one warp (one warp per cluster: 406 us at C2).
+__global__ void __launch_bounds__(256) km_inertia_kernel(const KmArgs a, double* __restrict__ part) {
+  __shared__ double wsum[8];
+  const int u = blockIdx.y, j = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int* off = a.offsets + (size_t)u * (a.C + 1);
   const float4 c = *reinterpret_cast<const float4*>(a.cent + ((size_t)u * a.C + j) * 128 + lane * 4);
-  // the cluster's member rows in order, 8 rows' loads in flight per warp (a lone dependent
-  // walk ran at ~0.3 TB/s); per-row sums added in row order, so the result is deterministic
   double s = 0.0;
   const int r0 = off[j], r1 = off[j + 1];
-  for (int rb = r0; rb < r1; rb += 8) {
+  for (int rb = r0 + warp; rb < r1; rb += 64) {
     uint2 raw[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int r = rb + i;
+      const int r = rb + 8 * i;
       // dims 4*lane..4*lane+3 live in logical chunk lane/2, half lane%2
       raw[i] = r < r1 ? *reinterpret_cast<const uint2*>(a.Kp + ((size_t)u * a.n + r) * 128 +
                                                         swz_chunk(lane >> 1, r) * 8 + (lane & 1) * 4)
@@ -599,7 +598,7 @@ __global__ void km_inertia_kernel(const KmArgs a, double* __restrict__ part) {
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      if (rb + i >= r1) break;
+      if (rb + 8 * i >= r1) break;
       const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&raw[i]);
       const float2 x0 = __bfloat1622float2(k2[0]), x1 = __bfloat1622float2(k2[1]);
       const double d0 = (double)x0.x - c.x, d1 = (double)x0.y - c.y;
@@ -608,7 +607,14 @@ __global__ void km_inertia_kernel(const KmArgs a, double* __restrict__ part) {
     }
   }
   s = warp_sum_d(s);
-  if (lane == 0) part[(size_t)u * a.C + j] = s;
+  if (lane == 0) wsum[warp] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += wsum[w];
+    part[(size_t)u * a.C + j] = t;
+  }
 }
 
 __global__ void km_finite_kernel(const KmArgs a, int* __restrict__ flag) {
@@ -670,7 +676,7 @@ cudaError_t km_finalize(const KmArgs& a, cudaStream_t s) {
 }
 
 cudaError_t km_inertia(const KmArgs& a, double* part, cudaStream_t s) {
-  km_inertia_kernel<<<dim3((a.C + 7) / 8, a.units), 256, 0, s>>>(a, part);
+  km_inertia_kernel<<<dim3(a.C, a.units), 256, 0, s>>>(a, part);
   return cudaGetLastError();
 }
 
