@@ -89,3 +89,35 @@ def test_library_sample_constants_equal_the_oracle_rule(L):
     for bad in [dict(p1=0.6, p2=0.1), dict(p2=1.0), dict(exact_frac=-0.1)]:
         with pytest.raises(tactic.TacticError):
             tactic.sample_constants(1000, bad)
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    """The binding's ctypes mirrors of the boundary's structs have the C layout: a C program
+    compiled against include/tactic.h (gcc) prints sizeof / offsetof of every field."""
+    import ctypes
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    from paper_2502_12216_b200 import tactic
+    structs = {"tactic_kv_desc_t": tactic.KvDesc, "tactic_params_t": tactic.Params,
+               "tactic_sample_constants_t": tactic.SampleConstants, "tactic_index_info_t": tactic.IndexInfo}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'  printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run([gcc, "-std=c99", "-o", str(exe), str(src)], check=True, capture_output=True)
+    got = {}
+    for ln in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.splitlines():
+        c, f, v = ln.split()
+        got[(c, f)] = int(v)
+    for cname, py in structs.items():
+        assert got[(cname, "size")] == ctypes.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
