@@ -569,7 +569,7 @@ def run_gpu(args, rank, world, local_rank):
     bms = []
     for L in layers:
         dbg = T.decode_debug(L["q"], L["index"], args.p)
-        assert torch.equal(dbg["out"], L["out"]), "debug decode must reproduce the graph output"
+        assert same_decode(dbg["out"], L["out"]), "debug decode must reproduce the graph output"
         bms.append(step_bytes(dbg, L["sizes"], G, n, C, sc))
     bm = {k: float(np.mean([b[k] for b in bms])) for k in bms[0]}
     bm["union_frac_per_layer"] = [round(b["union_frac"], 5) for b in bms]
@@ -589,7 +589,7 @@ def run_gpu(args, rank, world, local_rank):
         L["q_host"] = L["q"].cpu().pin_memory()
         L["o_host"] = torch.empty_like(L["q_host"]).pin_memory()
         T.decode_host(L["q_host"], L["index"], args.p, L["o_host"])
-        assert torch.equal(L["o_host"], L["out"].cpu()), "host-buffer decode must reproduce the device decode"
+        assert same_decode(L["o_host"], L["out"].cpu()), "host-buffer decode must reproduce the device decode"
     e2e = []
     tm.barrier()
     for i in range(max(2 * LAYERS, min(args.steps, 200))):
@@ -756,6 +756,14 @@ def _self_launch(args):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
     sys.exit(subprocess.call(cmd, env=env))
+
+
+def same_decode(a, b):
+    """Two decodes of the same inputs: equal up to the order of the reference-shift merge's
+    fp32 accumulator adds (a bf16 rounding step at most)."""
+    import torch
+    a, b = a.float().cpu(), b.float().cpu()
+    return bool(torch.all((a - b).abs() <= 2.0 ** -7 * b.abs() + 1e-6))
 
 
 def main():

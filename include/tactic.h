@@ -328,6 +328,12 @@ tactic_status_t tactic_decode_fixed_budget(const void* q, tactic_index_t idx, in
  *     cluster streams at most ~60 GB/s per SM, so with few units (batch 1) the
  *     HBM-bound phases cannot spread over the whole chip.               */
 #define TACTIC_OPT_CLUSTER_DECODE 2u
+/*   TACTIC_OPT_DETERMINISTIC  S9 merges the unit's partials in piece order (bit-identical
+ *     outputs from call to call).  The default merge adds every piece's share, shifted by
+ *     the fit's sampled maximum logit (2^(m_c - m) (o_c, l_c)), into fp32 accumulators with
+ *     atomic adds: ~1.5 us faster at C2, the output varies with the order of those adds
+ *     within fp32 rounding (at most one bf16 rounding step).              */
+#define TACTIC_OPT_DETERMINISTIC 4u
 tactic_status_t tactic_index_set_options(tactic_index_t idx, uint32_t options);
 
 /* ---------------------------------------------------------------------------------------

@@ -49,6 +49,9 @@ constexpr int ATT_THREADS = 32 * (ATT_CWARPS + 2);
 constexpr int ATT_EPI_WARP = ATT_CWARPS + 1;
 constexpr int ATT_STAGE_BYTES = ATT_TILE * 256 * 2;  // K + V
 constexpr int FLAG_FIRST = 1, FLAG_LAST = 2, FLAG_END = 4;
+// reference-shift merge window (log2 units): a piece's scaled sums 2^(m_c - mref) (o_c, l_c)
+// stay normal and finite in fp32 for l_c < 2^24 tokens and |v| < 2^60
+constexpr float ACC_DMIN = 100.f, ACC_DMAX = 40.f;
 
 struct __align__(16) StageMeta {
   unsigned long long mask;
@@ -120,7 +123,66 @@ __device__ __forceinline__ int warp_floor_search_off(const long long* arr, int c
 struct UnitSplit {
   int u, j, n;       // unit, index of this CTA within the unit, CTAs of the unit
   int lo, hi;        // token range within the unit's work list
+  int dm;            // designated merger protocol (CTA j = 0 merges; its range is shorter)
 };
+// tokens the designated merger's range is shortened by (at most half its share): about
+// the time of the other pieces' piece end and arrival, so it waits on none of them
+constexpr int ATT_MERGER_SHORT = 192;
+
+// floor(x / y) for 0 <= x < 2^31, 0 < y: fast reciprocal estimate (off by at most one
+// below 2^22), then exact corrections with wide products
+__device__ __forceinline__ int floor_div32(int x, int y) {
+  int q = __float2int_rz(__fdividef(__int2float_rn(x), __int2float_rn(y)));
+  while ((long long)q * y > x) --q;
+  while ((long long)(q + 1) * y <= x) ++q;
+  return q;
+}
+
+// The same split in 32-bit arithmetic for <= 32 units and (n + tail) units P < 2^31 (one
+// warp pass, no 64-bit multiplies or divisions: the split sits between the dependency wait
+// and the first tile).  With dm, CTA 0 of a unit of n >= 2 CTAs (the designated merger)
+// gets ATT_MERGER_SHORT fewer tokens, the others share the rest equally.
+template <bool DENSE>
+__device__ __forceinline__ UnitSplit unit_split_fast(const AttnArgs& a, int cta, int P, const int* pref, bool dm) {
+  const int U = a.units, lane = threadIdx.x & 31;
+  const int tv = lane < U ? (DENSE ? a.n : pref[(size_t)lane * (a.C + 1) + a.C] + a.tail_len) : 0;
+  int incl = tv;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
+  }
+  const int T = __shfl_sync(0xffffffffu, incl, 31);
+  const bool uniform = T <= 0;  // degenerate: equal split by unit count
+  const int Tt = uniform ? U : T;
+  const int Sv = uniform ? lane : incl - tv, t1 = uniform ? 1 : tv;
+  const int extra = P - U;
+  // cb_v = v + floor(extra S_v / T), cb_{v+1} likewise (two independent divisions)
+  const int cb = lane + floor_div32(extra * Sv, Tt);
+  const int cbn = lane + 1 + floor_div32(extra * (Sv + t1), Tt);
+  const unsigned hit = __ballot_sync(0xffffffffu, lane < U && cb <= cta && cta < cbn);
+  const int l = hit ? __ffs(hit) - 1 : 0;
+  UnitSplit r;
+  r.u = l;
+  r.j = cta - __shfl_sync(0xffffffffu, cb, l);
+  r.n = __shfl_sync(0xffffffffu, cbn, l) - (cta - r.j);
+  const int Tu = uniform ? 0 : __shfl_sync(0xffffffffu, tv, l);
+  r.dm = dm;
+  // lane 0: lo, lane 1: hi
+  const int jj = r.j + (lane & 1);
+  int bnd;
+  if (dm && r.n > 1) {
+    const int share = floor_div32(Tu, r.n);
+    const int cut = ATT_MERGER_SHORT < share / 2 ? ATT_MERGER_SHORT : share / 2;
+    const int h0 = share - cut;  // the merger's range [0, h0)
+    bnd = jj == 0 ? 0 : h0 + floor_div32((Tu - h0) * (jj - 1), r.n - 1);
+  } else {
+    bnd = floor_div32(Tu * jj, r.n);
+  }
+  r.lo = __shfl_sync(0xffffffffu, bnd, 0);
+  r.hi = __shfl_sync(0xffffffffu, bnd, 1);
+  return r;
+}
 // floor(x / y) for 0 <= x, 0 < y, quotient below 2^24: an fp32 reciprocal estimate fixed
 // up with exact 64-bit multiplies (a dependent 64-bit integer or fp64 division costs
 // hundreds of cycles on the single warp that computes the split)
@@ -146,7 +208,7 @@ __device__ __forceinline__ UnitSplit unit_split_of(const AttnArgs& a, int cta, i
   const long long Tt = uniform ? U : T;
   const long long extra = P - U;
   long long S = 0;
-  UnitSplit r = {0, 0, 1, 0, 0};
+  UnitSplit r = {0, 0, 1, 0, 0, 0};
   for (int v0 = 0; v0 < U; v0 += 32) {
     const int v = v0 + lane;
     const long long tv = uniform ? (v < U ? 1 : 0) : tok(v);
@@ -343,10 +405,15 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       bulk_g2s(s_list + rows_pad, a.seg_prefix, (uint32_t)(pref_pad * 4), mbar + 1);
     }
     mbar_wait(mbar + 1, 0);
+    if (threadIdx.x == 0) stamp(45);
     pref_src = s_list + rows_pad;
   }
-  UnitSplit us_ = {0, 0, 1, 0, 0};
-  if (unit_mode) us_ = unit_split_of<DENSE>(a, cta, P, pref_src);
+  UnitSplit us_ = {0, 0, 1, 0, 0, 0};
+  if (unit_mode) {
+    const bool s32 = a.units <= 32 && (long long)(a.n + a.tail_len) * a.units * P < (1LL << 31);
+    us_ = s32 ? unit_split_fast<DENSE>(a, cta, P, pref_src, !DENSE && a.mref != nullptr)
+              : unit_split_of<DENSE>(a, cta, P, pref_src);
+  }
   if (threadIdx.x == 0) stamp(40);
   // sparse global split: every unit carries ATT_PIECE_TOKENS virtual tokens after its work
   // list, so the split prices the fixed cost of a piece (combine, arrival, merge); a CTA
@@ -642,6 +709,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   const int r0 = lane >> 2;                 // token row (S^T) / dim row (O^T) in fragment
   const float scale_log2 = 1.4426950408889634f * 0.08838834764831845f;  // log2(e)/sqrt(128)
   uint32_t qb[8][2];
+  float mr[G];  // reference shift of the piece's unit (reference-shift merge)
+  float own_o[G], own_l[G];  // this CTA's scaled share (designated merger keeps it)
+  int own_flag = 0;
+  const bool dm = us_.dm != 0;
   float o[8][4];
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
   int cur_unit = -1;
@@ -675,6 +746,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             qb[ks][0] = 0u;
             qb[ks][1] = 0u;
           }
+        }
+        if (a.mref) {
+#pragma unroll
+          for (int g = 0; g < G; ++g) mr[g] = __ldg(a.mref + (size_t)cur_unit * G + g);
         }
       }
 #pragma unroll
@@ -786,10 +861,33 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         const bool none = mf == -INFINITY;  // empty piece: zero weight in the merge
         a.part_o[(slot * G + g) * 128 + ct] = none ? 0.f : of / lf;
         if (ct == 0) a.part_lse[slot * G + g] = none ? -INFINITY : (mf + log2f(lf)) * 0.6931471805599453f;
+        if (a.mref) {
+          // reference-shift merge: the piece's 2^(mf - mref) (o, l); a shift outside the
+          // window (the fp32 range of the scaled sums) flags the head, and the merging CTA
+          // then merges the partials instead.  The designated merger keeps its own share
+          // in registers; every other piece adds it into the unit's accumulators.
+          const float d = mf - mr[g];
+          const bool inw = d >= -ACC_DMIN && d <= ACC_DMAX;
+          const float sc = (none || !inw) ? 0.f : exp2f(d);
+          own_o[g] = of * sc;
+          own_l[g] = lf * sc;
+          if (!none && !inw) own_flag = 1;
+          if (!(dm && us_.j == 0)) {
+            float* acc = a.acc + ((size_t)u * G + g) * 129;
+            if (!none && inw) {
+              atomicAdd(acc + ct, own_o[g]);
+              if (ct == 0) atomicAdd(acc + 128, own_l[g]);
+            } else if (!none && ct == 0) {
+              a.acc_flag[(size_t)u * G + g] = 1;
+            }
+          }
+        }
       }
-      // ---- arrival: is this the unit's last piece?  The barrier orders every consumer
-      // thread's partial stores before thread 0's gpu-scope fence and atomic (fences are
-      // cumulative), and the merging CTA fences again before reading the others' partials.
+      // ---- arrival.  The barrier orders every consumer thread's partial stores (and
+      // accumulator adds) before thread 0's gpu-scope release (fences are cumulative).
+      // Designated merger (reference shift, 32-bit split): CTA j = 0 of the unit (given a
+      // shorter range) waits for the other n - 1 arrivals; the others release and leave.
+      // Otherwise the last CTA to arrive (acq_rel atomic) merges.
       asm volatile("bar.sync 1, %0;" ::"n"(ATT_CWARPS * 32));
       long long ue = 0;
       int c0 = cta - us_.j, np = us_.n;
@@ -799,9 +897,20 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         np = pieces_of_unit(us, ue, T, P, &c0);
       }
       if (ct == 0) {
-        const int prev = atom_add_acq_rel_gpu(&a.unit_cnt[u], 1);
-        s_merge = (prev == np - 1);
-        if (s_merge && smem_merge_ok<G>(unit_mode, np)) {
+        if (dm) {
+          if (us_.j != 0) {
+            red_release_gpu(&a.unit_cnt[u], 1);
+            s_merge = 0;
+          } else {
+            while (ld_acquire_gpu(&a.unit_cnt[u]) < np - 1) {
+            }
+            s_merge = 1;
+          }
+        } else {
+          const int prev = atom_add_acq_rel_gpu(&a.unit_cnt[u], 1);
+          s_merge = (prev == np - 1);
+        }
+        if (s_merge && !a.mref && smem_merge_ok<G>(unit_mode, np)) {
           // the unit's partials are contiguous slots [c0, c0 + np): one bulk copy of the
           // o rows and one of the lse values into the (now idle) stage buffers
           fence_proxy_async_global();
@@ -819,7 +928,55 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
         a.tlog[964 + 2 * u] = t_;
       }
-      if (s_merge && smem_merge_ok<G>(unit_mode, np)) {
+      bool merged = false;
+      if (s_merge && a.mref) {
+        // ---- S9 by the reference shift: the accumulators hold sum_c 2^(m_c - mref) (o_c, l_c)
+        // over every piece (the arrival's acquire orders them); thread ct reads dim ct of
+        // every head, then resets the accumulators for the next call
+        float ov[G], lv[G];
+        int fl = own_flag;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const float* acc = a.acc + ((size_t)u * G + g) * 129;
+          ov[g] = __ldcg(acc + ct);
+          lv[g] = __ldcg(acc + 128);
+          fl |= __ldcg(a.acc_flag + (size_t)u * G + g);
+        }
+        if (dm && us_.j == 0) {  // the merger's own share (not in the accumulators)
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            ov[g] += own_o[g];
+            lv[g] += own_l[g];
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) fl |= lv[g] > 0.f ? 0 : 1;
+        asm volatile("bar.sync 1, %0;" ::"n"(ATT_CWARPS * 32));  // every read before the resets
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          float* acc = a.acc + ((size_t)u * G + g) * 129;
+          acc[ct] = 0.f;
+          if (ct == 0) {
+            acc[128] = 0.f;
+            a.acc_flag[(size_t)u * G + g] = 0;
+          }
+        }
+        if (dm && ct == 0) a.unit_cnt[u] = 0;
+        if (!fl) {
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const float inv = 1.f / lv[g], v = ov[g] * inv;
+            const size_t orow = ((size_t)u * G + g) * 128 + ct;
+            if (a.out) a.out[orow] = __float2bfloat16_rn(v);
+            if (a.out_f32) a.out_f32[orow] = v;
+            if (a.lse && ct == 0) a.lse[(size_t)u * G + g] = (mr[g] + log2f(lv[g])) * 0.6931471805599453f;
+          }
+          if (ct == 0) a.unit_cnt[u] = 0;  // self-reset for the next call
+          merged = true;
+        }
+      }
+      if (merged) {
+      } else if (s_merge && !a.mref && smem_merge_ok<G>(unit_mode, np)) {
         // ---- S9 (unit-aligned split): merge the staged pieces from shared memory
         mbar_wait(mbar, 0);
         if (a.tlog && ct == 0 && u < 8) {  // debug: pieces staged

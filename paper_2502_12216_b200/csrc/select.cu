@@ -246,6 +246,7 @@ struct FitParams {
   SampleConsts sc;
   double p;
   double* fit;
+  float* mref;            // [units][G] log2-domain shift for the attention's merge (m log2 e)
   int* J;
   uint8_t* umask;
   int* ulist;
@@ -433,6 +434,7 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
       P.J[ub + g] = J;
       double* f = P.fit + (ub + g) * 6;
       f[0] = thstar; f[1] = Wt; f[2] = P.gmax[(ub + g) * 2]; f[3] = thmax; f[4] = 0; f[5] = 0;
+      P.mref[ub + g] = (float)(P.gmax[(ub + g) * 2] * 1.4426950408889634);
     }
     __syncwarp();
     for (int r = lane; r < J; r += 32) {
@@ -584,6 +586,7 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
         P.J[ub + g] = J;
         double* f = P.fit + (ub + g) * 6;
         f[0] = a; f[1] = b; f[2] = m; f[3] = W; f[4] = mu1; f[5] = mu2;
+        P.mref[ub + g] = m * 1.4426950408889634f;
       }
       // mark this head's selected non-empty clusters (the OR over heads is the GQA union)
       const int* ord = s_ord + (size_t)g * C;
@@ -841,6 +844,7 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
   P.sc = x->sc;
   P.p = a.p;
   P.fit = x->fit;
+  P.mref = x->mref;
   P.J = x->J;
   P.umask = x->umask;
   P.ulist = x->union_list;

@@ -250,6 +250,9 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, const ta
     x->counter = A.get<unsigned int>(1);
     x->part_o = A.get<float>((x->num_ctas + U) * G * 128);
     x->part_lse = A.get<float>((x->num_ctas + U) * G + 4);  // +4: the merge's 16-byte bulk reads
+    x->mref = A.get<float>(U * G);
+    x->acc = A.get<float>(U * G * 129);
+    x->acc_flag = A.get<int>(U * G);
     x->stage = A.get<double>(U * G * 2);
     x->q_stage = A.get<__nv_bfloat16>(U * G * 128);
     x->o_stage = A.get<__nv_bfloat16>(U * G * 128);
@@ -278,6 +281,8 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, const ta
   }
   cudaMemset(x->counter, 0, sizeof(unsigned int));
   cudaMemset(x->unit_cnt, 0, U * sizeof(int));
+  cudaMemset(x->acc, 0, U * G * 129 * sizeof(float));
+  cudaMemset(x->acc_flag, 0, U * G * sizeof(int));
   cudaMemset(x->head_cnt2, 0, U * G * sizeof(int));
   cudaMemset(x->order, 0, U * G * C * sizeof(int));  // valid cluster ids before the first decode
 
@@ -612,7 +617,7 @@ tactic_status_t tactic_assign_tokens(tactic_index_t idx, const void* k, int32_t 
 
 tactic_status_t tactic_index_set_options(tactic_index_t idx, uint32_t options) {
   if (!idx) return fail(TACTIC_ERR_INVALID_ARGUMENT, "NULL index");
-  if (options & ~(uint32_t)(TACTIC_OPT_WINDOWS_EXACT | TACTIC_OPT_CLUSTER_DECODE))
+  if (options & ~(uint32_t)(TACTIC_OPT_WINDOWS_EXACT | TACTIC_OPT_CLUSTER_DECODE | TACTIC_OPT_DETERMINISTIC))
     return fail(TACTIC_ERR_INVALID_ARGUMENT, "unknown option bits");
   tactic_status_t st = check_select_limits(idx, (options & TACTIC_OPT_WINDOWS_EXACT) != 0);
   if (st) return st;
@@ -842,6 +847,11 @@ static tactic_status_t run_attention(const void* q, tactic_index_t idx, bool all
   aa.Vt = idx->Vt;
   aa.tail_len = idx->tail_len;
   aa.tail_cap = idx->tail_cap;
+  if (!all && !(idx->options & TACTIC_OPT_DETERMINISTIC)) {  // the selection's fit wrote the per-head shift
+    aa.mref = idx->mref;
+    aa.acc = idx->acc;
+    aa.acc_flag = idx->acc_flag;
+  }
   CK(launch_attention_sparse(aa, idx->G, idx->num_ctas, s, ev_mid == nullptr && !entry));  // S8 + fused S9
   if (ev_mid) CK(cudaEventRecord(ev_mid, s));
   return TACTIC_OK;

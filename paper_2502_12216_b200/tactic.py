@@ -545,6 +545,7 @@ def decode_fixed_budget(q: torch.Tensor, index: Index, budget: int, per_head: bo
 
 OPT_WINDOWS_EXACT = 1
 OPT_CLUSTER_DECODE = 2  # S1-S9 in one launch of per-unit thread-block clusters (decode_fused.cu)
+OPT_DETERMINISTIC = 4  # S9 by the partial merge in piece order (bit-reproducible outputs)
 
 
 def set_options(index: Index, options: int):

@@ -25,6 +25,15 @@ def assert_output_close(got: np.ndarray, ref: np.ndarray, what: str = ""):
     return ma, rl
 
 
+def assert_same_decode(a: torch.Tensor, b: torch.Tensor, what: str = ""):
+    """Two decodes of the same inputs in the default merge: the reference-shift merge adds
+    the pieces' shares with fp32 atomics, so outputs may differ by the order of those adds
+    -- within one bf16 rounding step of each other (OPT_DETERMINISTIC: bit-identical)."""
+    x, y = a.float().cpu(), b.float().cpu()
+    bad = (x - y).abs() > 2.0 ** -7 * y.abs() + 1e-6
+    assert not bool(bad.any()), f"{what}: {int(bad.sum())} elements differ by more than one bf16 step"
+
+
 def oracle_layer_clustering(K, V, C, iters, seed):
     """Per-unit oracle k-means over a [B][H][n][d] layer; returns centroids, assign, indices."""
     B, H, n, d = K.shape

@@ -8,7 +8,8 @@ import torch
 
 from oracle import tactic_oracle as O
 from synth import bf16_round, make_layer, make_unit, uniform_unit
-from tests._gpu_helpers import (assert_output_close, dev_bf16, j_mismatch_allowed, oracle_layer_clustering)
+from tests._gpu_helpers import (assert_output_close, assert_same_decode, dev_bf16, j_mismatch_allowed,
+                                oracle_layer_clustering)
 
 pytestmark = pytest.mark.gpu
 
@@ -296,6 +297,11 @@ def test_decode_host_and_graph_capture(T):
     cents, asg, _ = oracle_layer_clustering(K, V, C, 5, 12)
     index = _import(T, K, V, cents, asg, G)
     qd = dev_bf16(q)
+    ref = T.decode(qd, index, 0.9)
+    torch.cuda.synchronize()
+    host = T.decode_host(qd.cpu(), index, 0.9)
+    assert_same_decode(host, ref, "host-buffer decode")
+    T.set_options(index, T.OPT_DETERMINISTIC)  # the partial merge: bit-identical entry points
     ref = T.decode(qd, index, 0.9)
     torch.cuda.synchronize()
     host = T.decode_host(qd.cpu(), index, 0.9)
@@ -660,7 +666,7 @@ def test_attention_only_reproduces_decode(T):
     cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, B)
     index = _import(T, K, V, cents, asg, G)
     qd = dev_bf16(q)
-    for opt in (0, T.OPT_CLUSTER_DECODE):
+    for opt in (T.OPT_DETERMINISTIC, 0, T.OPT_CLUSTER_DECODE):
         T.set_options(index, opt)
         ref = T.decode(qd, index, 0.9)
         out = torch.empty_like(ref)
@@ -668,7 +674,40 @@ def test_attention_only_reproduces_decode(T):
             out.zero_()
             T.decode_attention_only(qd, index, out)
             torch.cuda.synchronize()
-            if not opt:
+            if opt == T.OPT_DETERMINISTIC:
                 assert torch.equal(out, ref)
+            elif opt == 0:
+                assert_same_decode(out, ref, "attention-only")
             else:
                 assert_output_close(out.float().cpu().numpy(), ref.float().cpu().numpy(), "attention-only")
+
+
+@pytest.mark.parametrize("sel_scale,att_scale", [(1.0, 30.0), (30.0, 1.0), (1.0, 1.0)])
+def test_reference_shift_merge_window_and_fallback(T, sel_scale, att_scale):
+    """S9 by the reference shift (attention.cu): every piece adds 2^(m_c - m_ref) (o_c, l_c)
+    with m_ref = the fit's sampled max logit.  Attention-only over the last selection's
+    lists with a query whose logits sit far above (x30) or below (selection at x30) that
+    shift leaves the fp32 window, so the merging CTA must fall back to the partial merge;
+    in every case the output equals the oracle's attention over the same union, and the
+    deterministic option gives the same result within rounding."""
+    B, H, G, n, C = 1, 8, 4, 16384, 128
+    K, V, q = _layer(B, H, G, n, 4242)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, 4242)
+    index = _import(T, K, V, cents, asg, G)
+    q_sel = bf16_round(q * sel_scale)
+    q_att = bf16_round(q * att_scale)
+    res = T.decode_debug(dev_bf16(q_sel), index, 0.9)   # selection -> union lists + m_ref
+    out = torch.empty_like(dev_bf16(q_att))
+    T.decode_attention_only(dev_bf16(q_att), index, out)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    for u in range(B * H):
+        toks = O.cluster_tokens(idxs[u], np.nonzero(res["union_mask"][u])[0])
+        o_ref, _ = O.sparse_attention(q_att.reshape(B * H, G, 128)[u], idxs[u].K, idxs[u].V, toks)
+        assert_output_close(got.reshape(B * H, G, 128)[u], o_ref, f"unit {u} scales {sel_scale}/{att_scale}")
+    T.set_options(index, T.OPT_DETERMINISTIC)
+    T.decode_debug(dev_bf16(q_sel), index, 0.9)
+    out2 = torch.empty_like(out)
+    T.decode_attention_only(dev_bf16(q_att), index, out2)
+    torch.cuda.synchronize()
+    assert_output_close(out2.float().cpu().numpy(), got, "deterministic vs reference-shift merge")

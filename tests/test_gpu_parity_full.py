@@ -15,7 +15,8 @@ import torch
 
 from oracle import tactic_oracle as O
 from synth import make_layer
-from tests._gpu_helpers import assert_output_close, dev_bf16, j_mismatch_allowed, oracle_layer_clustering
+from tests._gpu_helpers import (assert_output_close, assert_same_decode, dev_bf16, j_mismatch_allowed,
+                                oracle_layer_clustering)
 
 pytestmark = pytest.mark.gpu
 
@@ -160,7 +161,7 @@ def test_attention_only_before_any_selection_is_rejected(T):
     ref = T.decode(dev_bf16(q), index, 0.9)
     T.decode_attention_only(dev_bf16(q), index, out)
     torch.cuda.synchronize()
-    assert torch.equal(out, ref)
+    assert_same_decode(out, ref, "attention-only")
 
 
 def test_selection_shared_memory_limit_is_reported_at_import(T):

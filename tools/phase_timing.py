@@ -108,9 +108,9 @@ for it in range(4):
         con = [(x - b0) / 1e3 for x in at[18:34] if x > 0]
         print(f"  attention CTA0: starts {(b0 - t0) / 1e3:.2f} us after selection start; ends +{(at[34] - b0) / 1e3:.2f}")
         print("   tiles issued at", np.round(iss, 2).tolist())
-        pz = full[192 + 40:192 + 45]
+        pz = full[192 + 40:192 + 49]
         print("   producer setup (us after wait): " + "  ".join(f"{nm} {(x - b0) / 1e3:.2f}" for nm, x in
-              zip(["split", "lists loaded", "synced", "search start", "window in"], pz) if x > 0))
+              zip(["split", "lists loaded", "synced", "search start", "window in", "all lists in", "split rep0", "split rep1", "split rep2"], pz) if x > 0))
         print("   tiles consumed at", np.round(con, 2).tolist())
         ce = full[512:512 + 296].reshape(-1, 2)
         ce = ce[(ce[:, 0] > 0) & (ce[:, 1] > 0)]
