@@ -143,9 +143,9 @@ __device__ __forceinline__ int floor_div32(int x, int y) {
 // and the first tile).  With dm, CTA 0 of a unit of n >= 2 CTAs (the designated merger)
 // gets ATT_MERGER_SHORT fewer tokens, the others share the rest equally.
 template <bool DENSE>
-__device__ __forceinline__ UnitSplit unit_split_fast(const AttnArgs& a, int cta, int P, const int* pref, bool dm) {
+__device__ __forceinline__ UnitSplit unit_split_fast(const AttnArgs& a, int cta, int P, bool dm) {
   const int U = a.units, lane = threadIdx.x & 31;
-  const int tv = lane < U ? (DENSE ? a.n : pref[(size_t)lane * (a.C + 1) + a.C] + a.tail_len) : 0;
+  const int tv = lane < U ? (DENSE ? a.n : __ldcg(a.seg_prefix + (size_t)lane * (a.C + 1) + a.C) + a.tail_len) : 0;
   int incl = tv;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -397,22 +397,22 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   const size_t rows_pad = (rows_n + 3) & ~(size_t)3, pref_pad = (pref_n + 3) & ~(size_t)3;
   const bool all_lists = !DENSE && unit_mode && rows_pad + pref_pad <= (size_t)LIST_INTS;
   const int* pref_src = a.seg_prefix;
-  if (all_lists) {
-    if (threadIdx.x == 0) {
-      fence_proxy_async_global();
-      mbar_arrive_expect_tx(mbar + 1, (uint32_t)((rows_pad + pref_pad) * 4));
-      bulk_g2s(s_list, a.seg_row, (uint32_t)(rows_pad * 4), mbar + 1);
-      bulk_g2s(s_list + rows_pad, a.seg_prefix, (uint32_t)(pref_pad * 4), mbar + 1);
-    }
-    mbar_wait(mbar + 1, 0);
-    if (threadIdx.x == 0) stamp(45);
-    pref_src = s_list + rows_pad;
+  if (all_lists && threadIdx.x == 0) {
+    fence_proxy_async_global();
+    mbar_arrive_expect_tx(mbar + 1, (uint32_t)((rows_pad + pref_pad) * 4));
+    bulk_g2s(s_list, a.seg_row, (uint32_t)(rows_pad * 4), mbar + 1);
+    bulk_g2s(s_list + rows_pad, a.seg_prefix, (uint32_t)(pref_pad * 4), mbar + 1);
   }
+  // the split needs only the per-unit totals: read them from L2 while the lists land
   UnitSplit us_ = {0, 0, 1, 0, 0, 0};
   if (unit_mode) {
     const bool s32 = a.units <= 32 && (long long)(a.n + a.tail_len) * a.units * P < (1LL << 31);
-    us_ = s32 ? unit_split_fast<DENSE>(a, cta, P, pref_src, !DENSE && a.mref != nullptr)
+    us_ = s32 ? unit_split_fast<DENSE>(a, cta, P, !DENSE && a.mref != nullptr)
               : unit_split_of<DENSE>(a, cta, P, pref_src);
+  }
+  if (all_lists) {
+    mbar_wait(mbar + 1, 0);
+    if (threadIdx.x == 0) stamp(45);
   }
   if (threadIdx.x == 0) stamp(40);
   // sparse global split: every unit carries ATT_PIECE_TOKENS virtual tokens after its work

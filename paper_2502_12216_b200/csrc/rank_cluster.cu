@@ -59,9 +59,20 @@ constexpr size_t sr_smem() {
   return (PS ? 0 : (size_t)M * 512) + (size_t)R * (M + 1) * sizeof(RunEnt) + 2 * (size_t)M * 8 + 2 * (size_t)M * 4 + 64;
 }
 
+// SW warps per 32 clusters score (non-PS: 4, so a warp's dependent chain covers 8 centroids
+// and each SM sub-partition holds several scoring warps; the extra warps leave after S1 and
+// the rank part synchronises its M threads on named barrier 1)
+template <bool PS>
+constexpr int sr_sw() { return PS ? 1 : 4; }
+template <int M>
+__device__ __forceinline__ void sr_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(M) : "memory");
+}
+
 template <int M, int R, bool PS>
-__global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
+__global__ void __launch_bounds__(M * sr_sw<PS>()) score_rank_kernel(const SRParams P) {
   constexpr int NW = M / 32;
+  constexpr int SW = sr_sw<PS>();
   const int c = blockIdx.x, g = blockIdx.y, u = blockIdx.z;  // the cluster spans grid x (R CTAs)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int C = P.C;
@@ -106,7 +117,7 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
     }
     if (R > 1) mbar_arrive_expect_tx(&rbar, (uint32_t)(R * (M + 1) * sizeof(RunEnt)));
   }
-  {
+  if (tid < M) {
     const int* off = P.offsets + (size_t)u * (C + 1);
     const int o0 = valid ? off[j] : 0, o1 = valid ? off[j + 1] : 0;
     s_size[tid] = o1 - o0;
@@ -129,10 +140,15 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
     }
     mbar_wait(&bar, 0);
     pstamp(0);
-    double v[32];
+    // warp w scores the CPW = 32 / SW centroids [w CPW, (w + 1) CPW): lane L holds dims
+    // 4L..4L+3 of each; a butterfly reduce-scatter over offsets 16, 8, ... leaves value
+    // (L >> 2) & (CPW - 1) on lane L after log2(CPW) levels, and plain butterflies over the
+    // remaining offsets finish it -- the same pairing tree as score_kernel (bit-identical crit)
+    constexpr int CPW = 32 / SW;
+    double v[CPW];
   #pragma unroll
-    for (int jj = 0; jj < 32; ++jj) {
-      const int lc = warp * 32 + jj;
+    for (int jj = 0; jj < CPW; ++jj) {
+      const int lc = warp * CPW + jj;
       const float4 cv = lc < nval ? reinterpret_cast<const float4*>(s_cent + lc * 128)[lane]
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
       double s = qd[0] * (double)cv.x;
@@ -142,7 +158,7 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
       v[jj] = s;
     }
   #pragma unroll
-    for (int o = 16, half = 16; o >= 1; o >>= 1, half >>= 1) {
+    for (int o = 16, half = CPW / 2; half >= 1; o >>= 1, half >>= 1) {
       const bool upper = (lane & o) != 0;
   #pragma unroll
       for (int i = 0; i < half; ++i) {
@@ -151,7 +167,17 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
         v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
       }
     }
-    crit = v[0];
+    if constexpr (SW == 1) {
+      crit = v[0];
+    } else {
+  #pragma unroll
+      for (int o = SW / 2; o >= 1; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+      double* s_crit = reinterpret_cast<double*>(bk);  // the sort buffer is idle until S2
+      if ((lane & (SW - 1)) == 0) s_crit[warp * CPW + ((lane / SW) & (CPW - 1))] = v[0];
+      __syncthreads();
+      if (tid >= M) return;  // the extra scoring warps are done (named barriers from here)
+      crit = s_crit[tid];
+    }
   }
   pstamp(1);
 
@@ -167,7 +193,7 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
         o = __shfl_xor_sync(0xffffffffu, x, d);
       } else {
         bk[buf * M + tid] = x;
-        __syncthreads();
+        sr_sync<M>();
         o = bk[buf * M + (tid ^ d)];
         buf ^= 1;
       }
@@ -187,7 +213,7 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
     if (lane >= o) incl += y;
   }
   if (lane == 31) red[warp] = incl;
-  __syncthreads();
+  sr_sync<M>();
   int wbase = 0, tot = 0;
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
@@ -213,7 +239,7 @@ __global__ void __launch_bounds__(M) score_rank_kernel(const SRParams P) {
   const size_t ug = (size_t)u * P.G + g;
   if (!PS && valid) P.crit[ug * C + j] = crit;
   pstamp(3);
-  if constexpr (R == 1) __syncthreads();
+  if constexpr (R == 1) sr_sync<M>();
   else mbar_wait(&rbar, 0);
   pstamp(4);
 
@@ -284,7 +310,7 @@ static cudaError_t launch_sr_t(const SRParams& P, int units, cudaStream_t s, boo
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(R, P.G, units);
-  cfg.blockDim = dim3(M);
+  cfg.blockDim = dim3(M * sr_sw<PS>());
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
