@@ -86,6 +86,15 @@ __global__ void __launch_bounds__(M * sr_sw<PS>()) score_rank_kernel(const SRPar
   __shared__ int red[NW];
   const bool tl_first = c == 0 && g == 0 && u == 0;
   if (tid == 0) tl_mark(P.tlog, 1, 0, tl_first);
+  const int cta_lin = (u * P.G + g) * R + c;  // debug: per-CTA start / end at tlog[3000 + 2 i]
+  auto cstamp = [&](int e) {
+    if (P.tlog && tid == 0 && cta_lin < 512) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      P.tlog[3000 + 2 * cta_lin + e] = t_;
+    }
+  };
+  cstamp(0);
   auto pstamp = [&](int i) {  // debug phase stamps of CTA (0, 0, 0) at tlog[1600 + i]
     if (P.tlog && tl_first && tid == 0) {
       unsigned long long t_;
@@ -299,6 +308,7 @@ __global__ void __launch_bounds__(M * sr_sw<PS>()) score_rank_kernel(const SRPar
     }
   }
   pstamp(6);
+  cstamp(1);
   if (tid == 0) tl_mark(P.tlog, 1, 2, tl_first);
   pdl_launch_dependents();
 }

@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libtactic.so")
+LIB_PATH = os.environ.get("TACTIC_LIB") or os.path.join(_HERE, "lib", "libtactic.so")  # TACTIC_LIB: A/B experiments
 
 STATUS = {0: "TACTIC_OK", 1: "TACTIC_ERR_INVALID_ARGUMENT", 2: "TACTIC_ERR_SHAPE", 3: "TACTIC_ERR_OOM",
           4: "TACTIC_ERR_CUDA", 5: "TACTIC_ERR_NOT_FINITE", 6: "TACTIC_ERR_UNSUPPORTED"}

@@ -65,6 +65,16 @@ for it in range(4):
         for k, nm in enumerate(["score", "score+rank", "sample", "fit", "attention"]):
             if tl[k, 0] > 0:
                 print(f"    {nm:9s} {(tl[k, 0] - z) / 1e3:7.2f} {(tl[k, 1] - z) / 1e3:7.2f} {(tl[k, 2] - z) / 1e3:7.2f}")
+        se = full[3000:3512].reshape(-1, 2)
+        live = se[:, 0] > 0
+        if live.any():
+            st, en = (se[live, 0] - z) / 1e3, (se[live, 1] - z) / 1e3
+            print(f"  score_rank CTAs: start min {st.min():.2f} max {st.max():.2f}; end min {en.min():.2f} "
+                  f"median {np.median(en):.2f} max {en.max():.2f}; dur min {(en - st).min():.2f} median "
+                  f"{np.median(en - st):.2f} max {(en - st).max():.2f}")
+            ids = np.nonzero(live)[0]
+            order = np.argsort(-en)[:6]
+            print("   slowest (cta, start, end): " + ", ".join(f"({ids[i]}, {st[i]:.2f}, {en[i]:.2f})" for i in order))
         rk = full[1600:1607]
         if rk[0] > 0:
             names = ["centroids in", "scored", "sorted", "pushed", "runs in", "ranked", "rowmap"]
@@ -80,10 +90,22 @@ for it in range(4):
         if ds[0] > 0:
             print("  fit unit 0 descriptors (us from first start): " + "  ".join(
                 f"{nm} {(x - z) / 1e3:.2f}" for nm, x in zip(["arrived", "all arrived", "totals", "written"], ds)))
+        hw = full[2720:2720 + 64].reshape(8, 8)
+        for g in range(8):
+            if hw[g, 0] > 0:
+                print(f"   fit head {g} (us after staged): " + "  ".join(
+                    f"{nm} {(hw[g, i] - full[256 + 2]) / 1e3:.2f}" for i, nm in
+                    [(0, "sums"), (1, "W"), (3, "J"), (4, "marked")] if hw[g, i] > 0) +
+                    f"  path {'exact-head' if hw[g, 7] == 1 else 'tail' if hw[g, 7] == 2 else '-'}")
         hs = full[1700:1705]
         if hs[0] > 0:
             print("  fit warp 0 (us after summaries staged): " + "  ".join(
                 f"{nm} {(hs[i] - fs[2]) / 1e3:.2f}" for i, nm in enumerate(["sums", "W", "-", "J", "marked"]) if hs[i] > 0))
+        cf = full[1720:1725]
+        print("  fit CTA u0 clock64 cycles: staged->marked %d  marked->lists %d" % (cf[3] - cf[2], cf[4] - cf[3]))
+        cr = full[1730:1734]
+        if cr[0] > 0:
+            print("  fit mask lists, cycles per repetition:", np.diff(cr).tolist())
         cs = full[264:268]
         print("  compaction (us from first start): " + "  ".join(f"{nm} {(cs[i] - z) / 1e3:6.2f}" for i, nm in
               enumerate(["pass1", "scan", "pass2", "fill"]) if cs[i] > 0))
