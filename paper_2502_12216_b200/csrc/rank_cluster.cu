@@ -25,6 +25,7 @@
 // bound): the cluster spreads one head's sort over R SMs instead of one.
 #include <cuda_bf16.h>
 #include <limits.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -36,6 +37,7 @@ struct SRParams {
   const __nv_bfloat16* q;   // [units][G][128]
   const float* cent;        // [units][C][128]
   const int* offsets;       // [units][C+1]
+  const __nv_bfloat16* Kp;  // [units][n][128] index layout (the sampled rows are prefetched to L2)
   int C, G, n;
   SampleConsts sc;
   double* crit;             // [units][G][C]
@@ -303,6 +305,9 @@ __global__ void __launch_bounds__(M * sr_sw<PS>()) score_rank_kernel(const SRPar
         const int s0 = __shfl_sync(0xffffffffu, my_slot, l);
         const int cnt = __shfl_sync(0xffffffffu, my_cnt, l);
         const int rw = __shfl_sync(0xffffffffu, my_row, l);
+        // the sample kernel reads these K rows next: start their HBM -> L2 transfer now
+        if (lane == 0 && P.Kp)
+          bulk_prefetch_l2(P.Kp + ((size_t)u * P.n + rw) * 128, (uint32_t)cnt * 256u);
         for (int i = lane; i < cnt; i += 32) rm[s0 + i] = rw + i;
       }
     }
@@ -345,6 +350,7 @@ cudaError_t launch_score_rank(const __nv_bfloat16* q, tactic_index_s* x, cudaStr
   P.q = q;
   P.cent = x->cent;
   P.offsets = x->offsets;
+  P.Kp = getenv("TACTIC_NO_SAMPLE_PREFETCH") ? nullptr : (const __nv_bfloat16*)x->Kp;
   P.C = x->C;
   P.G = x->G;
   P.n = x->n;
