@@ -317,7 +317,16 @@ __device__ __noinline__ float windows_cum(float EN, TailF tail, const float* xw,
 
 constexpr int FITU_THREADS = 256;
 
+// GEN = false: the plain Alg. 1 decode (no sharded stages, windows-exact variant, fixed
+// budget or unit prefix) compiled without those paths -- the fit is a chain of single-warp
+// steps, and its code arrives cold after every other layer's traffic has passed through L2
+// (the smaller kernel runs ~1 us faster per layer-step)
+template <bool GEN>
 __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams P) {
+  const int shard_mode = GEN ? P.shard_mode : 0;
+  const int fixed_budget = GEN ? P.fixed_budget : 0;
+  const bool windows_exact = GEN && P.windows_exact;
+  const bool need_unit_prefix = GEN && P.need_unit_prefix;
   extern __shared__ __align__(16) uint8_t fsm[];
   __shared__ int s_J[8];
   __shared__ bool s_last;
@@ -333,7 +342,7 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
   // inclusive prefix of exp(l - m) in place: [G][wx_stride] floats, 16-byte aligned
   const int W1s = 2 * sc.w + 1;
   const int wx_stride = ((2 * W1s + 3 + 3) & ~3) + 4;
-  float* s_wx = P.windows_exact ? (float*)(((uintptr_t)(mask + C) + 15) & ~(uintptr_t)15) : nullptr;
+  float* s_wx = windows_exact ? (float*)(((uintptr_t)(mask + C) + 15) & ~(uintptr_t)15) : nullptr;
   const bool stamp_on = P.tlog != nullptr && u == 0;
   auto stamp = [&](int i) {  // debug: CTA of unit 0 at tlog[256 + i]
     if (stamp_on && tid == 0) {
@@ -387,7 +396,7 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
     // stage the sample kernel's summaries (one round trip; + the window logits of every
     // head for the windows-exact variant, from the 16-byte aligned slot at or below N);
     // sharded stage 2 needs none (its rule reads the mass vector)
-    if (tid == 0 && P.shard_mode != 1) {
+    if (tid == 0 && shard_mode != 1) {
       const uint32_t bs = (uint32_t)G * nb * 16;
       uint32_t lb = 0;
       if (s_wx)
@@ -404,12 +413,12 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
                    (uint32_t)((((st - al) + 2 * W1s) * 4 + 15) & ~(size_t)15), &sbar);
         }
     }
-    if (P.shard_mode != 1) mbar_wait(&sbar, 0);
+    if (shard_mode != 1) mbar_wait(&sbar, 0);
     __syncthreads();
     stamp(2);
     if (stamp_on && tid == 0) P.tlog[1709] = clock64();
   }
-  if (warp < G && P.shard_mode == 1) {
+  if (warp < G && shard_mode == 1) {
     // sharded stage 2 (reading 23): theta* = the largest grid point theta_t whose
     // all-reduced mass reaches p W (none: every cluster); the head selects the rank prefix
     // of clusters with crit / sqrt(d) >= theta* (the order is by descending crit)
@@ -500,7 +509,7 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
       W = windows_cum(EN, tail, xw, sc, n);
     }
     wstamp(1);
-    if (P.shard_mode == 2) {  // sharded stage 1: the local fit only (stage 1b uses it)
+    if (shard_mode == 2) {  // sharded stage 1: the local fit only (stage 1b uses it)
       if (lane == 0) {
         double* f = P.fit + (ub + g) * 6;
         f[0] = a; f[1] = b; f[2] = m; f[3] = W; f[4] = mu1; f[5] = mu2;
@@ -511,11 +520,11 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
       }
     } else {  // the selection (stage 1 selects nothing)
       int J = C;  // p >= 1: every cluster (reading 15)
-      if (P.fixed_budget > 0) {
+      if (fixed_budget > 0) {
         // Quest-like baseline: clusters in criticality order until the head
         // holds fixed_budget tokens (rounded up to the cluster end, as reading 14)
         const int* eg = s_end + (size_t)g * C;
-        J = 1 + warp_count_false(C - 1, [&](int r) { return eg[r] >= P.fixed_budget; });
+        J = 1 + warp_count_false(C - 1, [&](int r) { return eg[r] >= fixed_budget; });
       } else if (P.p < 1.0) {
         const float target = (float)P.p * W;
         const int* eg = s_end + (size_t)g * C;
@@ -600,7 +609,7 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
   }
   __syncthreads();
   stamp(3);
-  if (P.shard_mode == 2) {
+  if (shard_mode == 2) {
     pdl_launch_dependents();
     return;
   }
@@ -652,7 +661,7 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
   stamp(4);
   // the unit-aligned attention split reads only the per-unit totals (uprefix[u][C]); the
   // global split needs unit_prefix, computed by the last CTA to finish
-  if (!P.need_unit_prefix) {
+  if (!need_unit_prefix) {
     if (tid == 0) tl_mark(P.tlog, 3, 2, u == 0);
     return;
   }
@@ -864,10 +873,12 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
   P.en_out = x->stage;
   cudaLaunchAttribute attr[1];
   const size_t smem = fit_smem_bytes(x, P.windows_exact != 0);
-  cudaError_t e = ensure_smem((const void*)fit_unit_kernel, smem);
+  const bool gen = P.shard_mode != 0 || P.windows_exact || P.fixed_budget > 0 || P.need_unit_prefix;
+  const void* fn = gen ? (const void*)fit_unit_kernel<true> : (const void*)fit_unit_kernel<false>;
+  cudaError_t e = ensure_smem(fn, smem);
   if (e != cudaSuccess) return e;
   auto cfg = make_cfg(dim3(x->units), dim3(FITU_THREADS), smem, s, pdl, attr);
-  return cudaLaunchKernelEx(&cfg, fit_unit_kernel, P);
+  return gen ? cudaLaunchKernelEx(&cfg, fit_unit_kernel<true>, P) : cudaLaunchKernelEx(&cfg, fit_unit_kernel<false>, P);
 }
 
 cudaError_t launch_stage1b(const SelArgs& a, cudaStream_t s) {
