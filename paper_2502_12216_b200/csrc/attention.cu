@@ -320,7 +320,10 @@ __device__ __forceinline__ bool smem_merge_ok(bool unit_mode, int np) {
          (size_t)np * G * 512 + 1024 <= (size_t)ATT_LIST_STAGES * ATT_STAGE_BYTES;
 }
 
-template <int G, bool DENSE>
+// UNIT: the unit-aligned split (a.unit_split != 0) compiled apart from the global split,
+// so each instantiation holds only its own prologue, piece-end and merge code (the kernel
+// starts with a cold instruction cache every layer)
+template <int G, bool DENSE, bool UNIT>
 __global__ void __launch_bounds__(ATT_THREADS, 1)
     attention_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, long long dense_total) {
@@ -344,7 +347,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   if (threadIdx.x == 0) tl_mark(a.tlog, 4, 0, blockIdx.x == 0);
   // zero the V halves of the stages once: a never-written V slot meets P = 0, and 0 * NaN
   // would poison O (a never-written K slot only feeds a logit that the mask replaces)
-  const int nst = (!DENSE && a.unit_split != 0) ? ATT_LIST_STAGES : ATT_STAGES;  // stages in use
+  const int nst = (!DENSE && UNIT) ? ATT_LIST_STAGES : ATT_STAGES;  // stages in use
   constexpr int HALF16 = ATT_STAGE_BYTES / 32;  // 16-byte words per K or V half
   for (int i = threadIdx.x; i < nst * HALF16; i += ATT_THREADS)
     reinterpret_cast<uint4*>(stages + (i / HALF16) * ATT_STAGE_BYTES + ATT_STAGE_BYTES / 2)[i % HALF16] =
@@ -390,7 +393,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   int ntile_dbg = 0;
   // unit-aligned split: CTA cta works on one unit only (see UnitSplit); otherwise the
   // global token range split (needs unit_prefix)
-  const bool unit_mode = a.unit_split != 0;
+  constexpr bool unit_mode = UNIT;
   // every unit's work list in smem (sparse, unit-aligned split, when it fits): rows then
   // prefixes, two bulk copies of 16-byte multiples (the arrays carry 4 ints of padding)
   const size_t rows_n = (size_t)a.units * a.C, pref_n = (size_t)a.units * (a.C + 1);
@@ -1125,7 +1128,7 @@ __global__ void lse_merge_plain_kernel(const float* __restrict__ o_parts, const 
 template <int G, bool DENSE>
 static cudaError_t launch_attn_t(const AttnArgs& a, const CUtensorMap* tmK, const CUtensorMap* tmV,
                                  long long dense_total, int num_ctas, cudaStream_t s, bool pdl) {
-  auto kern = attention_kernel<G, DENSE>;
+  auto kern = a.unit_split ? attention_kernel<G, DENSE, true> : attention_kernel<G, DENSE, false>;
   cudaError_t e = func_smem_optin((const void*)kern, ATT_SMEM);
   if (e != cudaSuccess) return e;
   CUtensorMap dummy;
