@@ -689,7 +689,7 @@ def run_gpu(args, rank, world, local_rank):
         # per decode layer-step: score_rank, sample, fit, attention (p < 1); 1 attention at p >= 1
         "gpu_launches": (1 if args.p >= 1 else 4) * LAYERS * args.steps,
         "p50_us": step_p50 * 1e3, "p99_us": step_p99 * 1e3,
-        "roofline": {"bound": "hbm", "kernel": "attention_kernel<4,false> (S8 sparse split-KV + fused S9)",
+        "roofline": {"bound": "hbm", "kernel": "attention_kernel<4,false,true> (S8 sparse split-KV, unit-aligned split + fused S9)",
                      "achieved": att_gbs, "peak": hbm, "unit": "GB/s", "frac": att_gbs / hbm,
                      "traffic": traffic, "peak_source": peak_src,
                      "bytes_per_launch": attn_bytes, "us_per_launch": att_launch_us,

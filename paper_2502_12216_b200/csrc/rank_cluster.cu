@@ -350,7 +350,10 @@ cudaError_t launch_score_rank(const __nv_bfloat16* q, tactic_index_s* x, cudaStr
   P.q = q;
   P.cent = x->cent;
   P.offsets = x->offsets;
-  P.Kp = getenv("TACTIC_NO_SAMPLE_PREFETCH") ? nullptr : (const __nv_bfloat16*)x->Kp;
+  // prefetch the sampled rows into L2 only when they fit there with room to spare (C2: 11 MB;
+  // C3's ~200 MB would be evicted before the sample kernel reads them: double HBM traffic)
+  const double sampled_mb = (double)x->units * x->G * x->sc.slots * 256.0 / 1e6;
+  P.Kp = (getenv("TACTIC_NO_SAMPLE_PREFETCH") || sampled_mb > 32.0) ? nullptr : (const __nv_bfloat16*)x->Kp;
   P.C = x->C;
   P.G = x->G;
   P.n = x->n;

@@ -15,6 +15,7 @@ import csv
 import io
 import json
 import os
+import re
 import subprocess
 import sys
 
@@ -23,6 +24,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 os.makedirs(PROF, exist_ok=True)
+
+def is_sparse_attention(name):
+    """attention_kernel<G, DENSE[, UNIT]> with DENSE = 0 / false (ncu prints either form)."""
+    m = re.search(r"attention_kernel<\s*(?:\(int\))?\d+,\s*(?:\(bool\))?(\w+)", name)
+    return bool(m) and m.group(1) in ("0", "false")
+
 
 # ---- bench line
 bench_line = None
@@ -45,8 +52,7 @@ if os.path.exists(lp):
         if len(r) > vi:
             agg[r[ki]].append(float(r[vi].replace(",", "")) / 1000.0)  # ns -> us
     decode = {k: v for k, v in agg.items()
-              if any(s in k for s in ("score_rank", "sample_kernel", "fit_unit", "attention_kernel<4, 0>",
-                                      "attention_kernel<(int)4, (bool)0>"))}
+              if any(s in k for s in ("score_rank", "sample_kernel", "fit_unit")) or is_sparse_attention(k)}
     tot = sum(sum(v) / len(v) for v in decode.values()) or 1.0
     with open(os.path.join(PROF, f"{R}_launches.txt"), "w") as f:
         f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none launch list of `python bench.py "
@@ -88,7 +94,7 @@ if os.path.exists(fp):
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
                 rd = float(r[idx["dram__bytes_read.sum"]]) * scale.get(units[idx["dram__bytes_read.sum"]], 1)
                 wr = float(r[idx["dram__bytes_write.sum"]]) * scale.get(units[idx["dram__bytes_write.sum"]], 1)
-                key = "dense" if ("1>" in name or "true" in name) else "sparse"
+                key = "sparse" if is_sparse_attention(name) else "dense"
                 traffic[f"attention_kernel_{key}_bytes_per_launch"] = rd + wr
         # stall breakdown per kernel from the source page
         f.write("\n# warp-stall reasons (share of samples) per kernel\n")
