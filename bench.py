@@ -716,8 +716,10 @@ def run_gpu(args, rank, world, local_rank):
                   "exec_tflops_split_bf16": 2 * alg_tflop / (build_gpu_ms * 1e-3)},
         "e2e": {"value": e2e_ms * 1e3, "unit": UNIT, "h2d_bytes_per_step": int(layers[0]["q"].numel() * 2),
                 "d2h_bytes_per_step": int(layers[0]["q"].numel() * 2),
-                "how": "tactic_decode_host per layer-step (pinned q in, decode, out back; the library replays its "
-                       "captured graph), CUDA events around each synchronising call, cold L2; max over ranks"},
+                "how": "tactic_decode_host per layer-step (pinned q in, decode, out back -- zero-copy: the entry "
+                       "kernel reads q from the pinned buffer, the merge writes the output into it; the library "
+                       "replays its captured graph), CUDA events around each synchronising call, cold L2; max over "
+                       "ranks"},
         "nccl": {"backend": "nccl", "world": world, "version": ".".join(map(str, tnccl.version()))
                  if hasattr(tnccl, "version") else None},
         "clocks": clk.summary(),

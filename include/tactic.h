@@ -196,12 +196,16 @@ tactic_status_t tactic_decode(const void* q, tactic_index_t idx, float p, void* 
 tactic_status_t tactic_decode_ex(const void* q, tactic_index_t idx, float p, void* out,
                                  float* lse, void* stream);
 
-/* Same computation through HOST buffers: q_host bf16 [B][Hq][128] is copied in, out_host
- * bf16 [B][Hq][128] copied back; synchronises the stream (end-to-end user call).  The
- * copy-in, the decode and the copy-out are captured once as one CUDA graph per (q_host,
- * out_host, p, tail length, options) and replayed by later calls with the same key (one
- * launch per call); use page-locked host buffers -- with pageable ones the capture is
- * refused and the call falls back to stream-ordered copies and launches.             */
+/* Same computation through HOST buffers: q_host bf16 [B][Hq][128] in, out_host bf16
+ * [B][Hq][128] out; synchronises the stream (end-to-end user call).  With page-locked,
+ * mapped buffers (cudaHostAlloc / torch pin_memory on a UVA system) and the multi-kernel
+ * path (p < 1, no cluster decode, no prescoring) the transfers are zero-copy: the entry
+ * kernel reads q over the bus (staging it for the later kernels) and the S9 merge writes
+ * the output into out_host; otherwise q is copied in and the output copied back.  Either
+ * way the call is captured once as one CUDA graph per (q_host, out_host, p, tail length,
+ * options) and replayed by later calls with the same key (one launch per call); with
+ * pageable buffers the capture is refused and the call falls back to stream-ordered
+ * copies and launches.  TACTIC_HOST_COPIES=1 forces the copies.                      */
 tactic_status_t tactic_decode_host(const void* q_host, tactic_index_t idx, float p,
                                    void* out_host, void* stream);
 

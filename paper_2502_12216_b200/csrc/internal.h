@@ -205,7 +205,10 @@ cudaError_t launch_score(const SelArgs& a, cudaStream_t s, bool pdl);
 // S1 for every (unit, head) into x->crit (score_kernel), q: [units][G][128]
 cudaError_t launch_score_all(const __nv_bfloat16* q, tactic_index_s* x, cudaStream_t s, bool pdl);
 // S1 + S2 + S3 (rank_cluster.cu): crit, order, ends, sampled-slot row map
-cudaError_t launch_score_rank(const __nv_bfloat16* q, tactic_index_s* x, cudaStream_t s, bool pdl);
+// q_copy (nullable): CTA 0 of every (unit, head) stores q there (q in mapped host memory)
+cudaError_t launch_score_rank(const __nv_bfloat16* q, tactic_index_s* x, cudaStream_t s, bool pdl,
+                              __nv_bfloat16* q_copy = nullptr);
+bool score_rank_prescored(const tactic_index_s* x);  // S1 runs in score_kernel first (C3)
 cudaError_t launch_sample(const SelArgs& a, cudaStream_t s, bool pdl);
 cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl);
 int sample_blocks(int slots);

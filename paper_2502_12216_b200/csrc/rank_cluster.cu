@@ -41,6 +41,8 @@ struct SRParams {
   int C, G, n;
   SampleConsts sc;
   double* crit;             // [units][G][C]
+  __nv_bfloat16* q_copy;    // nullable [units][G][128]: CTA 0 of each head stores q here
+                            // (q may live in mapped host memory; the later kernels read the copy)
   int* order;               // [units][G][C]
   int* ends;                // [units][G][C]
   int* rowmap;              // [units][G][slots]
@@ -149,6 +151,9 @@ __global__ void __launch_bounds__(M * sr_sw<PS>()) score_rank_kernel(const SRPar
       const float2 a = __bfloat1622float2(q2[0]), b = __bfloat1622float2(q2[1]);
       qd[0] = a.x; qd[1] = a.y; qd[2] = b.x; qd[3] = b.y;
     }
+    if (P.q_copy && c == 0 && warp == 0)
+      *reinterpret_cast<uint2*>(P.q_copy + ((size_t)u * P.G + g) * 128 + lane * 4) =
+          *reinterpret_cast<const uint2*>(P.q + ((size_t)u * P.G + g) * 128 + lane * 4);
     mbar_wait(&bar, 0);
     pstamp(0);
     // warp w scores the CPW = 32 / SW centroids [w CPW, (w + 1) CPW): lane L holds dims
@@ -345,9 +350,18 @@ static cudaError_t launch_sr(const SRParams& P, int units, cudaStream_t s, bool 
   return ps ? launch_sr_t<M, R, true>(P, units, s, pdl) : launch_sr_t<M, R, false>(P, units, s, pdl);
 }
 
-cudaError_t launch_score_rank(const __nv_bfloat16* q, tactic_index_s* x, cudaStream_t s, bool pdl) {
+bool score_rank_prescored(const tactic_index_s* x) {
+  const int C = x->C, M = C <= 1024 ? 128 : 256, R = (C + M - 1) / M;
+  const int sms = x->num_sms > 0 ? x->num_sms : 148;
+  const bool g_ok = x->G == 1 || x->G == 2 || x->G == 4 || x->G == 8;
+  return g_ok && (long long)R * x->G * x->units > 6LL * sms;
+}
+
+cudaError_t launch_score_rank(const __nv_bfloat16* q, tactic_index_s* x, cudaStream_t s, bool pdl,
+                              __nv_bfloat16* q_copy) {
   SRParams P = {};
   P.q = q;
+  P.q_copy = q_copy;
   P.cent = x->cent;
   P.offsets = x->offsets;
   // prefetch the sampled rows into L2 only when they fit there with room to spare (C2: 11 MB;
@@ -369,9 +383,8 @@ cudaError_t launch_score_rank(const __nv_bfloat16* q, tactic_index_s* x, cudaStr
   // centroids first (score_kernel), then rank from crit with the smaller footprint
   const int M = C <= 1024 ? 128 : 256;
   const int R = (C + M - 1) / M;
-  const int sms = x->num_sms > 0 ? x->num_sms : 148;
-  const bool g_ok = x->G == 1 || x->G == 2 || x->G == 4 || x->G == 8;  // score_kernel's G
-  const bool ps = g_ok && (long long)R * x->G * U > 6LL * sms;
+  const bool ps = score_rank_prescored(x);
+  if (ps && q_copy) return cudaErrorInvalidValue;  // (the mapped-host q path is not prescored)
   if (ps) {
     cudaError_t e = launch_score_all(q, x, s, pdl);
     if (e != cudaSuccess) return e;

@@ -202,6 +202,11 @@ static void free_index(tactic_index_s* x, std::vector<void*>* ptrs) {
 }
 
 // all index allocations are recorded here (keyed by index pointer)
+static bool getenv_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && e[0] == '1';
+}
+
 static std::mutex g_mu;
 static std::map<tactic_index_s*, std::vector<void*>> g_allocs;
 
@@ -799,10 +804,13 @@ static tactic_status_t run_fused(const void* q, tactic_index_t idx, float p, int
   return TACTIC_OK;
 }
 
+// q_copy (nullable): q lives in mapped host memory; score_rank copies it there and the
+// later kernels read the copy
 static tactic_status_t run_selection(const void* q, tactic_index_t idx, double p, int mode, cudaStream_t s,
-                                     const double* gmax, const double* gmass, double* local_max) {
+                                     const double* gmax, const double* gmass, double* local_max,
+                                     __nv_bfloat16* q_copy = nullptr) {
   SelArgs sa = {};
-  sa.q = (const __nv_bfloat16*)q;
+  sa.q = q_copy ? q_copy : (const __nv_bfloat16*)q;
   sa.idx = idx;
   sa.p = p;
   sa.mode = mode;
@@ -813,7 +821,7 @@ static tactic_status_t run_selection(const void* q, tactic_index_t idx, double p
   // a caller's preceding kernel produces q.  The later kernels overlap their prologues
   // with the previous kernel's tail through programmatic dependent launch.
   const bool pdl = true;
-  CK(launch_score_rank(sa.q, idx, s, false));    // S1, S2, S3 (+ sampled-slot row map)
+  CK(launch_score_rank((const __nv_bfloat16*)q, idx, s, false, q_copy));  // S1, S2, S3 (+ row map)
   CK(launch_sample(sa, s, pdl));                 // S4 (+ per-block fit summaries)
   // mode 0: Alg. 1 selection; mode 2: sharded stage 1 (the fit only, same kernel)
   CK(launch_fit(sa, s, pdl));                    // S5-S7
@@ -901,9 +909,31 @@ tactic_status_t tactic_decode(const void* q, tactic_index_t idx, float p, void* 
 }
 
 // H2D q -> decode -> D2H out, enqueued on s (the body of the host-buffer call)
+// device alias of a pinned, mapped host buffer (nullptr: pageable or not mapped)
+static void* mapped_alias(const void* h) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
 static tactic_status_t decode_host_body(const void* q_host, tactic_index_t idx, float p, void* out_host,
                                         cudaStream_t s) {
   const size_t bytes = (size_t)idx->units * idx->G * 128 * 2;
+  // zero-copy: q is read over the bus by score_rank (which stages it for the later kernels)
+  // and the attention's merge writes the output straight into the caller's pinned buffer;
+  // the graph then holds only the decode kernels (no copy-engine round trips)
+  int M = 0, R = 0;
+  void* qd = mapped_alias(q_host);
+  void* od = mapped_alias(out_host);
+  if (qd && od && p < 1.0f && !fused_plan(idx, &M, &R) && !score_rank_prescored(idx) &&
+      !getenv_flag("TACTIC_HOST_COPIES")) {
+    tactic_status_t st = run_selection(qd, idx, (double)p, 0, s, nullptr, nullptr, nullptr, idx->q_stage);
+    if (st) return st;
+    return run_attention(idx->q_stage, idx, false, s, od, nullptr, nullptr);
+  }
   CK(cudaMemcpyAsync(idx->q_stage, q_host, bytes, cudaMemcpyHostToDevice, s));
   tactic_status_t st = tactic_decode_ex(idx->q_stage, idx, p, idx->o_stage, nullptr, s);
   if (st) return st;
