@@ -299,13 +299,24 @@ def test_decode_host_and_graph_capture(T):
     qd = dev_bf16(q)
     ref = T.decode(qd, index, 0.9)
     torch.cuda.synchronize()
-    host = T.decode_host(qd.cpu(), index, 0.9)
+    host = T.decode_host(qd.cpu(), index, 0.9)          # pageable: copies in and out
     assert_same_decode(host, ref, "host-buffer decode")
+    q_pin = qd.cpu().pin_memory()                          # pinned + mapped: zero-copy path
+    o_pin = torch.empty_like(q_pin).pin_memory()
+    for _ in range(3):                                     # capture, then graph replays
+        o_pin.zero_()
+        T.decode_host(q_pin, index, 0.9, o_pin)
+        assert_same_decode(o_pin, ref, "zero-copy host decode")
+    q_pin.copy_((qd * 0.5).cpu())                          # new contents, same buffers
+    T.decode_host(q_pin, index, 0.9, o_pin)
+    assert_same_decode(o_pin, T.decode(qd * 0.5, index, 0.9), "zero-copy host decode, new q")
     T.set_options(index, T.OPT_DETERMINISTIC)  # the partial merge: bit-identical entry points
     ref = T.decode(qd, index, 0.9)
     torch.cuda.synchronize()
     host = T.decode_host(qd.cpu(), index, 0.9)
     assert torch.equal(host, ref.cpu())
+    T.decode_host(q_pin.copy_(qd.cpu()), index, 0.9, o_pin)
+    assert torch.equal(o_pin, ref.cpu())
     out = torch.empty_like(qd)
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
