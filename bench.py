@@ -607,6 +607,8 @@ def run_gpu(args, rank, world, local_rank):
 
     c3 = measure_c3(T, dev, args, rank, world, tm) if args.c3 else None
     c4 = measure_c4(T, dev, args, rank, world, tm) if args.c4 else None
+    if c4:  # like for like: one step per graph launch, cold L2 (C2's isolated layer-step)
+        c4["compute_vs_c2_isolated_layer"] = c4["compute_only_us"] / iso_us
 
     # ---- Table-1 diagnostics (NEXT 3) over the same layers: Optimal /
     # Cluster-Optimal / Tactic budgets, achieved cumulative score and success rate

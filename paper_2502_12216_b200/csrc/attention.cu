@@ -52,6 +52,45 @@ constexpr int FLAG_FIRST = 1, FLAG_LAST = 2, FLAG_END = 4;
 // reference-shift merge window (log2 units): a piece's scaled sums 2^(m_c - mref) (o_c, l_c)
 // stay normal and finite in fp32 for l_c < 2^24 tokens and |v| < 2^60
 constexpr float ACC_DMIN = 100.f, ACC_DMAX = 40.f;
+constexpr int ATT_ACC_ROW = 132;  // accumulator row per (unit, head): o[128], l, padding (16-byte rows)
+
+// G consecutive fp32 adds into global memory as 16- / 8-byte vector reductions
+template <int G>
+__device__ __forceinline__ void red_add_f32xG(float* p, const float* v) {
+  if constexpr (G == 1) {
+    atomicAdd(p, v[0]);
+  } else if constexpr (G == 2) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v[0]), "f"(v[1]) : "memory");
+  } else {
+#pragma unroll
+    for (int i = 0; i < G; i += 4)
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p + i), "f"(v[i]), "f"(v[i + 1]),
+                   "f"(v[i + 2]), "f"(v[i + 3])
+                   : "memory");
+  }
+}
+template <int G>
+__device__ __forceinline__ void ld_cg_f32xG(const float* p, float* v) {
+  if constexpr (G == 1) {
+    v[0] = __ldcg(p);
+  } else if constexpr (G == 2) {
+    const float2 x = __ldcg(reinterpret_cast<const float2*>(p));
+    v[0] = x.x; v[1] = x.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < G; i += 4) {
+      const float4 x = __ldcg(reinterpret_cast<const float4*>(p + i));
+      v[i] = x.x; v[i + 1] = x.y; v[i + 2] = x.z; v[i + 3] = x.w;
+    }
+  }
+}
+// OR of a predicate over the 128 consumer threads (named barrier 1), a barrier as well
+__device__ __forceinline__ int bar_red_or(int x) {
+  int r;
+  asm volatile("{\n .reg .pred p, q;\n setp.ne.s32 q, %1, 0;\n bar.red.or.pred p, 1, %2, q;\n selp.s32 %0, 1, 0, p;\n}"
+               : "=r"(r) : "r"(x), "n"(ATT_CWARPS * 32) : "memory");
+  return r;
+}
 
 struct __align__(16) StageMeta {
   unsigned long long mask;
@@ -713,7 +752,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   const float scale_log2 = 1.4426950408889634f * 0.08838834764831845f;  // log2(e)/sqrt(128)
   uint32_t qb[8][2];
   float mr[G];  // reference shift of the piece's unit (reference-shift merge)
-  float own_o[G], own_l[G];  // this CTA's scaled share (designated merger keeps it)
+  float own_o[G], own_l[1];  // this CTA's scaled share, head-major (designated merger keeps it)
   int own_flag = 0;
   const bool dm = us_.dm != 0;
   float o[8][4];
@@ -848,6 +887,51 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       // partial slot: the CTA index (unit-aligned split: one piece per CTA) or cta + unit
       // (global split: a CTA may hold pieces of several units; c + u is unique)
       const size_t slot = unit_mode ? (size_t)cta : (size_t)cta + u;
+      if (a.mref) {
+        // reference-shift merge, head-major: thread ct combines head gh = ct / TPH, dims
+        // [d0, d0 + G) (G values per thread, so the accumulator adds are G-wide vectors).
+        // The piece's 2^(mf - mref) (o, l): a shift outside the window (the fp32 range of
+        // the scaled sums) flags the head, and the merger then merges the partials
+        // instead.  The designated merger keeps its own share in registers; every other
+        // piece adds it into the unit's accumulators.
+        constexpr int TPH = 128 / G;
+        const int gh = ct / TPH, d0 = (ct % TPH) * G;
+        float mf = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < ATT_CWARPS; ++w) mf = fmaxf(mf, scratch[w * (8 * 128 + 16) + 8 * 128 + gh]);
+        const bool none = mf == -INFINITY;  // empty piece: zero weight in the merge
+        float lf = 0.f, of[G];
+#pragma unroll
+        for (int i = 0; i < G; ++i) of[i] = 0.f;
+#pragma unroll
+        for (int w = 0; w < ATT_CWARPS; ++w) {
+          const float* sww = scratch + w * (8 * 128 + 16);
+          const float e = none ? 0.f : exp2f(sww[8 * 128 + gh] - mf);
+          lf += sww[8 * 128 + 8 + gh] * e;
+#pragma unroll
+          for (int i = 0; i < G; ++i) of[i] += sww[gh * 128 + d0 + i] * e;
+        }
+        const float il = none ? 0.f : 1.f / lf;
+#pragma unroll
+        for (int i = 0; i < G; ++i) a.part_o[(slot * G + gh) * 128 + d0 + i] = of[i] * il;
+        if (ct % TPH == 0) a.part_lse[slot * G + gh] = none ? -INFINITY : (mf + log2f(lf)) * 0.6931471805599453f;
+        const float d = mf - mr[gh];
+        const bool inw = d >= -ACC_DMIN && d <= ACC_DMAX;
+        const float sc = (none || !inw) ? 0.f : exp2f(d);
+#pragma unroll
+        for (int i = 0; i < G; ++i) own_o[i] = of[i] * sc;
+        own_l[0] = lf * sc;
+        if (!none && !inw) own_flag = 1;
+        if (!(dm && us_.j == 0)) {
+          float* acc = a.acc + ((size_t)u * G + gh) * ATT_ACC_ROW;
+          if (!none && inw) {
+            red_add_f32xG<G>(acc + d0, own_o);
+            if (ct % TPH == 0) atomicAdd(acc + 128, own_l[0]);
+          } else if (!none && ct % TPH == 0) {
+            a.acc_flag[(size_t)u * G + gh] = 1;
+          }
+        }
+      } else {
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         float mf = -INFINITY;
@@ -864,27 +948,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         const bool none = mf == -INFINITY;  // empty piece: zero weight in the merge
         a.part_o[(slot * G + g) * 128 + ct] = none ? 0.f : of / lf;
         if (ct == 0) a.part_lse[slot * G + g] = none ? -INFINITY : (mf + log2f(lf)) * 0.6931471805599453f;
-        if (a.mref) {
-          // reference-shift merge: the piece's 2^(mf - mref) (o, l); a shift outside the
-          // window (the fp32 range of the scaled sums) flags the head, and the merging CTA
-          // then merges the partials instead.  The designated merger keeps its own share
-          // in registers; every other piece adds it into the unit's accumulators.
-          const float d = mf - mr[g];
-          const bool inw = d >= -ACC_DMIN && d <= ACC_DMAX;
-          const float sc = (none || !inw) ? 0.f : exp2f(d);
-          own_o[g] = of * sc;
-          own_l[g] = lf * sc;
-          if (!none && !inw) own_flag = 1;
-          if (!(dm && us_.j == 0)) {
-            float* acc = a.acc + ((size_t)u * G + g) * 129;
-            if (!none && inw) {
-              atomicAdd(acc + ct, own_o[g]);
-              if (ct == 0) atomicAdd(acc + 128, own_l[g]);
-            } else if (!none && ct == 0) {
-              a.acc_flag[(size_t)u * G + g] = 1;
-            }
-          }
-        }
+      }
       }
       // ---- arrival.  The barrier orders every consumer thread's partial stores (and
       // accumulator adds) before thread 0's gpu-scope release (fences are cumulative).
@@ -926,6 +990,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(ATT_CWARPS * 32));
+      if (a.tlog && ct == 0 && cta < 512) {  // debug: the CTA's unit, index, CTAs of the unit; release time
+        unsigned long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+        a.tlog[3600 + cta] = (unsigned long long)u | ((unsigned long long)us_.j << 16) | ((unsigned long long)us_.n << 32);
+        a.tlog[3800 + cta] = t_;  // after the arrival (release / poll)
+      }
       if (s_merge && a.tlog && ct == 0 && u < 8) {  // debug: merge start
         unsigned long long t_;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
@@ -936,44 +1006,46 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         // ---- S9 by the reference shift: the accumulators hold sum_c 2^(m_c - mref) (o_c, l_c)
         // over every piece (the arrival's acquire orders them); thread ct reads dim ct of
         // every head, then resets the accumulators for the next call
-        float ov[G], lv[G];
+        constexpr int TPH = 128 / G;
+        const int gh = ct / TPH, d0 = (ct % TPH) * G;
+        float* acc = a.acc + ((size_t)u * G + gh) * ATT_ACC_ROW;
+        float ov[G];
+        ld_cg_f32xG<G>(acc + d0, ov);
+        float lv = __ldcg(acc + 128);
         int fl = own_flag;
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const float* acc = a.acc + ((size_t)u * G + g) * 129;
-          ov[g] = __ldcg(acc + ct);
-          lv[g] = __ldcg(acc + 128);
-          fl |= __ldcg(a.acc_flag + (size_t)u * G + g);
-        }
+        for (int g = 0; g < G; ++g) fl |= __ldcg(a.acc_flag + (size_t)u * G + g);
         if (dm && us_.j == 0) {  // the merger's own share (not in the accumulators)
 #pragma unroll
-          for (int g = 0; g < G; ++g) {
-            ov[g] += own_o[g];
-            lv[g] += own_l[g];
-          }
+          for (int i = 0; i < G; ++i) ov[i] += own_o[i];
+          lv += own_l[0];
         }
+        fl |= lv > 0.f ? 0 : 1;
+        // every read before the resets; the OR over the CTA's threads makes the choice of
+        // merge uniform (a flag or an empty head anywhere -> the partial merge)
+        fl = bar_red_or(fl);
 #pragma unroll
-        for (int g = 0; g < G; ++g) fl |= lv[g] > 0.f ? 0 : 1;
-        asm volatile("bar.sync 1, %0;" ::"n"(ATT_CWARPS * 32));  // every read before the resets
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          float* acc = a.acc + ((size_t)u * G + g) * 129;
-          acc[ct] = 0.f;
-          if (ct == 0) {
-            acc[128] = 0.f;
-            a.acc_flag[(size_t)u * G + g] = 0;
-          }
+        for (int i = 0; i < G; ++i) acc[d0 + i] = 0.f;
+        if (ct % TPH == 0) {
+          acc[128] = 0.f;
+          a.acc_flag[(size_t)u * G + gh] = 0;
         }
         if (dm && ct == 0) a.unit_cnt[u] = 0;
         if (!fl) {
+          const float inv = 1.f / lv;
+          const size_t orow = ((size_t)u * G + gh) * 128 + d0;
+          if (a.out) {
 #pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const float inv = 1.f / lv[g], v = ov[g] * inv;
-            const size_t orow = ((size_t)u * G + g) * 128 + ct;
-            if (a.out) a.out[orow] = __float2bfloat16_rn(v);
-            if (a.out_f32) a.out_f32[orow] = v;
-            if (a.lse && ct == 0) a.lse[(size_t)u * G + g] = (mr[g] + log2f(lv[g])) * 0.6931471805599453f;
+            for (int i = 0; i < G; i += 2) {
+              if (G == 1) a.out[orow] = __float2bfloat16_rn(ov[0] * inv);
+              else *reinterpret_cast<__nv_bfloat162*>(a.out + orow + i) = __floats2bfloat162_rn(ov[i] * inv, ov[i + (G > 1)] * inv);
+            }
           }
+          if (a.out_f32) {
+#pragma unroll
+            for (int i = 0; i < G; ++i) a.out_f32[orow + i] = ov[i] * inv;
+          }
+          if (a.lse && ct % TPH == 0) a.lse[(size_t)u * G + gh] = (mr[gh] + log2f(lv)) * 0.6931471805599453f;
           if (ct == 0) a.unit_cnt[u] = 0;  // self-reset for the next call
           merged = true;
         }

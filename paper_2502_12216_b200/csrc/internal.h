@@ -114,7 +114,7 @@ struct tactic_index_s {
   // accumulators the pieces add into, and the per-head out-of-window flags (all zero
   // between calls: the merging CTA resets them)
   float* mref = nullptr;         // [units][G] log2-domain shift (the fit's sampled max m)
-  float* acc = nullptr;          // [units][G][129]: sum of 2^(m_c - mref) (o_c, l_c)
+  float* acc = nullptr;          // [units][G][132]: sum of 2^(m_c - mref) (o_c, l_c)
   int* acc_flag = nullptr;       // [units][G]
   double* stage = nullptr;       // sharded stage 1 -> 1b: [units][G][2] (E_N, 0)
   __nv_bfloat16* q_stage = nullptr;  // [units][G][128] (host-buffer decode)
@@ -157,7 +157,7 @@ struct AttnArgs {
   int* unit_cnt;                   // [units] arrival counters, zero between calls
   // reference-shift merge (unit-aligned split only; nullptr: the partial merge)
   const float* mref;               // [units][G] log2-domain shift per head
-  float* acc;                      // [units][G][129] (o[128], l), zero between calls
+  float* acc;                      // [units][G][132] (o[128], l), zero between calls
   int* acc_flag;                   // [units][G] a piece fell outside the shift window
   __nv_bfloat16* out;              // nullable [units][G][128]
   float* out_f32;                  // nullable

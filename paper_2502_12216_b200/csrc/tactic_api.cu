@@ -256,7 +256,7 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, const ta
     x->part_o = A.get<float>((x->num_ctas + U) * G * 128);
     x->part_lse = A.get<float>((x->num_ctas + U) * G + 4);  // +4: the merge's 16-byte bulk reads
     x->mref = A.get<float>(U * G);
-    x->acc = A.get<float>(U * G * 129);
+    x->acc = A.get<float>(U * G * 132);
     x->acc_flag = A.get<int>(U * G);
     x->stage = A.get<double>(U * G * 2);
     x->q_stage = A.get<__nv_bfloat16>(U * G * 128);
@@ -286,7 +286,7 @@ static tactic_status_t alloc_index(const Resolved& r, int C, int iters, const ta
   }
   cudaMemset(x->counter, 0, sizeof(unsigned int));
   cudaMemset(x->unit_cnt, 0, U * sizeof(int));
-  cudaMemset(x->acc, 0, U * G * 129 * sizeof(float));
+  cudaMemset(x->acc, 0, U * G * 132 * sizeof(float));
   cudaMemset(x->acc_flag, 0, U * G * sizeof(int));
   cudaMemset(x->head_cnt2, 0, U * G * sizeof(int));
   cudaMemset(x->order, 0, U * G * C * sizeof(int));  // valid cluster ids before the first decode

@@ -155,6 +155,20 @@ for it in range(4):
             fast = np.argsort(en)[:5]
             print("   fastest CTAs (cta, end, piece-end us, merges, pieces, tiles):",
                   [(int(c), round(float(en[c]), 1), round(float(pe[c]), 2), int(nm_[c]), int(npc_[c]), int(nt_[c])) for c in fast])
+            meta = full[3600:3748]
+            rel = full[3800:3948]
+            if (rel > 0).any():
+                uu = (meta & 0xFFFF).astype(int)
+                jj = ((meta >> 16) & 0xFFFF).astype(int)
+                print("   per unit: CTAs, slowest piece arrival (non-merger), merger poll done, merger end (us):")
+                for uni in sorted(set(uu.tolist())):
+                    cs = [c for c in range(148) if uu[c] == uni and rel[c] > 0]
+                    nm = [c for c in cs if jj[c] != 0]
+                    mc = [c for c in cs if jj[c] == 0]
+                    sl = max(((rel[c] - b0) / 1e3 for c in nm), default=float('nan'))
+                    md = ((rel[mc[0]] - b0) / 1e3) if mc else float('nan')
+                    me = (en[mc[0]]) if mc else float('nan')
+                    print(f"     unit {uni}: {len(cs)} CTAs, slowest arrival {sl:.2f}, merger poll {md:.2f}, merger end {me:.2f}")
             mg = full[964:964 + 16].reshape(8, 2)
             print("   merges (start, end) us:", [(round((s - b0) / 1e3, 2), round((e - b0) / 1e3, 2)) for s, e in mg if s > 0])
             cp = full[980:988]
