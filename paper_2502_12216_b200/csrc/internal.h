@@ -38,7 +38,7 @@ inline bool unit_split_ok(int units, int ctas) { return 2 * units <= ctas; }
 // griddepcontrol.wait, last CTA end (atomicMax); k = 0 score, 1 rank, 2 sample, 3 fit,
 // 4 attention
 constexpr int TL_BASE = 1536;
-inline size_t tlog_entries(int units) { return (size_t)(units * 128 > 4096 ? units * 128 : 4096); }
+inline size_t tlog_entries(int units) { return (size_t)(units * 128 > 8192 ? units * 128 : 8192); }
 #ifdef __CUDACC__
 // what: 0 start, 1 past the wait (first CTA only), 2 end (every CTA; the max survives).
 // Called by one thread per CTA.

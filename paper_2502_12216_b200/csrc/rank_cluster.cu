@@ -281,6 +281,11 @@ __global__ void __launch_bounds__(M * sr_sw<PS>()) score_rank_kernel(const SRPar
     }
   }
   pstamp(5);
+  if (P.tlog && tid == 0 && cta_lin < 512) {  // debug: per-CTA "ranked" time
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    P.tlog[4096 + cta_lin] = t_;
+  }
   if (real) {
     P.order[ug * C + r] = id;
     P.ends[ug * C + r] = end;

@@ -219,7 +219,7 @@ class Index:
     def debug_timing(self) -> np.ndarray:
         """Debug %globaltimer stamps (ns), flat: kernel-specific slots below 1536, the decode
         timeline at 1536 + 4k (TACTIC_TLOG=1 indexes only; see csrc/internal.h)."""
-        buf = np.zeros(max(self.units * 128, 4096), dtype=np.uint64)
+        buf = np.zeros(max(self.units * 128, 8192), dtype=np.uint64)
         _check(lib().tactic_index_debug_timing(self.handle, buf.ctypes.data, buf.size))
         return buf
 

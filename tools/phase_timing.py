@@ -74,7 +74,10 @@ for it in range(4):
                   f"{np.median(en - st):.2f} max {(en - st).max():.2f}")
             ids = np.nonzero(live)[0]
             order = np.argsort(-en)[:6]
-            print("   slowest (cta, start, end): " + ", ".join(f"({ids[i]}, {st[i]:.2f}, {en[i]:.2f})" for i in order))
+            rkd = (full[4096:4096 + 512][live] - z) / 1e3
+            print("   slowest (cta, start, ranked, end): " + ", ".join(f"({ids[i]}, {st[i]:.2f}, {rkd[i]:.2f}, {en[i]:.2f})" for i in order))
+            print(f"   ranked: min {rkd.min():.2f} median {np.median(rkd):.2f} max {rkd.max():.2f}; rowmap phase (end - ranked): "
+                  f"median {np.median(en - rkd):.2f} max {(en - rkd).max():.2f}")
         rk = full[1600:1607]
         if rk[0] > 0:
             names = ["centroids in", "scored", "sorted", "pushed", "runs in", "ranked", "rowmap"]
