@@ -88,6 +88,8 @@ __global__ void __launch_bounds__(M * sr_sw<PS>()) score_rank_kernel(const SRPar
   int* s_row = s_size + M;                                    // [M]
   __shared__ uint64_t bar, rbar;
   __shared__ int red[NW];
+  __shared__ int4 s_iv[3 * M];  // S3: sampled-slot intervals (slot, count, row) of this CTA
+  __shared__ int s_niv;
   const bool tl_first = c == 0 && g == 0 && u == 0;
   if (tid == 0) tl_mark(P.tlog, 1, 0, tl_first);
   const int cta_lin = (u * P.G + g) * R + c;  // debug: per-CTA start / end at tlog[3000 + 2 i]
@@ -112,6 +114,7 @@ __global__ void __launch_bounds__(M * sr_sw<PS>()) score_rank_kernel(const SRPar
   const bool valid = j < C;
   const int nval = C - c * M < M ? (C - c * M > 0 ? C - c * M : 0) : M;  // clusters of this CTA
   if (tid == 0) {
+    s_niv = 0;
     mbar_init(&bar, 1);
     mbar_init(&rbar, 1);
     fence_barrier_init();
@@ -294,7 +297,6 @@ __global__ void __launch_bounds__(M * sr_sw<PS>()) score_rank_kernel(const SRPar
   // ---- S3: row-map entries of the sampled slots inside (end - size, end]
   {
     const SampleConsts sc = P.sc;
-    int* rm = P.rowmap + ug * sc.slots;
     const int t_lo = end - size + 1, t_hi = end;  // 1-based token ranks of this cluster
     const int row0 = real ? s_row[id - c * M] : 0;
     const int W1 = 2 * sc.w + 1;
@@ -306,20 +308,23 @@ __global__ void __launch_bounds__(M * sr_sw<PS>()) score_rank_kernel(const SRPar
       else if (sgi == 1) { seg_lo = sc.x1 - sc.w; seg_hi = sc.x1 + sc.w; slot_base = sc.N; }
       else { seg_lo = sc.x2 - sc.w; seg_hi = sc.x2 + sc.w; slot_base = sc.N + W1; }
       const int a = t_lo > seg_lo ? t_lo : seg_lo, b = t_hi < seg_hi ? t_hi : seg_hi;
-      const bool has = real && size > 0 && a <= b;
-      unsigned bal = __ballot_sync(0xffffffffu, has);
-      const int my_slot = slot_base + (a - seg_lo), my_cnt = b - a + 1, my_row = row0 + (a - t_lo);
-      while (bal) {
-        const int l = __ffs(bal) - 1;
-        bal &= bal - 1;
-        const int s0 = __shfl_sync(0xffffffffu, my_slot, l);
-        const int cnt = __shfl_sync(0xffffffffu, my_cnt, l);
-        const int rw = __shfl_sync(0xffffffffu, my_row, l);
-        // the sample kernel reads these K rows next: start their HBM -> L2 transfer now
-        if (lane == 0 && P.Kp)
-          bulk_prefetch_l2(P.Kp + ((size_t)u * P.n + rw) * 128, (uint32_t)cnt * 256u);
-        for (int i = lane; i < cnt; i += 32) rm[s0 + i] = rw + i;
+      if (real && size > 0 && a <= b) {  // one interval of sampled slots: queue it for the CTA
+        const int e = atomicAdd(&s_niv, 1);
+        s_iv[e] = make_int4(slot_base + (a - seg_lo), b - a + 1, row0 + (a - t_lo), 0);
       }
+    }
+  }
+  // the CTA's intervals round-robin over its warps (a warp holding several top-ranked
+  // clusters no longer writes all of their rows alone)
+  sr_sync<M>();
+  {
+    int* rm = P.rowmap + ug * P.sc.slots;
+    const int niv = s_niv;
+    for (int e = warp; e < niv; e += NW) {
+      const int4 iv = s_iv[e];
+      // the sample kernel reads these K rows next: start their HBM -> L2 transfer now
+      if (lane == 0 && P.Kp) bulk_prefetch_l2(P.Kp + ((size_t)u * P.n + iv.z) * 128, (uint32_t)iv.y * 256u);
+      for (int i = lane; i < iv.y; i += 32) rm[iv.x + i] = iv.z + i;
     }
   }
   pstamp(6);

@@ -74,7 +74,7 @@ for it in range(4):
                   f"{np.median(en - st):.2f} max {(en - st).max():.2f}")
             ids = np.nonzero(live)[0]
             order = np.argsort(-en)[:6]
-            rkd = (full[4096:4096 + 512][live] - z) / 1e3
+            rkd = (full[4096:4096 + len(live)][live].astype(np.int64) - z) / 1e3
             print("   slowest (cta, start, ranked, end): " + ", ".join(f"({ids[i]}, {st[i]:.2f}, {rkd[i]:.2f}, {en[i]:.2f})" for i in order))
             print(f"   ranked: min {rkd.min():.2f} median {np.median(rkd):.2f} max {rkd.max():.2f}; rowmap phase (end - ranked): "
                   f"median {np.median(en - rkd):.2f} max {(en - rkd).max():.2f}")
