@@ -78,6 +78,15 @@ for it in range(4):
             print("   slowest (cta, start, ranked, end): " + ", ".join(f"({ids[i]}, {st[i]:.2f}, {rkd[i]:.2f}, {en[i]:.2f})" for i in order))
             print(f"   ranked: min {rkd.min():.2f} median {np.median(rkd):.2f} max {rkd.max():.2f}; rowmap phase (end - ranked): "
                   f"median {np.median(en - rkd):.2f} max {(en - rkd).max():.2f}")
+        sp = full[4608:4608 + 4 * 880].reshape(-1, 4).astype(np.int64)
+        lv = sp[:, 3] > 0
+        if lv.any():
+            sp = (sp[lv] - z) / 1e3
+            print(f"  sample CTAs ({int(lv.sum())}): start min {sp[:,0].min():.2f} max {sp[:,0].max():.2f}; past wait min "
+                  f"{sp[:,1].min():.2f} max {sp[:,1].max():.2f}; rows in (after wait) median {np.median(sp[:,2]-sp[:,1]):.2f} "
+                  f"max {(sp[:,2]-sp[:,1]).max():.2f}; end min {sp[:,3].min():.2f} median {np.median(sp[:,3]):.2f} max {sp[:,3].max():.2f}")
+            late = np.argsort(-sp[:, 3])[:5]
+            print("   latest (start, wait, rows, end):", [tuple(np.round(sp[i], 2).tolist()) for i in late])
         rk = full[1600:1607]
         if rk[0] > 0:
             names = ["centroids in", "scored", "sorted", "pushed", "runs in", "ranked", "rowmap"]

@@ -29,6 +29,15 @@ if CLUSTER:
     T.set_options(idx, T.OPT_CLUSTER_DECODE)
     T.decode_debug(qd, idx, 0.9)
     T.decode_fixed_budget(qd, idx, 300)
+q_pin = qd.cpu().pin_memory()  # zero-copy host decode (entry kernel reads q, merge writes out)
+o_pin = torch.empty_like(q_pin).pin_memory()
+T.decode_host(q_pin, idx, 0.9, o_pin)
+T.decode_host(q_pin, idx, 0.9, o_pin)
+T.set_options(idx, T.OPT_DETERMINISTIC)  # the partial merge by the last CTA
+T.decode(qd, idx, 0.9)
+T.decode_attention_only(qd * 30, idx, torch.empty_like(qd))  # reference-shift window fallback
+T.set_options(idx, 0)
+T.decode_attention_only(qd * 30, idx, torch.empty_like(qd))
 T.set_options(idx, T.OPT_WINDOWS_EXACT)
 T.decode(qd, idx, 0.9)
 T.set_options(idx, 0)
