@@ -995,6 +995,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
         a.tlog[3600 + cta] = (unsigned long long)u | ((unsigned long long)us_.j << 16) | ((unsigned long long)us_.n << 32);
         a.tlog[3800 + cta] = t_;  // after the arrival (release / poll)
+        a.tlog[5200 + cta] = (unsigned long long)(us_.hi - us_.lo);  // the CTA's tokens
       }
       if (s_merge && a.tlog && ct == 0 && u < 8) {  // debug: merge start
         unsigned long long t_;

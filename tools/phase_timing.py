@@ -180,7 +180,10 @@ for it in range(4):
                     sl = max(((rel[c] - b0) / 1e3 for c in nm), default=float('nan'))
                     md = ((rel[mc[0]] - b0) / 1e3) if mc else float('nan')
                     me = (en[mc[0]]) if mc else float('nan')
-                    print(f"     unit {uni}: {len(cs)} CTAs, slowest arrival {sl:.2f}, merger poll {md:.2f}, merger end {me:.2f}")
+                    tk = full[5200:5348]
+                    tks = [int(tk[c]) for c in nm] or [0]
+                    print(f"     unit {uni}: {len(cs)} CTAs, tokens per CTA {min(tks)}-{max(tks)} (merger {int(tk[mc[0]]) if mc else -1}), "
+                          f"slowest arrival {sl:.2f}, merger poll {md:.2f}, merger end {me:.2f}")
             mg = full[964:964 + 16].reshape(8, 2)
             print("   merges (start, end) us:", [(round((s - b0) / 1e3, 2), round((e - b0) / 1e3, 2)) for s, e in mg if s > 0])
             cp = full[980:988]
