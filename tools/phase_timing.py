@@ -184,6 +184,18 @@ for it in range(4):
                     tks = [int(tk[c]) for c in nm] or [0]
                     print(f"     unit {uni}: {len(cs)} CTAs, tokens per CTA {min(tks)}-{max(tks)} (merger {int(tk[mc[0]]) if mc else -1}), "
                           f"slowest arrival {sl:.2f}, merger poll {md:.2f}, merger end {me:.2f}")
+            nr = full[5400:5548].astype(np.int64)
+            tk = full[5200:5348].astype(np.int64)
+            if (rel > 0).any() and nr.sum() > 0:
+                arr = (rel.astype(np.int64) - b0) / 1e3
+                ok = (rel > 0) & (tk > 0)
+                c = np.corrcoef(np.vstack([arr[ok], nr[ok], tk[ok]]))
+                print(f"   per CTA: runs min {nr[ok].min()} median {int(np.median(nr[ok]))} max {nr[ok].max()}; "
+                      f"corr(arrival, runs) {c[0,1]:.2f}, corr(arrival, tokens) {c[0,2]:.2f}")
+                slow = np.argsort(-np.where(ok, arr, -1))[:6]
+                print("   slowest arrivals (cta, arrival, tokens, runs):", [(int(i), round(float(arr[i]), 2), int(tk[i]), int(nr[i])) for i in slow])
+                fastc = np.argsort(np.where(ok, arr, 1e9))[:6]
+                print("   fastest arrivals (cta, arrival, tokens, runs):", [(int(i), round(float(arr[i]), 2), int(tk[i]), int(nr[i])) for i in fastc])
             mg = full[964:964 + 16].reshape(8, 2)
             print("   merges (start, end) us:", [(round((s - b0) / 1e3, 2), round((e - b0) / 1e3, 2)) for s, e in mg if s > 0])
             cp = full[980:988]
