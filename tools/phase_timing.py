@@ -118,6 +118,10 @@ for it in range(4):
         cr = full[1730:1734]
         if cr[0] > 0:
             print("  fit mask lists, cycles per repetition:", np.diff(cr).tolist())
+        cc = full[1740:1745].astype(np.int64)
+        if cc[0] > 0:
+            print("  fit compaction (clock64 cycles, thread 0 of unit 0): loc+scan %d  w_sum sync %d  base+lists %d  padding %d"
+                  % (cc[1] - cc[0], cc[2] - cc[1], cc[3] - cc[2], cc[4] - cc[3]))
         cs = full[264:268]
         print("  compaction (us from first start): " + "  ".join(f"{nm} {(cs[i] - z) / 1e3:6.2f}" for i, nm in
               enumerate(["pass1", "scan", "pass2", "fill"]) if cs[i] > 0))
