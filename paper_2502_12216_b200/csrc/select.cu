@@ -321,9 +321,12 @@ constexpr int FITU_THREADS = 256;
 // budget or unit prefix) compiled without those paths -- the fit is a chain of single-warp
 // steps, and its code arrives cold after every other layer's traffic has passed through L2
 // (the smaller kernel runs ~1 us faster per layer-step)
-template <bool GEN>
+// MODE 0: the plain decode; 1 / 2: sharded stage 2 / stage 1 alone; 3: generic (any mode
+// with the windows-exact variant, a fixed budget or the global unit prefix)
+template <int MODE>
 __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams P) {
-  const int shard_mode = GEN ? P.shard_mode : 0;
+  constexpr bool GEN = MODE == 3;
+  const int shard_mode = GEN ? P.shard_mode : MODE;
   const int fixed_budget = GEN ? P.fixed_budget : 0;
   const bool windows_exact = GEN && P.windows_exact;
   const bool need_unit_prefix = GEN && P.need_unit_prefix;
@@ -873,12 +876,13 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
   P.en_out = x->stage;
   cudaLaunchAttribute attr[1];
   const size_t smem = fit_smem_bytes(x, P.windows_exact != 0);
-  const bool gen = P.shard_mode != 0 || P.windows_exact || P.fixed_budget > 0 || P.need_unit_prefix;
-  const void* fn = gen ? (const void*)fit_unit_kernel<true> : (const void*)fit_unit_kernel<false>;
-  cudaError_t e = ensure_smem(fn, smem);
+  const int mode = (P.windows_exact || P.fixed_budget > 0 || P.need_unit_prefix) ? 3 : P.shard_mode;
+  void (*kern)(const FitParams) = mode == 0 ? fit_unit_kernel<0> : mode == 1 ? fit_unit_kernel<1>
+                                : mode == 2 ? fit_unit_kernel<2> : fit_unit_kernel<3>;
+  cudaError_t e = ensure_smem((const void*)kern, smem);
   if (e != cudaSuccess) return e;
   auto cfg = make_cfg(dim3(x->units), dim3(FITU_THREADS), smem, s, pdl, attr);
-  return gen ? cudaLaunchKernelEx(&cfg, fit_unit_kernel<true>, P) : cudaLaunchKernelEx(&cfg, fit_unit_kernel<false>, P);
+  return cudaLaunchKernelEx(&cfg, kern, P);
 }
 
 cudaError_t launch_stage1b(const SelArgs& a, cudaStream_t s) {
