@@ -389,11 +389,15 @@ def test_c2_full_size_sampled_parity(T):
 
 # ----------------------------------------------------------------------------- attention work-split modes
 @pytest.mark.parametrize("B,H,n,C", [(12, 8, 2048, 32),    # 96 units > CTAs/2: global token split,
-                                     (64, 8, 1024, 16)])   # C3-like unit count (512 units)
+                                     (64, 8, 1024, 16),    # C3-like unit count (512 units)
+                                     (7, 10, 2048, 32),    # 70 units <= CTAs/2: unit-aligned split with
+                                     (9, 8, 4096, 64)])    # 1-3 CTAs per unit (designated merger alone)
 def test_global_split_many_units(T, B, H, n, C):
     """More units than half the CTAs (BASELINE configs[2] shape class: batch x KV heads):
     the fit kernel's last unit writes the token prefix over units and the attention
-    kernel cuts one global token list (a CTA may hold pieces of two units)."""
+    kernel cuts one global token list (a CTA may hold pieces of two units).  Just below
+    that (70 / 72 units) the unit-aligned split gives units 1-3 CTAs, so the designated
+    merger of the reference-shift merge often has no other piece to wait for."""
     G = 4
     K, V, q = _layer(B, H, G, n, 500 + B)
     cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, B)
