@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 #include <float.h>
 #include <limits.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -326,7 +327,7 @@ constexpr int FITU_THREADS = 256;
 template <int MODE>
 __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams P) {
   constexpr bool GEN = MODE == 3;
-  const int shard_mode = GEN ? P.shard_mode : MODE;
+  const int shard_mode = GEN ? P.shard_mode : (MODE == 4 ? 0 : MODE);
   const int fixed_budget = GEN ? P.fixed_budget : 0;
   const bool windows_exact = GEN && P.windows_exact;
   const bool need_unit_prefix = GEN && P.need_unit_prefix;
@@ -421,6 +422,142 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
     stamp(2);
     if (stamp_on && tid == 0) P.tlog[1709] = clock64();
   }
+  if constexpr (MODE == 4) {
+    // paired plain decode (G <= 4, C <= 1024): warp 2g computes head g's W while warp 2g + 1
+    // evaluates the first round of the J search (the probes need a, b, E_N, not W) and then
+    // finishes the selection -- the W evaluation leaves the head's critical path
+    __shared__ float s_W[8];
+    if (warp < 2 * G) {
+      const int g = warp >> 1, role = warp & 1;
+      const float* sg = sm + (size_t)g * nb * 4;
+      float mf = -INFINITY;
+      for (int b = lane; b < nb; b += 32) mf = fmaxf(mf, sg[b * 4]);
+      const float m = warp_max(mf);
+      float eh = 0.f, e1 = 0.f, e2 = 0.f;
+      for (int b = lane; b < nb; b += 32) {
+        const float4 v = *reinterpret_cast<const float4*>(sg + b * 4);
+        const float f = __expf(v.x - m);
+        eh = fmaf(v.y, f, eh);
+        e1 = fmaf(v.z, f, e1);
+        e2 = fmaf(v.w, f, e2);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        eh += __shfl_xor_sync(0xffffffffu, eh, o);
+        e1 += __shfl_xor_sync(0xffffffffu, e1, o);
+        e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+      }
+      const float EN = eh;
+      float a = 0.f, b = 0.f, mu1 = 0.f, mu2 = 0.f;
+      TailF tail = {0.f, 0.f, 1, 0};
+      if (!sc.fallback) {
+        const float W1 = (float)(2 * sc.w + 1);
+        mu1 = e1 / W1;
+        mu2 = e2 / W1;
+        const float x1 = (float)sc.x1, x2 = (float)sc.x2;
+        a = (mu1 - mu2) * (x1 * x2 / (x2 - x1));  // O8 / Alg. 1 l.4
+        b = mu1 - a / x1;
+        tail = make_tail_f(a, b, sc.N, n);
+      }
+      if (role == 0) {
+        const float W = sc.fallback ? EN : EN + tail(n);
+        if (lane == 0) s_W[g] = W;
+        asm volatile("bar.arrive %0, 64;" ::"r"(2 + g) : "memory");
+      } else {
+        const int* eg = s_end + (size_t)g * C;
+        // round 1 of the search over the cluster ends (see warp_count_false): its probes
+        const int step = (C + 31) >> 5;
+        const int idx1 = lane * step;
+        bool past = false;
+        float v1 = -INFINITY;
+        if (idx1 < C) {
+          const int e = eg[idx1];
+          past = e > sc.N;
+          if (past && !sc.fallback) v1 = EN + tail(e);
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(2 + g) : "memory");
+        const float W = s_W[g];
+        int J = C;  // p >= 1: every cluster (reading 15)
+        if (P.p < 1.0) {
+          const float target = (float)P.p * W;
+          if (EN >= target) {
+            // the crossing lies inside the exact head: the crossing block of the per-block
+            // prefix, then the slot inside it (one global round trip)
+            const int nex = sc.fallback ? n : sc.N;
+            const int nbh = (nex + SB - 1) / SB;
+            float carry = 0.f, before = 0.f;
+            int bs = nbh - 1;
+            for (int b0 = 0; b0 < nbh; b0 += 32) {
+              const int bb = b0 + lane;
+              const float vo = bb < nbh ? sg[bb * 4 + 1] * __expf(sg[bb * 4] - m) : 0.f;
+              float v = vo;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const float x = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += x;
+              }
+              const unsigned hit = __ballot_sync(0xffffffffu, bb < nbh && carry + v >= target);
+              if (hit) {
+                const int hl = __ffs(hit) - 1;
+                bs = b0 + hl;
+                before = carry + __shfl_sync(0xffffffffu, v, hl) - __shfl_sync(0xffffffffu, vo, hl);
+                break;
+              }
+              carry += __shfl_sync(0xffffffffu, v, 31);
+              before = carry;
+            }
+            const int s0 = bs * SB, s1 = min(nex, s0 + SB);
+            constexpr int PER = SB / 32;
+            float w[PER];
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+              const int s = s0 + PER * lane + k;
+              w[k] = s < s1 ? __expf(__ldcg(P.logits + (ub + g) * sc.slots + s) - m) : 0.f;
+            }
+#pragma unroll
+            for (int k = 1; k < PER; ++k) w[k] += w[k - 1];
+            float v = w[PER - 1];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const float x = __shfl_up_sync(0xffffffffu, v, o);
+              if (lane >= o) v += x;
+            }
+            const float excl = before + v - w[PER - 1];
+            int kl = PER;
+#pragma unroll
+            for (int k = PER - 1; k >= 0; --k)
+              if (s0 + PER * lane + k < s1 && excl + w[k] >= target) kl = k;
+            const unsigned hit = __ballot_sync(0xffffffffu, kl < PER);
+            const int hl = hit ? __ffs(hit) - 1 : 31;
+            const int kls = __shfl_sync(0xffffffffu, kl, hl);
+            const int kstar = hit ? s0 + PER * hl + kls + 1 : s1;
+            J = 1 + warp_count_false(C - 1, [&](int r) { return eg[r] >= kstar; });
+          } else {
+            // past the head: the first cluster end whose estimated mass reaches the target
+            const int c1 = __popc(__ballot_sync(0xffffffffu, idx1 < C && !(past && v1 >= target)));
+            const int lo = c1 > 0 ? (c1 - 1) * step + 1 : 0, hi = min(c1 * step, C);
+            const int idx = lo + lane;
+            const bool nf = idx < hi && !(eg[idx] > sc.N && EN + tail(eg[idx]) >= target);
+            const int r = lo + __popc(__ballot_sync(0xffffffffu, nf));
+            J = r < C ? r + 1 : C;
+          }
+        }
+        if (lane == 0) {
+          s_J[g] = J;
+          P.J[ub + g] = J;
+          double* f = P.fit + (ub + g) * 6;
+          f[0] = a; f[1] = b; f[2] = m; f[3] = W; f[4] = mu1; f[5] = mu2;
+          P.mref[ub + g] = m * 1.4426950408889634f;
+        }
+        const int* ord = s_ord + (size_t)g * C;
+        __syncwarp();
+        for (int r = lane; r < J; r += 32) {
+          const int cid = ord[r];
+          if (s_off[cid + 1] > s_off[cid]) mask[cid] = 1;
+        }
+      }
+    }
+  } else {
   if (warp < G && shard_mode == 1) {
     // sharded stage 2 (reading 23): theta* = the largest grid point theta_t whose
     // all-reduced mass reaches p W (none: every cluster); the head selects the rank prefix
@@ -609,6 +746,7 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
       }
     }
     wstamp(4);
+  }
   }
   __syncthreads();
   stamp(3);
@@ -876,9 +1014,12 @@ cudaError_t launch_fit(const SelArgs& a, cudaStream_t s, bool pdl) {
   P.en_out = x->stage;
   cudaLaunchAttribute attr[1];
   const size_t smem = fit_smem_bytes(x, P.windows_exact != 0);
-  const int mode = (P.windows_exact || P.fixed_budget > 0 || P.need_unit_prefix) ? 3 : P.shard_mode;
+  int mode = (P.windows_exact || P.fixed_budget > 0 || P.need_unit_prefix) ? 3 : P.shard_mode;
+  static const bool no_pair = getenv("TACTIC_FIT_UNPAIRED") != nullptr;
+  if (mode == 0 && x->G <= 4 && x->C <= 1024 && !no_pair) mode = 4;  // paired W / search warps
   void (*kern)(const FitParams) = mode == 0 ? fit_unit_kernel<0> : mode == 1 ? fit_unit_kernel<1>
-                                : mode == 2 ? fit_unit_kernel<2> : fit_unit_kernel<3>;
+                                : mode == 2 ? fit_unit_kernel<2> : mode == 3 ? fit_unit_kernel<3>
+                                : fit_unit_kernel<4>;
   cudaError_t e = ensure_smem((const void*)kern, smem);
   if (e != cudaSuccess) return e;
   auto cfg = make_cfg(dim3(x->units), dim3(FITU_THREADS), smem, s, pdl, attr);
