@@ -762,8 +762,24 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
     const int per = (C + nt - 1) / nt;
     const int j0 = tid * per, j1 = min(C, j0 + per);
     unsigned long long loc = 0;
-    for (int j = j0; j < j1; ++j)
-      if (mask[j]) loc += ((unsigned long long)(s_off[j + 1] - s_off[j]) << 20) | 1ull;
+    // four clusters per thread (C = 4 x threads): the thread's mask bytes and offsets as
+    // one 32-bit and one 16-byte load, kept in registers for the second pass
+    const bool quad = per == 4 && j1 - j0 == 4 && (C & 3) == 0;
+    uint32_t q_mk = 0;
+    int4 q_off = make_int4(0, 0, 0, 0);
+    int q_end = 0;
+    if (quad) {
+      q_mk = *reinterpret_cast<const uint32_t*>(mask + j0);
+      q_off = *reinterpret_cast<const int4*>(s_off + j0);
+      q_end = s_off[j0 + 4];
+      const int o[5] = {q_off.x, q_off.y, q_off.z, q_off.w, q_end};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((q_mk >> (8 * k)) & 0xFFu) loc += ((unsigned long long)(o[k + 1] - o[k]) << 20) | 1ull;
+    } else {
+      for (int j = j0; j < j1; ++j)
+        if (mask[j]) loc += ((unsigned long long)(s_off[j + 1] - s_off[j]) << 20) | 1ull;
+    }
     unsigned long long incl = loc;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -782,14 +798,27 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
     int* ul = P.ulist + (size_t)u * C;
     int* up = P.uprefix + (size_t)u * (C + 1);
     uint8_t* um = P.umask + (size_t)u * C;
-    for (int j = j0; j < j1; ++j) {
-      const uint8_t mk = mask[j];
-      um[j] = mk;
-      if (mk) {
-        ul[cb] = s_off[j];
-        up[cb] = tb;
-        ++cb;
-        tb += s_off[j + 1] - s_off[j];
+    if (quad) {
+      *reinterpret_cast<uint32_t*>(um + j0) = q_mk;
+      const int o[5] = {q_off.x, q_off.y, q_off.z, q_off.w, q_end};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((q_mk >> (8 * k)) & 0xFFu) {
+          ul[cb] = o[k];
+          up[cb] = tb;
+          ++cb;
+          tb += o[k + 1] - o[k];
+        }
+    } else {
+      for (int j = j0; j < j1; ++j) {
+        const uint8_t mk = mask[j];
+        um[j] = mk;
+        if (mk) {
+          ul[cb] = s_off[j];
+          up[cb] = tb;
+          ++cb;
+          tb += s_off[j + 1] - s_off[j];
+        }
       }
     }
     // entries past the union: total tokens (keeps the prefix monotone for searches)
