@@ -788,12 +788,16 @@ __global__ void __launch_bounds__(FITU_THREADS) fit_unit_kernel(const FitParams 
     }
     if (lane == 31) w_sum[warp] = incl;
     __syncthreads();
-    unsigned long long base = incl - loc, tot = 0;
-    for (int w = 0; w < nw; ++w) {
-      const unsigned long long v = w_sum[w];
-      if (w < warp) base += v;
-      tot += v;
+    // the warp totals: lane w holds warp w's, one shuffle scan gives this warp's base
+    const unsigned long long ws = lane < nw ? w_sum[lane] : 0ull;
+    unsigned long long wi = ws;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long x = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += x;
     }
+    const unsigned long long base = incl - loc + __shfl_sync(0xffffffffu, wi - ws, warp);
+    const unsigned long long tot = __shfl_sync(0xffffffffu, wi, 31);
     int cb = (int)(base & 0xFFFFFull), tb = (int)(base >> 20);
     int* ul = P.ulist + (size_t)u * C;
     int* up = P.uprefix + (size_t)u * (C + 1);
