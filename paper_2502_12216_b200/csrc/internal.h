@@ -276,6 +276,7 @@ struct KmArgs {
   int* col_tot;                    // [units][C] cluster sizes (km_scan -> km_scatter)
   int* changed;                    // [units]
   int* converged;                  // [units]
+  double* acc;                     // nullable [units][C][128]: B3 member sums (zero between uses)
 };
 cudaError_t km_init_centroids(const KmArgs& a, const int* init_dev, cudaStream_t s);
 // tmK: 4-D map of the caller's K ([B][Hkv][n][128], box 64 dims x 128 rows, SWIZZLE_128B)

@@ -508,6 +508,100 @@ __global__ void __launch_bounds__(256) km_update_kernel(const KmArgs a, int iter
   }
 }
 
+// B3 as a streaming pass (a.acc): the member rows in cluster order (perm), each warp over 128
+// consecutive positions with 8 rows in flight (a half-warp per row, 16 bytes per lane), the
+// running sum of the current cluster in registers and flushed with fp64 reductions at every
+// cluster boundary; km_update_fin_kernel divides by the sizes.  The fp64 sums of bf16 rows
+// are exact (8-bit mantissas, < 2^17 terms over a bounded exponent range), so the order of
+// the reductions does not change the means.
+__global__ void __launch_bounds__(256) km_update_seg_kernel(const KmArgs a, int iter) {
+  const int u = blockIdx.y;
+  if (km_skip(a, u, iter)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = lane >> 4, l16 = lane & 15;
+  const int p_begin = (blockIdx.x * 8 + warp) * 128;
+  if (p_begin >= a.n) return;
+  const int p_end = min(a.n, p_begin + 128);
+  const int* perm = a.perm + (size_t)u * a.n;
+  const int* asg = a.assign + (size_t)u * a.n;
+  const __nv_bfloat16* Ku = krow(a.K, a.sb, a.sh, a.sn, a.Hkv, u, 0) + l16 * 8;
+  double* accu = a.acc + (size_t)u * a.C * 128 + l16 * 8;
+  double sacc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sacc[i] = 0.0;
+  int cur = -1;  // the cluster being summed (warp-uniform)
+  auto flush = [&]() {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      sacc[i] += __shfl_xor_sync(0xffffffffu, sacc[i], 16);
+      if (half == 0) atomicAdd(accu + (size_t)cur * 128 + i, sacc[i]);
+      sacc[i] = 0.0;
+    }
+  };
+  auto add = [&](const uint4& raw) {
+    const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(k2[i]);
+      sacc[2 * i] += f.x;
+      sacc[2 * i + 1] += f.y;
+    }
+  };
+  for (int p0 = p_begin; p0 < p_end; p0 += 8) {
+    uint4 raw[4];
+    int cj[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int p = p0 + 2 * q + half;
+      const bool ok = p < p_end;
+      const int key = ok ? __ldg(perm + p) : 0;
+      cj[q] = ok ? __ldg(asg + key) : -1;
+      raw[q] = ok ? __ldg(reinterpret_cast<const uint4*>(Ku + (long long)key * a.sn)) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c0 = __shfl_sync(0xffffffffu, cj[q], 0), c1 = __shfl_sync(0xffffffffu, cj[q], 16);
+      if (c0 < 0) continue;  // past the warp's positions
+      if (cur < 0) cur = c0;
+      if (c0 != cur) {  // both rows start a later cluster
+        flush();
+        cur = c0;
+      }
+      if (c1 >= 0 && c1 != cur) {  // the half-0 row ends cluster cur, the half-1 row starts c1
+        if (half == 0) add(raw[q]);
+        flush();
+        cur = c1;
+        if (half == 1) add(raw[q]);
+      } else if (half == 0 || c1 >= 0) {
+        add(raw[q]);
+      }
+    }
+  }
+  if (cur >= 0) flush();
+}
+
+// means from the streamed sums: one warp per cluster (lane: dims 4 lane .. 4 lane + 3); an
+// empty cluster keeps its centroid; the sums are zeroed for the next iteration
+__global__ void __launch_bounds__(256) km_update_fin_kernel(const KmArgs a, int iter) {
+  const int u = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (km_skip(a, u, iter)) return;
+  const int j = blockIdx.x * 8 + warp;
+  if (j >= a.C) return;
+  const int* off = a.offsets + (size_t)u * (a.C + 1);
+  const int sz = off[j + 1] - off[j];
+  double* acc = a.acc + ((size_t)u * a.C + j) * 128 + lane * 4;
+  if (sz <= 0) {
+    const float4 c = *reinterpret_cast<const float4*>(a.cent + ((size_t)u * a.C + j) * 128 + lane * 4);
+    store_centroid(a, u, j, c);
+    return;
+  }
+  const double2 s01 = *reinterpret_cast<const double2*>(acc), s23 = *reinterpret_cast<const double2*>(acc + 2);
+  *reinterpret_cast<double2*>(acc) = make_double2(0.0, 0.0);
+  *reinterpret_cast<double2*>(acc + 2) = make_double2(0.0, 0.0);
+  const double inv = (double)sz;
+  store_centroid(a, u, j, make_float4((float)(s01.x / inv), (float)(s01.y / inv), (float)(s23.x / inv),
+                                      (float)(s23.y / inv)));
+}
+
 // ---------------------------------------------------------------- B5 / B6
 __global__ void km_relayout_kernel(const KmArgs a) {
   const int u = blockIdx.y;
@@ -665,6 +759,11 @@ cudaError_t km_count_scan_scatter(const KmArgs& a, int iter, cudaStream_t s) {
 }
 
 cudaError_t km_update(const KmArgs& a, int iter, cudaStream_t s) {
+  if (a.acc) {  // streaming pass over the member rows + means (16-byte row slices)
+    km_update_seg_kernel<<<dim3((a.n + 1023) / 1024, a.units), 256, 0, s>>>(a, iter);
+    km_update_fin_kernel<<<dim3((a.C + 7) / 8, a.units), 256, 0, s>>>(a, iter);
+    return cudaGetLastError();
+  }
   km_update_kernel<<<dim3(a.C, a.units), 256, 0, s>>>(a, iter);
   return cudaGetLastError();
 }

@@ -434,6 +434,12 @@ static tactic_status_t build_common(const void* K, const void* V, const tactic_k
   if ((e = cudaMallocAsync((void**)&a.converged, (size_t)units * 4, s))) return bail(cuda_fail(e, "scratch"));
   if ((e = cudaMallocAsync((void**)&d_init, (size_t)units * C * 4, s))) return bail(cuda_fail(e, "scratch"));
   if ((e = cudaMallocAsync((void**)&d_flag, 4, s))) return bail(cuda_fail(e, "scratch"));
+  a.acc = nullptr;  // streamed B3 sums: 16-byte row slices, up to 64 MB of fp64 sums
+  if (build && r.sn % 8 == 0 && r.sb % 8 == 0 && r.sh % 8 == 0 && ((uintptr_t)K & 15) == 0 &&
+      (size_t)units * C * 128 * 8 <= (64u << 20) && !getenv_flag("TACTIC_KM_UPDATE_PER_CLUSTER")) {
+    if ((e = cudaMallocAsync((void**)&a.acc, (size_t)units * C * 128 * 8, s))) return bail(cuda_fail(e, "scratch"));
+    cudaMemsetAsync(a.acc, 0, (size_t)units * C * 128 * 8, s);
+  }
   if (cudaEventCreate(&x->ev_build[0]) != cudaSuccess || cudaEventCreate(&x->ev_build[1]) != cudaSuccess) {
     cudaGetLastError();  // timing only: the build goes on without it
     for (cudaEvent_t& ev : x->ev_build)
@@ -451,6 +457,7 @@ static tactic_status_t build_common(const void* K, const void* V, const tactic_k
     cudaFreeAsync(a.converged, s);
     cudaFreeAsync(d_init, s);
     cudaFreeAsync(d_flag, s);
+    if (a.acc) cudaFreeAsync(a.acc, s);
   };
 #define CKB(expr)                                           \
   do {                                                      \
