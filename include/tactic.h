@@ -179,7 +179,9 @@ void tactic_index_destroy(tactic_index_t idx);
  *  estimated total (Alg. 1 l.10, cluster granularity reading 14; p >= 1 selects
  *  every cluster, reading 15),  S7 union over the G heads turned into a balanced
  *  token work list over all units (sub-requests),  S8 split-KV flash-decode
- *  of every head over the union (reading 17),  S9 log-sum-exp merge.
+ *  of every head over the union (reading 17),  S9 log-sum-exp merge (by default every
+ *  piece's share is expressed against the fit's sampled maximum logit and added into fp32
+ *  accumulators -- see TACTIC_OPT_DETERMINISTIC for the bit-reproducible piece-order merge).
  * Execution: a chain of kernels (score/rank, sample, fit, attention; the later ones
  * overlap their prologues with programmatic dependent launch).  With
  * TACTIC_OPT_CLUSTER_DECODE (and G in {1,2,4,8}, C <= 2048, C x G <= 4096, default
