@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   UnitSplit us_ = {0, 0, 1, 0, 0, 0};
   if (unit_mode) {
     const bool s32 = a.units <= 32 && (long long)(a.n + a.tail_len) * a.units * P < (1LL << 31);
-    us_ = s32 ? unit_split_fast<DENSE>(a, cta, P, !DENSE && a.mref != nullptr)
+    us_ = s32 ? unit_split_fast<DENSE>(a, cta, P, !DENSE && a.mref != nullptr && a.dm_ok)
               : unit_split_of<DENSE>(a, cta, P, pref_src);
   }
   if (all_lists) {

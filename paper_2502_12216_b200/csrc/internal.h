@@ -172,6 +172,10 @@ struct AttnArgs {
   // per-head loading ablation (NEXT 2): work-list units are (unit, head) pairs with G = 1,
   // reading the K/V of unit u / kv_div (0 or 1: units are KV units)
   int kv_div;
+  // the designated-merger protocol (a unit's CTA 0 polls for the others' arrivals) only when
+  // the whole grid fits on the device at once (num_ctas <= SMs), so a polling CTA never
+  // holds an SM that one of the CTAs it waits for needs
+  int dm_ok;
 };
 cudaError_t launch_attention_sparse(const AttnArgs& a, int G, int num_ctas, cudaStream_t s, bool pdl);
 cudaError_t launch_attention_dense(const AttnArgs& a, const CUtensorMap* tmK, const CUtensorMap* tmV, int G,

@@ -866,6 +866,7 @@ static tactic_status_t run_attention(const void* q, tactic_index_t idx, bool all
     aa.mref = idx->mref;
     aa.acc = idx->acc;
     aa.acc_flag = idx->acc_flag;
+    aa.dm_ok = idx->num_ctas <= idx->num_sms ? 1 : 0;
   }
   CK(launch_attention_sparse(aa, idx->G, idx->num_ctas, s, ev_mid == nullptr && !entry));  // S8 + fused S9
   if (ev_mid) CK(cudaEventRecord(ev_mid, s));

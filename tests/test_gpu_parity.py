@@ -726,3 +726,22 @@ def test_reference_shift_merge_window_and_fallback(T, sel_scale, att_scale):
     T.decode_attention_only(dev_bf16(q_att), index, out2)
     torch.cuda.synchronize()
     assert_output_close(out2.float().cpu().numpy(), got, "deterministic vs reference-shift merge")
+
+
+@pytest.mark.parametrize("num_ctas", [64, 300])
+def test_reference_shift_merge_protocols(T, num_ctas):
+    """The reference-shift merge with the designated merger (grid fits the device: 64 CTAs)
+    and with the last-arriver atomic (300 CTAs > SMs: a polling CTA could hold an SM that a
+    CTA it waits for needs, so the library falls back): both match the oracle and each
+    other."""
+    B, H, G, n, C = 1, 8, 4, 16384, 128
+    K, V, q = _layer(B, H, G, n, 77)
+    cents, asg, idxs = oracle_layer_clustering(K, V, C, 3, 77)
+    index = _import(T, K, V, cents, asg, G, num_ctas=num_ctas)
+    res = T.decode_debug(dev_bf16(q), index, 0.9)
+    got = res["out"].float().cpu().numpy()
+    for u in (0, 3, 7):
+        qo = q[0, u * G:(u + 1) * G]
+        toks = O.cluster_tokens(idxs[u], np.nonzero(res["union_mask"][u])[0])
+        o, _ = O.sparse_attention(qo, idxs[u].K, idxs[u].V, toks)
+        assert_output_close(got[0, u * G:(u + 1) * G], o, f"num_ctas={num_ctas} u={u}")
